@@ -1,0 +1,416 @@
+"""Host-side setup of one run: everything the fused GPU kernels consume.
+
+This restates the constructor of the reference solver
+(``FdtdSolver.__init__``, ``mblight/solver_fdtd.py:207-326``) minus the time
+loop: grid sizing (``init_fdtd_simulation``, ``solver_fdtd.py:80-102``),
+per-material update coefficients (``get_fdtd_constants``,
+``solver_fdtd.py:122-133``), the cell -> region map (``solver_fdtd.py:242-272``),
+quantum groups and their stepper constants (``_kernels.py:351-374,
+431-439, 467-500``), sources, record plans (``solver_fdtd.py:136-172``) and
+the boundary constants (``solver_fdtd.py:310-325``).
+
+Where the reference stores per-cell coefficient arrays (32 B/cell read
+every step), the plan keeps a *region table*: region r covers E cells
+[e_start[r], e_start[r+1]) and H nodes [h_start[r], h_start[r+1]); the
+kernels look coefficients up by region, so no coefficient bytes cross HBM.
+The tables are derived from the very same ``searchsorted`` maps the
+reference builds, so the per-cell values are identical.
+
+The plan only reads attributes of the device/scenario objects, so both this
+package's setup model and the reference ``mblight`` objects work.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .constants import HBAR
+from .errors import ValidationError
+from .qm import precompute_relaxation_propagator
+from .setup_model import DEFAULT_SEED, scenario_validate
+
+COURANT_NUMBER = 0.5
+NONFINITE_CHECK_EVERY = 1024  # solver_fdtd.py:50
+QUANTITY_CODES = {"e": 0, "h": 1, "d": 2, "inv": 3}
+STEPPERS = ("splitting", "rk4")
+
+
+@dataclass(frozen=True)
+class GridLayout:
+    """Spatio-temporal discretisation (field names of ``solver_fdtd.py:69-77``)."""
+
+    num_x: int
+    dx: float
+    num_t: int
+    dt: float
+    courant: float = COURANT_NUMBER
+
+
+def init_fdtd_simulation(device, scenario) -> GridLayout:
+    """dx = L/(Nx-1); dt from Courant 0.5 at the fastest material, shrunk so an
+    integer number of steps lands on the end time (``solver_fdtd.py:80-102``)."""
+    nx = scenario.num_gridpoints
+    if nx == 1:
+        if scenario.num_timesteps is None or scenario.num_timesteps < 2:
+            raise ValueError("scenarios with a single grid point must specify num_timesteps")
+        nt = int(scenario.num_timesteps)
+        return GridLayout(1, 0.0, nt, scenario.end_time / (nt - 1))
+    c_max = max(m.light_speed for m in device.materials())
+    dx = device.length / (nx - 1)
+    dt0 = COURANT_NUMBER * dx / c_max
+    nt = int(math.ceil(scenario.end_time / dt0)) + 1
+    return GridLayout(nx, dx, nt, scenario.end_time / (nt - 1))
+
+
+@dataclass(frozen=True)
+class CellCoefficients:
+    a_prime: float
+    b_prime: float
+    c_prime: float
+    gamma: float
+    inv_dx: float
+    qm: object = None
+
+
+def get_fdtd_constants(material, dt: float, dx: float) -> CellCoefficients:
+    """Lossy-Yee coefficients a', b', c' of one material (``solver_fdtd.py:122-133``)."""
+    if not (dt > 0 and dx > 0):
+        raise ValueError("dt and dx must be positive")
+    eps = material.permittivity
+    loss = dt * material.conductivity / (2.0 * eps)
+    return CellCoefficients(
+        (1.0 - loss) / (1.0 + loss),
+        (dt / eps) / (1.0 + loss),
+        dt / (dx * material.permeability),
+        material.overlap_factor,
+        1.0 / dx,
+        material.qm,
+    )
+
+
+def resolve_threads(explicit, num_x: int) -> int:
+    """Host worker count, kept for API parity (``solver_fdtd.py:184-195``)."""
+    if explicit is not None:
+        n = int(explicit)
+    else:
+        env = os.environ.get("MBLIGHT_THREADS", "").strip()
+        n = int(env) if env else (os.cpu_count() or 1)
+    if n < 1:
+        raise ValueError("worker count must be at least 1")
+    return min(n, num_x)
+
+
+class RecordPlan:
+    """Sampling schedule of one record (``solver_fdtd.py:136-172``)."""
+
+    def __init__(self, record, grid: GridLayout):
+        self.record = record
+        if record.interval > 0:
+            self.every = max(1, int(math.floor(record.interval / grid.dt + 0.5)))
+        else:
+            self.every = 1
+        self.rows = (grid.num_t - 1) // self.every + 1
+        half = 0.5 * grid.dx if record.quantity == "h" else 0.0
+        if record.position is None:
+            self.cell = None
+            self.cols = grid.num_x
+            self.x0 = -half
+        else:
+            self.cell = 0 if grid.num_x == 1 else int(math.floor(record.position / grid.dx + 0.5))
+            self.cols = 1
+            self.x0 = self.cell * grid.dx
+            if half:
+                self.x0 -= half
+        self.quantity = QUANTITY_CODES[record.quantity]
+        self.i = record.i - 1 if record.quantity == "d" else 0
+        self.j = record.j - 1 if record.quantity == "d" else 0
+        self.is_complex = bool(record.is_complex)
+
+    def to_result(self, grid: GridLayout, data: np.ndarray, result_cls):
+        return result_cls(
+            name=self.record.name,
+            data=data,
+            t0=0.0,
+            dt_sample=self.every * grid.dt,
+            x0=self.x0,
+            dx=grid.dx if self.cols > 1 else 0.0,
+        )
+
+
+def state_words(levels: int, stepper: str = "splitting") -> int:
+    """fp64 planes per quantum cell: Bloch (x, y, z) for two-level splitting,
+    Hermitian-packed N^2 otherwise (N real diagonal planes, then re/im planes of
+    the upper triangle in row-major i<j order)."""
+    if levels == 0:
+        return 0
+    if levels == 2 and stepper == "splitting":
+        return 3
+    return levels * levels
+
+
+def upper_pairs_rowmajor(n: int) -> list[tuple[int, int]]:
+    return [(i, j) for i in range(n) for j in range(i + 1, n)]
+
+
+def pack_density(rho: np.ndarray, stepper: str = "splitting") -> np.ndarray:
+    """Density matrix -> per-cell state vector in the kernels' plane order."""
+    rho = np.asarray(rho, dtype=complex)
+    n = rho.shape[0]
+    if n == 2 and stepper == "splitting":
+        # Bloch vector (_kernels.py:496-500)
+        return np.array([2.0 * rho[0, 1].real, -2.0 * rho[0, 1].imag, (rho[0, 0] - rho[1, 1]).real])
+    out = [rho[i, i].real for i in range(n)]
+    for i, j in upper_pairs_rowmajor(n):
+        out.extend((rho[i, j].real, rho[i, j].imag))
+    return np.array(out, dtype=float)
+
+
+def unpack_density(words: np.ndarray, n: int, stepper: str = "splitting") -> np.ndarray:
+    """Inverse of :func:`pack_density` on a (words, cells) array -> (cells, n, n).
+
+    The two-level Bloch form maps back with the accessor formulas of
+    ``_kernels.py:530-536``.
+    """
+    words = np.asarray(words, dtype=float)
+    cells = words.shape[1]
+    rho = np.zeros((cells, n, n), dtype=complex)
+    if n == 2 and stepper == "splitting":
+        x, y, z = words
+        rho[:, 0, 0] = 0.5 * (1.0 + z)
+        rho[:, 1, 1] = 0.5 * (1.0 - z)
+        rho[:, 0, 1] = 0.5 * (x - 1j * y)
+        rho[:, 1, 0] = 0.5 * (x + 1j * y)
+        return rho
+    for i in range(n):
+        rho[:, i, i] = words[i]
+    for p, (i, j) in enumerate(upper_pairs_rowmajor(n)):
+        v = words[n + 2 * p] + 1j * words[n + 2 * p + 1]
+        rho[:, i, j] = v
+        rho[:, j, i] = np.conj(v)
+    return rho
+
+
+@dataclass
+class QmConstants:
+    """Stepper constants of one quantum material (host precompute, uploaded once)."""
+
+    levels: int
+    pol_factor: float
+    # dipole entries driving the polarisation (_kernels.py:360-374)
+    pol_i: np.ndarray
+    pol_j: np.ndarray
+    pol_v: np.ndarray
+    pol_di: np.ndarray
+    pol_dv: np.ndarray
+    # Bloch form, N == 2 splitting (_kernels.py:472-494)
+    bloch: dict | None = None
+    # dense splitting, N >= 3 (_kernels.py:433-439)
+    pop_half: np.ndarray | None = None
+    coh_half: np.ndarray | None = None
+    b_const: np.ndarray | None = None
+    b_field: np.ndarray | None = None
+    # RK4 (_kernels.py:554-557)
+    h0: np.ndarray | None = None
+    mu: np.ndarray | None = None
+    pop_matrix: np.ndarray | None = None
+    deph_matrix: np.ndarray | None = None
+
+
+def qm_constants(desc, dt: float, stepper: str) -> QmConstants:
+    n = desc.dim
+    mu = desc.dipole_op.matrix()
+    upper = [(i, j, mu[i, j]) for i in range(n) for j in range(i + 1, n) if mu[i, j] != 0]
+    diag = [(i, mu[i, i].real) for i in range(n) if mu[i, i] != 0]
+    qc = QmConstants(
+        levels=n,
+        pol_factor=desc.density_3d / dt,
+        pol_i=np.array([u[0] for u in upper], dtype=np.int32),
+        pol_j=np.array([u[1] for u in upper], dtype=np.int32),
+        pol_v=np.array([u[2] for u in upper], dtype=np.complex128),
+        pol_di=np.array([d[0] for d in diag], dtype=np.int32),
+        pol_dv=np.array([d[1] for d in diag], dtype=np.float64),
+    )
+    h0 = desc.hamiltonian.matrix()
+    a = 0.5 * dt / HBAR
+    if stepper == "rk4":
+        qc.h0 = h0
+        qc.mu = mu
+        qc.pop_matrix = np.asarray(desc.dissipator.pop_matrix, dtype=float)
+        qc.deph_matrix = np.asarray(desc.dissipator.dephasing_matrix, dtype=float)
+        return qc
+    ws = precompute_relaxation_propagator(desc, dt)
+    if n == 2:
+        pop = ws.pop_half
+        # identical expression order to BlochSplittingKernel.__init__
+        qc.bloch = dict(
+            kz=0.5 * (pop[0, 0] - pop[1, 0] - pop[0, 1] + pop[1, 1]),
+            cz=0.5 * (pop[0, 0] - pop[1, 0] + pop[0, 1] - pop[1, 1]),
+            fxy=ws.coh_half[0, 1],
+            ax_c=a * h0[0, 1].real, ax_s=-a * mu[0, 1].real,
+            ay_c=-a * h0[0, 1].imag, ay_s=a * mu[0, 1].imag,
+            az_c=0.5 * a * (h0[0, 0].real - h0[1, 1].real),
+            az_s=-0.5 * a * (mu[0, 0].real - mu[1, 1].real),
+            a0_c=0.5 * a * (h0[0, 0].real + h0[1, 1].real),
+            a0_s=-0.5 * a * (mu[0, 0].real + mu[1, 1].real),
+            mu_x=mu[0, 1].real, mu_y=-mu[0, 1].imag,
+            mu_z=0.5 * (mu[0, 0].real - mu[1, 1].real),
+        )
+    else:
+        qc.pop_half = ws.pop_half
+        qc.coh_half = ws.coh_half
+        qc.b_const = np.eye(n, dtype=complex) + 1j * a * h0
+        qc.b_field = -1j * a * mu
+    return qc
+
+
+@dataclass
+class RegionTable:
+    e_start: np.ndarray  # int64[R]: first E cell of region r
+    h_start: np.ndarray  # int64[R]: first H node (1..Nx-1) of region r
+    coef_a: np.ndarray
+    coef_bg: np.ndarray
+    coef_bdx: np.ndarray
+    coef_ch: np.ndarray
+    qm_index: np.ndarray  # int32[R]; -1 = classical material
+
+    def per_cell(self, num_x: int) -> dict:
+        """Expand to the reference's per-cell arrays (tests / oracle)."""
+        e_reg = np.searchsorted(self.e_start, np.arange(num_x), side="right") - 1
+        out = dict(
+            coef_a=self.coef_a[e_reg], coef_bg=self.coef_bg[e_reg],
+            coef_bdx=self.coef_bdx[e_reg], cell_region=e_reg,
+        )
+        ch = np.zeros(num_x + 1)
+        if num_x > 1:
+            m = np.arange(1, num_x)
+            h_reg = np.searchsorted(self.h_start, m, side="right") - 1
+            ch[1:num_x] = self.coef_ch[h_reg]
+        out["coef_ch"] = ch
+        return out
+
+
+@dataclass
+class SolverPlan:
+    grid: GridLayout
+    seed: int
+    stepper: str
+    levels: int  # N of the quantum materials, 0 if none
+    e_init: np.ndarray
+    h_init: np.ndarray  # num_x + 1 entries, last is 0
+    regions: RegionTable
+    qm: list
+    groups: list  # (start, stop, qm_index)
+    rho_init: np.ndarray  # complex N x N (or None)
+    src_cells: np.ndarray
+    src_hard: np.ndarray
+    src_values: np.ndarray  # [num_t, n_src], row n = value at t = n dt
+    plans: list
+    boundary: tuple  # ((w, c dt/dx, Z) left, (...) right) or None
+    materials: list = field(default_factory=list)
+
+    @property
+    def state_words(self) -> int:
+        return state_words(self.levels, self.stepper)
+
+    def rho_init_packed(self) -> np.ndarray:
+        if self.levels == 0:
+            return np.zeros(0)
+        return pack_density(self.rho_init, self.stepper)
+
+
+def build_plan(device, scenario, stepper: str = "splitting", seed=None) -> SolverPlan:
+    """Validate and precompute a run (``FdtdSolver.__init__`` minus state arrays)."""
+    problems = scenario_validate(device, scenario)
+    if problems:
+        raise ValidationError(problems)
+    if stepper not in STEPPERS:
+        raise ValueError(f"unknown stepper {stepper!r}")
+    grid = init_fdtd_simulation(device, scenario)
+    seed = DEFAULT_SEED if seed is None else int(seed)
+    nx, dt, dx = grid.num_x, grid.dt, grid.dx
+
+    e_init = np.ascontiguousarray(scenario.ic_e_field.build(nx, seed), dtype=float)
+    h_init = np.zeros(nx + 1)
+    h_init[0:nx] = scenario.ic_h_field.build(nx, seed + 1)
+
+    lib = {m.id: m for m in device.materials()}
+    mats = [lib[r.material_id] for r in device.regions]
+    n_reg = len(device.regions)
+    ends = np.array([r.x_end for r in device.regions])
+    if nx > 1:
+        cell_region = np.minimum(np.searchsorted(ends, np.arange(nx) * dx, side="right"), n_reg - 1)
+        x_h = (np.arange(1, nx) - 0.5) * dx
+        h_region = np.minimum(np.searchsorted(ends, x_h, side="right"), n_reg - 1)
+        coeffs = [get_fdtd_constants(m, dt, dx) for m in mats]
+    else:
+        cell_region = np.zeros(1, dtype=np.int64)
+        h_region = np.zeros(0, dtype=np.int64)
+        coeffs = [CellCoefficients(1.0, 0.0, 0.0, m.overlap_factor, 0.0, m.qm) for m in mats]
+
+    # quantum materials (one constant set per distinct qm material)
+    qm_ids: list[str] = []
+    qm_list: list[QmConstants] = []
+    qm_index = np.full(n_reg, -1, dtype=np.int32)
+    for r, m in enumerate(mats):
+        if m.qm is None:
+            continue
+        if m.id not in qm_ids:
+            qm_ids.append(m.id)
+            qm_list.append(qm_constants(m.qm, dt, stepper))
+        qm_index[r] = qm_ids.index(m.id)
+    levels = qm_list[0].levels if qm_list else 0
+
+    regions = RegionTable(
+        e_start=np.searchsorted(cell_region, np.arange(n_reg), side="left").astype(np.int64),
+        h_start=(np.searchsorted(h_region, np.arange(n_reg), side="left") + 1).astype(np.int64),
+        coef_a=np.array([c.a_prime for c in coeffs]),
+        coef_bg=np.array([c.b_prime * c.gamma for c in coeffs]),
+        coef_bdx=np.array([c.b_prime * c.inv_dx for c in coeffs]),
+        coef_ch=np.array([c.c_prime for c in coeffs]),
+        qm_index=qm_index,
+    )
+
+    groups = []
+    start = 0
+    for m in range(1, nx + 1):
+        if m == nx or cell_region[m] != cell_region[m - 1]:
+            r = int(cell_region[start])
+            if qm_index[r] >= 0:
+                groups.append((start, m, int(qm_index[r])))
+            start = m
+
+    srcs = list(scenario.sources)
+    cells = [0 if nx == 1 else int(math.floor(s.position / dx + 0.5)) for s in srcs]
+    values = np.zeros((grid.num_t, len(srcs)))
+    for k, s in enumerate(srcs):
+        col = values[:, k]
+        for n in range(1, grid.num_t):
+            col[n] = s.value(n * dt)
+
+    plans = [RecordPlan(rec, grid) for rec in scenario.records]
+    names = [p.record.name for p in plans]
+    if len(set(names)) != len(names):
+        raise ValueError("record names must be unique")
+
+    boundary = None
+    if nx > 1:
+        left, right = mats[int(cell_region[0])], mats[int(cell_region[-1])]
+        boundary = (
+            (1.0 - math.sqrt(device.bc_left.reflectivity), left.light_speed * dt / dx,
+             math.sqrt(left.permeability / left.permittivity)),
+            (1.0 - math.sqrt(device.bc_right.reflectivity), right.light_speed * dt / dx,
+             math.sqrt(right.permeability / right.permittivity)),
+        )
+
+    rho0 = np.asarray(scenario.rho_init.matrix(), dtype=complex) if levels else None
+    return SolverPlan(
+        grid=grid, seed=seed, stepper=stepper, levels=levels, e_init=e_init, h_init=h_init,
+        regions=regions, qm=qm_list, groups=groups, rho_init=rho0,
+        src_cells=np.array(cells, dtype=np.int64),
+        src_hard=np.array([1 if s.kind == "hard" else 0 for s in srcs], dtype=np.int32),
+        src_values=values, plans=plans, boundary=boundary, materials=mats,
+    )
