@@ -1,0 +1,146 @@
+/*
+ * mbgpu.h -- C ABI of the B200 time-stepping core (libmbgpu.so).
+ *
+ * The reference has no FFI: its hot loop is FdtdSolver.run()
+ * (/root/reference/pkg/src/mblight/solver_fdtd.py:444-498) calling numba
+ * loops per step.  This ABI is the seam a Python (ctypes) or any other host
+ * binds to replace that loop; the setup arithmetic stays in the host
+ * (paper_2005_05412_b200/plan.py restates FdtdSolver.__init__,
+ * solver_fdtd.py:207-326) and is passed here as plain arrays.
+ *
+ * Entry point -> reference interface it replaces:
+ *   mbg_create            FdtdSolver.__init__ state allocation      solver_fdtd.py:235-240
+ *   mbg_set_regions       per-cell coefficient arrays              solver_fdtd.py:242-272
+ *   mbg_set_qm_bloch      BlochSplittingKernel constants           _kernels.py:467-494
+ *   mbg_set_qm_dense      VectorSplittingKernel constants          _kernels.py:431-439
+ *   mbg_set_qm_rk4        VectorRk4Kernel constants                _kernels.py:552-557
+ *   mbg_set_boundary      boundary precompute                      solver_fdtd.py:310-325
+ *   mbg_set_sources       Source.value(n dt) per step              solver_fdtd.py:379-385
+ *   mbg_set_records       _RecordPlan list                         solver_fdtd.py:136-172,300-305
+ *   mbg_upload_fields     initial E / H                            solver_fdtd.py:237-239
+ *   mbg_upload_density    DensityKernel.init_state                 _kernels.py:376-377, 496-500
+ *   mbg_sample            _sample(0)                               solver_fdtd.py:449
+ *   mbg_advance           the step loop (phase1/2 + after_*)       solver_fdtd.py:457-463
+ *   mbg_poll_nonfinite    SolverError("non-finite ... at step n")  solver_fdtd.py:386-388
+ *   mbg_download_record   plan.to_result                           solver_fdtd.py:164-172
+ *   mbg_pack_halo/unpack  (new) slab ghost exchange, no reference analogue
+ *
+ * Conventions: every function returns 0 on success or a negative MBG_E_*
+ * code; mbg_last_error() gives the message.  All host pointers are plain
+ * C arrays owned by the caller and only read during the call.  Device
+ * memory is owned by the solver handle.  Cells are global grid indices.
+ */
+#ifndef MBGPU_H
+#define MBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBG_OK 0
+#define MBG_E_ARG (-1)
+#define MBG_E_CUDA (-2)
+#define MBG_E_UNSUPPORTED (-3)
+#define MBG_E_STATE (-4)
+
+#define MBG_STEPPER_SPLITTING 0
+#define MBG_STEPPER_RK4 1
+
+#define MBG_Q_E 0
+#define MBG_Q_H 1
+#define MBG_Q_D 2
+#define MBG_Q_INV 3
+
+#define MBG_MAX_REGIONS 16
+#define MBG_MAX_QM 4
+#define MBG_MAX_SOURCES 8
+#define MBG_MAX_RECORDS 64
+#define MBG_MAX_LEVELS 8
+#define MBG_MAX_TILE_STEPS 64
+
+typedef struct mbg_solver mbg_solver;
+
+typedef struct {
+    int64_t num_x;      /* global grid points (>= 1) */
+    int64_t num_t;      /* time levels; the run is steps 1 .. num_t-1 */
+    double dt, dx;
+    int32_t levels;     /* N of every quantum material, 0 if none */
+    int32_t stepper;    /* MBG_STEPPER_* */
+    int32_t tile_steps; /* k: time steps fused per kernel launch (0 = default) */
+    int32_t exact;      /* 1: no FMA contraction (bit-exact to the reference for N = 2) */
+    int32_t device;     /* CUDA device ordinal */
+    int32_t reserved;
+    int64_t win_lo, win_hi; /* cells held on this device (slab incl. ghosts) */
+    int64_t own_lo, own_hi; /* cells owned (recorded, scanned) by this device */
+} mbg_grid;
+
+/* lifecycle */
+int mbg_create(const mbg_grid *grid, mbg_solver **out);
+void mbg_destroy(mbg_solver *s);
+const char *mbg_last_error(const mbg_solver *s);
+const char *mbg_version(void);
+int mbg_device_count(int *count);
+/* stream: 0 = solver-owned stream; otherwise a cudaStream_t to launch on */
+int mbg_set_stream(mbg_solver *s, uint64_t stream);
+int mbg_tile_steps(const mbg_solver *s, int32_t *k);
+
+/* setup (host arrays, copied) */
+int mbg_set_regions(mbg_solver *s, int32_t n, const int64_t *e_start, const int64_t *h_start,
+                    const double *coef_a, const double *coef_bg, const double *coef_bdx,
+                    const double *coef_ch, const int32_t *qm_index);
+/* c[15] = kz cz fxy ax_c ax_s ay_c ay_s az_c az_s a0_c a0_s mu_x mu_y mu_z pol_factor */
+int mbg_set_qm_bloch(mbg_solver *s, int32_t qm, const double *c);
+/* row-major N x N; complex arrays interleaved (re, im); pol lists as _kernels.py:360-374 */
+int mbg_set_qm_dense(mbg_solver *s, int32_t qm, const double *pop_half, const double *coh_half,
+                     const double *b_const, const double *b_field, int32_t npol,
+                     const int32_t *pol_i, const int32_t *pol_j, const double *pol_v,
+                     int32_t ndpol, const int32_t *pol_di, const double *pol_dv, double pol_factor);
+int mbg_set_qm_rk4(mbg_solver *s, int32_t qm, const double *h0, const double *mu,
+                   const double *pop_matrix, const double *deph_matrix, int32_t npol,
+                   const int32_t *pol_i, const int32_t *pol_j, const double *pol_v,
+                   int32_t ndpol, const int32_t *pol_di, const double *pol_dv, double pol_factor);
+/* w = 1 - sqrt(R), c = v dt / dx, z = sqrt(mu / eps) of the edge materials */
+int mbg_set_boundary(mbg_solver *s, double wl, double cl, double zl, double wr, double cr, double zr);
+/* values: [num_t][n] samples Source.value(n dt) (row 0 unused) */
+int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t *hard,
+                    const double *values);
+/* quantity MBG_Q_*, cell -1 = whole domain, i/j 0-based, every >= 1; complex for d with i != j */
+int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *quantity, const int64_t *cell,
+                    const int32_t *i, const int32_t *j, const int64_t *every);
+
+/* state: e has (win_hi - win_lo) entries, h has one more (node win_hi) */
+int mbg_upload_fields(mbg_solver *s, const double *e, const double *h);
+/* one packed state vector (words per cell) broadcast to every quantum cell */
+int mbg_upload_density(mbg_solver *s, const double *words);
+/* full state planes [words][win cells] (tests, restarts) */
+int mbg_upload_state(mbg_solver *s, const double *planes);
+int mbg_download_fields(mbg_solver *s, double *e, double *h);
+int mbg_download_state(mbg_solver *s, double *planes);
+
+/* run */
+int mbg_sample(mbg_solver *s, int64_t step);
+int mbg_advance(mbg_solver *s, int64_t first_step, int64_t n_steps); /* async */
+int mbg_synchronize(mbg_solver *s);
+int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step); /* syncs; -1 when all finite */
+int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols);
+int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im);
+
+/* multi-device slabs: pack/unpack `count` cells starting at global cell
+ * `cell0` of E, H and every state plane into/out of a device buffer of
+ * (2 + words) * count doubles (ordered on the solver's stream) */
+int mbg_halo_words(const mbg_solver *s, int32_t *words);
+int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
+int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
+
+/* timing helpers for bench.py: device time of the launches issued by
+ * mbg_advance between mark_begin/mark_end (CUDA events on the solver stream) */
+int mbg_event_begin(mbg_solver *s);
+int mbg_event_end(mbg_solver *s, float *ms);
+int mbg_launch_count(const mbg_solver *s, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MBGPU_H */

@@ -1,0 +1,684 @@
+// C ABI of libmbgpu.so (declared in include/mbgpu.h).
+//
+// Owns the device state of one run (or of one slab of a multi-GPU run):
+// ping-pong buffers for E, H and the density state planes, the per-step
+// source samples, the record buffers and the non-finite flag.  mbg_advance
+// is the replacement of FdtdSolver._run_serial (solver_fdtd.py:457-463): it
+// issues one fused kernel per k time steps, computing on the host, per
+// launch, which records sample and whether the non-finite scan runs at each
+// fused step (solver_fdtd.py:386-393) so the kernels never divide in their
+// inner loop.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mbgpu.h"
+#include "mbg_kernels.h"
+
+using namespace mbg;
+
+namespace {
+
+struct QmHost {
+    int n = 0;
+    bool dense = false, rk4 = false;
+    double bloch[15] = {};
+    std::vector<double> pop, coh, bc, bf, h0, mu, popm, deph;  // complex interleaved where complex
+    std::vector<double> pol_re, pol_im, pol_dv;
+    double pol_factor = 0.0;
+};
+
+struct Rec {
+    int q = 0, i = 0, j = 0;
+    long long cell = -1, every = 1, rows = 0, cols = 0, col0 = 0;
+    double *re = nullptr, *im = nullptr;
+};
+
+}  // namespace
+
+struct mbg_solver {
+    mbg_grid g{};
+    int words = 0;
+    bool bloch = false;
+    int k = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    long long win_n = 0, plane = 0;
+    double *e[2] = {nullptr, nullptr}, *h[2] = {nullptr, nullptr}, *s[2] = {nullptr, nullptr};
+    int cur = 0;
+    Regions rg{};
+    bool have_regions = false;
+    std::vector<QmHost> qm;
+    bool has_boundary = false;
+    double bnd[6] = {};
+    int n_src = 0;
+    long long src_cell[kMaxSources] = {};
+    int src_hard[kMaxSources] = {};
+    double *src_values = nullptr;
+    std::vector<Rec> recs;
+    unsigned long long *bad = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    long long launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int fail(mbg_solver *s, int code, const std::string &msg) {
+    if (s) s->err = msg;
+    return code;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t _e = (call);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return fail(s, MBG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+
+int default_tile_steps(int levels, int stepper) {
+    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 16;
+    if (levels <= 3) return 8;
+    return 4;
+}
+
+int tile_width(const mbg_solver *s) {
+    if (s->bloch || s->g.levels == 0) return kBlochTile;
+    return s->g.levels >= 7 ? 64 : kDenseTile;
+}
+
+Launch base_launch(const mbg_solver *s) {
+    Launch L;
+    std::memset(&L, 0, sizeof(L));
+    L.num_x = s->g.num_x;
+    L.win_lo = s->g.win_lo;
+    L.win_n = s->win_n;
+    L.own_lo = s->g.own_lo;
+    L.own_hi = s->g.own_hi;
+    L.plane = s->plane;
+    L.e_in = s->e[s->cur];
+    L.h_in = s->h[s->cur];
+    L.s_in = s->s[s->cur];
+    L.e_out = s->e[1 - s->cur];
+    L.h_out = s->h[1 - s->cur];
+    L.s_out = s->s[1 - s->cur];
+    L.has_boundary = s->has_boundary ? 1 : 0;
+    // solver_fdtd.py:372-377: e_at = (1 - c) e0 + c e1; e = w * 0.5 * (...)
+    L.l_omc = 1.0 - s->bnd[1];
+    L.l_c = s->bnd[1];
+    L.l_hw = s->bnd[0] * 0.5;
+    L.l_z = s->bnd[2];
+    L.r_omc = 1.0 - s->bnd[4];
+    L.r_c = s->bnd[4];
+    L.r_hw = s->bnd[3] * 0.5;
+    L.r_z = s->bnd[5];
+    L.n_src = s->n_src;
+    for (int q = 0; q < s->n_src; ++q) {
+        L.src_cell[q] = s->src_cell[q];
+        L.src_hard[q] = s->src_hard[q];
+    }
+    L.src_values = s->src_values;
+    L.n_rec = (int)s->recs.size();
+    for (int r = 0; r < L.n_rec; ++r) {
+        const Rec &R = s->recs[r];
+        L.rec_q[r] = R.q;
+        L.rec_i[r] = R.i;
+        L.rec_j[r] = R.j;
+        L.rec_cell[r] = R.cell;
+        L.rec_every[r] = R.every;
+        L.rec_cols[r] = R.cols;
+        L.rec_col0[r] = R.col0;
+        L.rec_re[r] = R.re;
+        L.rec_im[r] = R.im;
+    }
+    L.bad_step = s->bad;
+    L.rg = s->rg;
+    return L;
+}
+
+template <int N>
+void fill_split(DenseQm<N> &d, const QmHost &h) {
+    for (int i = 0; i < N * N; ++i) {
+        d.pop[i] = h.pop[i];
+        d.coh[i] = h.coh[i];
+        d.bc_re[i] = h.bc[2 * i];
+        d.bc_im[i] = h.bc[2 * i + 1];
+        d.bf_re[i] = h.bf[2 * i];
+        d.bf_im[i] = h.bf[2 * i + 1];
+    }
+    for (int p = 0; p < N * (N - 1) / 2; ++p) {
+        d.pol.pol_re[p] = h.pol_re[p];
+        d.pol.pol_im[p] = h.pol_im[p];
+    }
+    for (int i = 0; i < N; ++i) d.pol.pol_dv[i] = h.pol_dv[i];
+    d.pol.pol_factor = h.pol_factor;
+}
+
+template <int N>
+void fill_rk4(Rk4Qm<N> &d, const QmHost &h, double dt) {
+    for (int i = 0; i < N * N; ++i) {
+        d.h0_re[i] = h.h0[2 * i];
+        d.h0_im[i] = h.h0[2 * i + 1];
+        d.mu_re[i] = h.mu[2 * i];
+        d.mu_im[i] = h.mu[2 * i + 1];
+        d.popm[i] = h.popm[i];
+        d.deph[i] = h.deph[i];
+    }
+    d.dt = dt;
+    for (int p = 0; p < N * (N - 1) / 2; ++p) {
+        d.pol.pol_re[p] = h.pol_re[p];
+        d.pol.pol_im[p] = h.pol_im[p];
+    }
+    for (int i = 0; i < N; ++i) d.pol.pol_dv[i] = h.pol_dv[i];
+    d.pol.pol_factor = h.pol_factor;
+}
+
+template <int N>
+cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles) {
+    const bool rk4 = s->g.stepper == MBG_STEPPER_RK4;
+    if (rk4) {
+        auto *P = new DenseParams<N, Rk4Qm<N>>();
+        P->L = L;
+        P->n_qm = (int)s->qm.size();
+        for (int q = 0; q < P->n_qm; ++q) fill_rk4<N>(P->qm[q], s->qm[q], s->g.dt);
+        cudaError_t e = s->g.exact ? exact::launch_dense_rk4(N, P, tiles, s->stream)
+                                   : fast::launch_dense_rk4(N, P, tiles, s->stream);
+        delete P;
+        return e;
+    }
+    if constexpr (N >= 3) {
+        auto *P = new DenseParams<N, DenseQm<N>>();
+        P->L = L;
+        P->n_qm = (int)s->qm.size();
+        for (int q = 0; q < P->n_qm; ++q) fill_split<N>(P->qm[q], s->qm[q]);
+        cudaError_t e = s->g.exact ? exact::launch_dense_split(N, P, tiles, s->stream)
+                                   : fast::launch_dense_split(N, P, tiles, s->stream);
+        delete P;
+        return e;
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
+    if (s->bloch || s->g.levels == 0) {
+        BlochParams P;
+        std::memset(&P, 0, sizeof(P));
+        P.L = L;
+        P.n_qm = (int)s->qm.size();
+        for (int q = 0; q < P.n_qm; ++q) std::memcpy(&P.qm[q], s->qm[q].bloch, sizeof(BlochQm));
+        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream) : fast::launch_bloch(P, tiles, s->stream);
+    }
+    switch (s->g.levels) {
+        case 2: return launch_dense_n<2>(s, L, tiles);
+        case 3: return launch_dense_n<3>(s, L, tiles);
+        case 4: return launch_dense_n<4>(s, L, tiles);
+        case 5: return launch_dense_n<5>(s, L, tiles);
+        case 6: return launch_dense_n<6>(s, L, tiles);
+        case 7: return launch_dense_n<7>(s, L, tiles);
+        case 8: return launch_dense_n<8>(s, L, tiles);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool window_ok(const mbg_grid *g) {
+    return g->win_lo >= 0 && g->win_hi <= g->num_x && g->win_lo < g->win_hi && g->own_lo >= g->win_lo &&
+           g->own_hi <= g->win_hi && g->own_lo < g->own_hi;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *mbg_version(void) { return "mbgpu 0.1 (sm_100a)"; }
+
+int mbg_device_count(int *count) {
+    mbg_solver *s = nullptr;
+    CK(cudaGetDeviceCount(count));
+    return MBG_OK;
+}
+
+const char *mbg_last_error(const mbg_solver *s) { return s ? s->err.c_str() : "null solver"; }
+
+int mbg_create(const mbg_grid *grid, mbg_solver **out) {
+    mbg_solver *s = nullptr;
+    if (!grid || !out) return MBG_E_ARG;
+    *out = nullptr;
+    mbg_grid g = *grid;
+    if (g.num_x < 1 || g.num_t < 2 || !(g.dt > 0)) return MBG_E_ARG;
+    if (g.win_hi == 0 && g.win_lo == 0) {
+        g.win_hi = g.num_x;
+        g.own_lo = 0;
+        g.own_hi = g.num_x;
+    }
+    if (!window_ok(&g)) return MBG_E_ARG;
+    if (g.levels < 0 || g.levels > MBG_MAX_LEVELS || g.levels == 1) return MBG_E_UNSUPPORTED;
+    if (g.stepper != MBG_STEPPER_SPLITTING && g.stepper != MBG_STEPPER_RK4) return MBG_E_ARG;
+    s = new mbg_solver();
+    s->g = g;
+    s->bloch = g.levels == 2 && g.stepper == MBG_STEPPER_SPLITTING;
+    s->words = g.levels == 0 ? 0 : (s->bloch ? 3 : g.levels * g.levels);
+    s->win_n = g.win_hi - g.win_lo;
+    s->plane = (s->win_n + 31) / 32 * 32;  // 256-byte aligned planes
+    int k = g.tile_steps > 0 ? g.tile_steps : default_tile_steps(g.levels, g.stepper);
+    const int w = tile_width(s);
+    k = std::min(k, std::min(MBG_MAX_TILE_STEPS, (w - 32) / 2));
+    s->k = std::max(k, 1);
+    auto cleanup = [&](int code) {
+        mbg_destroy(s);
+        return code;
+    };
+    if (cudaSetDevice(g.device) != cudaSuccess) return cleanup(MBG_E_CUDA);
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup(MBG_E_CUDA);
+    s->own_stream = true;
+    const size_t fb = sizeof(double) * (s->win_n + 1);
+    const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
+    for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&s->e[b], fb) != cudaSuccess || cudaMalloc(&s->h[b], fb) != cudaSuccess ||
+            cudaMalloc(&s->s[b], sb) != cudaSuccess)
+            return cleanup(MBG_E_CUDA);
+        cudaMemset(s->e[b], 0, fb);
+        cudaMemset(s->h[b], 0, fb);
+        cudaMemset(s->s[b], 0, sb);
+    }
+    if (cudaMalloc(&s->bad, sizeof(unsigned long long)) != cudaSuccess) return cleanup(MBG_E_CUDA);
+    cudaMemset(s->bad, 0xff, sizeof(unsigned long long));
+    cudaEventCreate(&s->ev0);
+    cudaEventCreate(&s->ev1);
+    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(MBG_E_CUDA);
+    *out = s;
+    return MBG_OK;
+}
+
+void mbg_destroy(mbg_solver *s) {
+    if (!s) return;
+    cudaSetDevice(s->g.device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(s->e[b]);
+        cudaFree(s->h[b]);
+        cudaFree(s->s[b]);
+    }
+    cudaFree(s->bad);
+    cudaFree(s->src_values);
+    for (auto &r : s->recs) {
+        cudaFree(r.re);
+        cudaFree(r.im);
+    }
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+int mbg_set_stream(mbg_solver *s, uint64_t stream) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    CK(cudaStreamSynchronize(s->stream));
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    if (stream == 0) {
+        CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+        s->own_stream = true;
+    } else {
+        s->stream = reinterpret_cast<cudaStream_t>(stream);
+        s->own_stream = false;
+    }
+    return MBG_OK;
+}
+
+int mbg_tile_steps(const mbg_solver *s, int32_t *k) {
+    if (!s || !k) return MBG_E_ARG;
+    *k = s->k;
+    return MBG_OK;
+}
+
+int mbg_set_regions(mbg_solver *s, int32_t n, const int64_t *e_start, const int64_t *h_start, const double *a,
+                    const double *bg, const double *bdx, const double *ch, const int32_t *qm_index) {
+    if (!s || n < 1) return fail(s, MBG_E_ARG, "need at least one region");
+    if (n > kMaxRegions) return fail(s, MBG_E_UNSUPPORTED, "too many regions (max 16)");
+    Regions &rg = s->rg;
+    std::memset(&rg, 0, sizeof(rg));
+    rg.n = n;
+    for (int r = 0; r < n; ++r) {
+        rg.e_start[r] = e_start[r];
+        rg.h_start[r] = h_start[r];
+        rg.a[r] = a[r];
+        rg.bg[r] = bg[r];
+        rg.bdx[r] = bdx[r];
+        rg.ch[r] = ch[r];
+        rg.qm[r] = qm_index[r];
+        if (qm_index[r] >= kMaxQm) return fail(s, MBG_E_UNSUPPORTED, "too many quantum materials");
+        if (r > 0 && (e_start[r] < e_start[r - 1] || h_start[r] < h_start[r - 1]))
+            return fail(s, MBG_E_ARG, "region starts must be non-decreasing");
+    }
+    s->have_regions = true;
+    return MBG_OK;
+}
+
+static QmHost &qm_slot(mbg_solver *s, int q) {
+    if ((int)s->qm.size() <= q) s->qm.resize(q + 1);
+    return s->qm[q];
+}
+
+int mbg_set_qm_bloch(mbg_solver *s, int32_t q, const double *c) {
+    if (!s || q < 0 || q >= kMaxQm || !c) return fail(s, MBG_E_ARG, "bad qm index");
+    if (!s->bloch) return fail(s, MBG_E_STATE, "solver is not a two-level splitting solver");
+    QmHost &h = qm_slot(s, q);
+    h.n = 2;
+    std::memcpy(h.bloch, c, sizeof(h.bloch));
+    return MBG_OK;
+}
+
+static void set_pol(QmHost &h, int n, int npol, const int32_t *pi, const int32_t *pj, const double *pv, int ndpol,
+                    const int32_t *pdi, const double *pdv, double pol_factor) {
+    const int nu = n * (n - 1) / 2;
+    h.pol_re.assign(std::max(nu, 1), 0.0);
+    h.pol_im.assign(std::max(nu, 1), 0.0);
+    h.pol_dv.assign(n, 0.0);
+    for (int k = 0; k < npol; ++k) {
+        const int i = pi[k], j = pj[k];
+        const int p = i * n - i * (i + 1) / 2 + (j - i - 1);
+        h.pol_re[p] = pv[2 * k];
+        h.pol_im[p] = pv[2 * k + 1];
+    }
+    for (int k = 0; k < ndpol; ++k) h.pol_dv[pdi[k]] = pdv[k];
+    h.pol_factor = pol_factor;
+}
+
+static bool pol_ok(int n, int npol, const int32_t *pi, const int32_t *pj, int ndpol, const int32_t *pdi) {
+    for (int k = 0; k < npol; ++k)
+        if (pi[k] < 0 || pj[k] <= pi[k] || pj[k] >= n) return false;
+    for (int k = 0; k < ndpol; ++k)
+        if (pdi[k] < 0 || pdi[k] >= n) return false;
+    return true;
+}
+
+int mbg_set_qm_dense(mbg_solver *s, int32_t q, const double *pop, const double *coh, const double *bc,
+                     const double *bf, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
+                     int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
+    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support 2 quantum materials");
+    const int n = s->g.levels;
+    if (s->bloch || s->g.stepper != MBG_STEPPER_SPLITTING || n < 3)
+        return fail(s, MBG_E_STATE, "solver is not an N>=3 splitting solver");
+    if (!pol_ok(n, npol, pi, pj, ndpol, pdi)) return fail(s, MBG_E_ARG, "bad dipole index list");
+    QmHost &h = qm_slot(s, q);
+    h.n = n;
+    h.dense = true;
+    h.pop.assign(pop, pop + n * n);
+    h.coh.assign(coh, coh + n * n);
+    h.bc.assign(bc, bc + 2 * n * n);
+    h.bf.assign(bf, bf + 2 * n * n);
+    set_pol(h, n, npol, pi, pj, pv, ndpol, pdi, pdv, pol_factor);
+    return MBG_OK;
+}
+
+int mbg_set_qm_rk4(mbg_solver *s, int32_t q, const double *h0, const double *mu, const double *popm,
+                   const double *deph, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
+                   int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
+    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support 2 quantum materials");
+    const int n = s->g.levels;
+    if (s->g.stepper != MBG_STEPPER_RK4 || n < 2) return fail(s, MBG_E_STATE, "solver is not an RK4 solver");
+    if (!pol_ok(n, npol, pi, pj, ndpol, pdi)) return fail(s, MBG_E_ARG, "bad dipole index list");
+    QmHost &h = qm_slot(s, q);
+    h.n = n;
+    h.rk4 = true;
+    h.h0.assign(h0, h0 + 2 * n * n);
+    h.mu.assign(mu, mu + 2 * n * n);
+    h.popm.assign(popm, popm + n * n);
+    h.deph.assign(deph, deph + n * n);
+    set_pol(h, n, npol, pi, pj, pv, ndpol, pdi, pdv, pol_factor);
+    return MBG_OK;
+}
+
+int mbg_set_boundary(mbg_solver *s, double wl, double cl, double zl, double wr, double cr, double zr) {
+    if (!s) return MBG_E_ARG;
+    s->has_boundary = s->g.num_x > 1;
+    const double v[6] = {wl, cl, zl, wr, cr, zr};
+    std::memcpy(s->bnd, v, sizeof(v));
+    return MBG_OK;
+}
+
+int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t *hard, const double *values) {
+    if (!s || n < 0) return MBG_E_ARG;
+    if (n > kMaxSources) return fail(s, MBG_E_UNSUPPORTED, "too many sources (max 8)");
+    cudaSetDevice(s->g.device);
+    cudaFree(s->src_values);
+    s->src_values = nullptr;
+    s->n_src = n;
+    for (int q = 0; q < n; ++q) {
+        if (cell[q] < 0 || cell[q] >= s->g.num_x) return fail(s, MBG_E_ARG, "source cell outside the grid");
+        s->src_cell[q] = cell[q];
+        s->src_hard[q] = hard[q] ? 1 : 0;
+    }
+    if (n > 0) {
+        const size_t bytes = sizeof(double) * (size_t)n * s->g.num_t;
+        CK(cudaMalloc(&s->src_values, bytes));
+        CK(cudaMemcpy(s->src_values, values, bytes, cudaMemcpyHostToDevice));
+    }
+    return MBG_OK;
+}
+
+int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *cell, const int32_t *i,
+                    const int32_t *j, const int64_t *every) {
+    if (!s || n < 0) return MBG_E_ARG;
+    if (n > kMaxRecords) return fail(s, MBG_E_UNSUPPORTED, "too many records (max 64)");
+    cudaSetDevice(s->g.device);
+    for (auto &r : s->recs) {
+        cudaFree(r.re);
+        cudaFree(r.im);
+    }
+    s->recs.assign(n, Rec());
+    for (int r = 0; r < n; ++r) {
+        Rec &R = s->recs[r];
+        R.q = q[r];
+        R.i = i[r];
+        R.j = j[r];
+        R.cell = cell[r];
+        R.every = every[r];
+        if (R.q < 0 || R.q > 3 || R.every < 1 || R.cell >= s->g.num_x ||
+            (R.q == MBG_Q_D && (R.i < 0 || R.j < 0 || R.i >= std::max(1, s->g.levels) || R.j >= std::max(1, s->g.levels))))
+            return fail(s, MBG_E_ARG, "bad record specification");
+        R.rows = (s->g.num_t - 1) / R.every + 1;
+        R.cols = R.cell >= 0 ? 1 : s->g.own_hi - s->g.own_lo;
+        R.col0 = R.cell >= 0 ? R.cell : s->g.own_lo;
+        const size_t bytes = sizeof(double) * (size_t)R.rows * R.cols;
+        CK(cudaMalloc(&R.re, bytes));
+        CK(cudaMemset(R.re, 0, bytes));
+        if (R.q == MBG_Q_D && R.i != R.j) {
+            CK(cudaMalloc(&R.im, bytes));
+            CK(cudaMemset(R.im, 0, bytes));
+        }
+    }
+    return MBG_OK;
+}
+
+int mbg_upload_fields(mbg_solver *s, const double *e, const double *h) {
+    if (!s || !e || !h) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMemcpyAsync(s->e[b], e, sizeof(double) * s->win_n, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaMemcpyAsync(s->h[b], h, sizeof(double) * (s->win_n + 1), cudaMemcpyHostToDevice, s->stream));
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_upload_density(mbg_solver *s, const double *words) {
+    if (!s || (!words && s->words)) return MBG_E_ARG;
+    if (!s->have_regions) return fail(s, MBG_E_STATE, "set regions before the density state");
+    if (s->words == 0) return MBG_OK;
+    cudaSetDevice(s->g.device);
+    double *w = nullptr;
+    CK(cudaMalloc(&w, sizeof(double) * s->words));
+    CK(cudaMemcpy(w, words, sizeof(double) * s->words, cudaMemcpyHostToDevice));
+    for (int b = 0; b < 2; ++b)
+        CK(launch_broadcast_state(s->s[b], s->plane, s->win_n, s->words, w, s->rg, s->g.win_lo, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    cudaFree(w);
+    return MBG_OK;
+}
+
+int mbg_upload_state(mbg_solver *s, const double *planes) {
+    if (!s || !planes) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    for (int b = 0; b < 2; ++b)
+        for (int w = 0; w < s->words; ++w)
+            CK(cudaMemcpyAsync(s->s[b] + w * s->plane, planes + w * s->win_n, sizeof(double) * s->win_n,
+                               cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_download_fields(mbg_solver *s, double *e, double *h) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    if (e) CK(cudaMemcpyAsync(e, s->e[s->cur], sizeof(double) * s->win_n, cudaMemcpyDeviceToHost, s->stream));
+    if (h) CK(cudaMemcpyAsync(h, s->h[s->cur], sizeof(double) * (s->win_n + 1), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_download_state(mbg_solver *s, double *planes) {
+    if (!s || !planes) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    for (int w = 0; w < s->words; ++w)
+        CK(cudaMemcpyAsync(planes + w * s->win_n, s->s[s->cur] + w * s->plane, sizeof(double) * s->win_n,
+                           cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_sample(mbg_solver *s, int64_t step) {
+    if (!s) return MBG_E_ARG;
+    if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
+    cudaSetDevice(s->g.device);
+    const Launch L = base_launch(s);
+    CK(launch_sample(L, nullptr, s->g.levels, s->bloch ? 1 : 0, step, s->stream));
+    return MBG_OK;
+}
+
+int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
+    if (!s) return MBG_E_ARG;
+    if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
+    if ((s->bloch || s->g.levels >= 3 || s->g.stepper == MBG_STEPPER_RK4) && s->g.levels > 0 &&
+        s->qm.empty())
+        return fail(s, MBG_E_STATE, "quantum constants not set");
+    if (first < 1 || n_steps < 0 || first + n_steps > s->g.num_t)
+        return fail(s, MBG_E_ARG, "step range outside 1 .. num_t-1");
+    const long long ghost_l = s->g.own_lo - s->g.win_lo, ghost_r = s->g.win_hi - s->g.own_hi;
+    const bool windowed = s->g.win_lo > 0 || s->g.win_hi < s->g.num_x;
+    if (windowed) {
+        const long long gw = std::min(s->g.win_lo > 0 ? ghost_l : LLONG_MAX, s->g.win_hi < s->g.num_x ? ghost_r : LLONG_MAX);
+        if (n_steps > std::min<long long>(gw, s->k))
+            return fail(s, MBG_E_ARG, "a slab advances at most min(ghost width, k) steps between exchanges");
+    }
+    cudaSetDevice(s->g.device);
+    const int tw = tile_width(s);
+    long long n = first;
+    const long long end = first + n_steps;
+    while (n < end) {
+        const int kk = (int)std::min<long long>(s->k, end - n);
+        Launch L = base_launch(s);
+        L.n0 = n;
+        L.k = kk;
+        L.res_lo = s->g.win_lo == 0 ? 0 : s->g.win_lo + kk;
+        L.res_hi = s->g.win_hi == s->g.num_x ? s->g.num_x : s->g.win_hi - kk;
+        L.tile_own = tw - 2 * kk;
+        for (int t = 0; t < kk; ++t) {
+            const long long step = n + t;
+            unsigned long long m = 0;
+            for (size_t r = 0; r < s->recs.size(); ++r)
+                if (step % s->recs[r].every == 0) m |= 1ull << r;
+            L.step_mask[t] = m;
+            if (step % 1024 == 0 || step == s->g.num_t - 1) L.check_mask |= 1ull << t;
+        }
+        const long long tiles = (L.res_hi - L.res_lo + L.tile_own - 1) / L.tile_own;
+        CK(launch_step(s, L, tiles));
+        ++s->launches;
+        s->cur ^= 1;
+        n += kk;
+    }
+    return MBG_OK;
+}
+
+int mbg_synchronize(mbg_solver *s) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step) {
+    if (!s || !bad_step) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, s->bad, sizeof(v), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *bad_step = v == ~0ull ? -1 : (int64_t)v;
+    return MBG_OK;
+}
+
+int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols) {
+    if (!s || r < 0 || r >= (int)s->recs.size()) return MBG_E_ARG;
+    *rows = s->recs[r].rows;
+    *cols = s->recs[r].cols;
+    return MBG_OK;
+}
+
+int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im) {
+    if (!s || r < 0 || r >= (int)s->recs.size() || !re) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    const Rec &R = s->recs[r];
+    const size_t bytes = sizeof(double) * (size_t)R.rows * R.cols;
+    CK(cudaMemcpyAsync(re, R.re, bytes, cudaMemcpyDeviceToHost, s->stream));
+    if (R.im && im) CK(cudaMemcpyAsync(im, R.im, bytes, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_halo_words(const mbg_solver *s, int32_t *words) {
+    if (!s || !words) return MBG_E_ARG;
+    *words = 2 + s->words;
+    return MBG_OK;
+}
+
+static int halo(mbg_solver *s, bool pack, int64_t cell0, int64_t count, uint64_t buf) {
+    if (!s || !buf || count < 0) return MBG_E_ARG;
+    const long long l0 = cell0 - s->g.win_lo;
+    if (l0 < 0 || l0 + count > s->win_n) return fail(s, MBG_E_ARG, "halo range outside the window");
+    cudaSetDevice(s->g.device);
+    CK(launch_halo(pack, s->e[s->cur], s->h[s->cur], s->s[s->cur], s->plane, s->words, l0, count,
+                   reinterpret_cast<double *>(buf), s->stream));
+    return MBG_OK;
+}
+
+int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, true, cell0, count, buf); }
+int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, false, cell0, count, buf); }
+
+int mbg_event_begin(mbg_solver *s) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    CK(cudaEventRecord(s->ev0, s->stream));
+    return MBG_OK;
+}
+
+int mbg_event_end(mbg_solver *s, float *ms) {
+    if (!s || !ms) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    CK(cudaEventRecord(s->ev1, s->stream));
+    CK(cudaEventSynchronize(s->ev1));
+    CK(cudaEventElapsedTime(ms, s->ev0, s->ev1));
+    return MBG_OK;
+}
+
+int mbg_launch_count(const mbg_solver *s, int64_t *launches) {
+    if (!s || !launches) return MBG_E_ARG;
+    *launches = s->launches;
+    return MBG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Auxiliary kernels: initial-state broadcast, step-0 sampling, halo packing.
+#include "mbg_kernels.h"
+
+namespace mbg {
+
+namespace {
+
+__device__ __forceinline__ int pair_index(int n, int i, int j) { return i * n - i * (i + 1) / 2 + (j - i - 1); }
+
+// DensityKernel.init_state: the same rho0 in every quantum cell
+// (_kernels.py:376-377, Bloch form _kernels.py:496-500)
+__global__ void broadcast_state_kernel(double *s, long long plane, long long win_n, int words,
+                                       const double *w, const Regions rg, long long win_lo) {
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= win_n) return;
+    const int r = region_of(rg.e_start, rg.n, win_lo + l);
+    const bool qm = rg.qm[r] >= 0;
+    for (int k = 0; k < words; ++k) s[k * plane + l] = qm ? w[k] : 0.0;
+}
+
+// _sample(step) from the current state (used for row 0, solver_fdtd.py:449)
+__global__ void sample_kernel(const Launch L, int levels, int bloch, long long step) {
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L.win_n) return;
+    const long long c = L.win_lo + l;
+    if (c < L.own_lo || c >= L.own_hi) return;
+    const int qm = L.rg.qm[region_of(L.rg.e_start, L.rg.n, c)];
+    for (int r = 0; r < L.n_rec; ++r) {
+        if (step % L.rec_every[r]) continue;
+        const long long cell = L.rec_cell[r];
+        if (cell >= 0 && cell != c) continue;
+        const long long idx = (step / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+        double re = 0.0, im = 0.0;
+        const int q = L.rec_q[r];
+        if (q == MBG_Q_E) {
+            re = L.e_in[l];
+        } else if (q == MBG_Q_H) {
+            re = L.h_in[l];
+        } else if (qm >= 0) {
+            const double *s = L.s_in + l;
+            const long long P = L.plane;
+            if (bloch) {
+                const double x = s[0], y = s[P], z = s[2 * P];
+                if (q == MBG_Q_INV) {
+                    re = -z;
+                } else {
+                    const int i = L.rec_i[r], j = L.rec_j[r];
+                    if (i == j) {
+                        re = (i == 0) ? 0.5 * (1.0 + z) : 0.5 * (1.0 - z);
+                    } else {
+                        re = 0.5 * x;
+                        im = (i == 0) ? 0.5 * -y : 0.5 * y;
+                    }
+                }
+            } else if (q == MBG_Q_INV) {
+                re = s[P] - s[0];
+            } else {
+                const int i = L.rec_i[r], j = L.rec_j[r], n = levels;
+                if (i == j) {
+                    re = s[i * P];
+                } else if (i < j) {
+                    const int w = n + 2 * pair_index(n, i, j);
+                    re = s[w * P];
+                    im = s[(w + 1) * P];
+                } else {
+                    const int w = n + 2 * pair_index(n, j, i);
+                    re = s[w * P];
+                    im = -s[(w + 1) * P];
+                }
+            }
+        }
+        L.rec_re[r][idx] = re;
+        if (L.rec_im[r]) L.rec_im[r][idx] = im;
+    }
+}
+
+// ghost exchange: [E | H | state planes] x count cells starting at local l0
+__global__ void halo_kernel(bool pack, double *e, double *h, double *s, long long plane, int words, long long l0,
+                            long long count, double *buf) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long total = (long long)(2 + words) * count;
+    if (t >= total) return;
+    const long long w = t / count, c = t % count, l = l0 + c;
+    double *p = (w == 0) ? e + l : (w == 1) ? h + l : s + (w - 2) * plane + l;
+    if (pack)
+        buf[t] = *p;
+    else
+        *p = buf[t];
+}
+
+unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace
+
+cudaError_t launch_sample(const Launch &L, const void *, int levels, int bloch, long long step, cudaStream_t st) {
+    if (L.win_n <= 0) return cudaSuccess;
+    sample_kernel<<<blocks_for(L.win_n, 256), 256, 0, st>>>(L, levels, bloch, step);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, int words, const double *w,
+                                   const Regions &rg, long long win_lo, cudaStream_t st) {
+    if (win_n <= 0 || words == 0) return cudaSuccess;
+    broadcast_state_kernel<<<blocks_for(win_n, 256), 256, 0, st>>>(s, plane, win_n, words, w, rg, win_lo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long plane, int words, long long l0,
+                        long long count, double *buf, cudaStream_t st) {
+    const long long total = (long long)(2 + words) * count;
+    if (total <= 0) return cudaSuccess;
+    halo_kernel<<<blocks_for(total, 256), 256, 0, st>>>(pack, e, h, s, plane, words, l0, count, buf);
+    return cudaGetLastError();
+}
+
+}  // namespace mbg

@@ -1,0 +1,242 @@
+// Fused time-step kernel for two-level media (and purely classical devices).
+//
+// One launch advances the Yee fields and the Bloch vectors by k time steps
+// (temporal tiling).  Each warp owns a tile of 32*C consecutive cells laid out
+// cyclically (slot i*32 + lane), so every global load/store is a coalesced
+// 256-byte row.  E, H and the Bloch vector (x, y, z) stay in registers for all
+// k steps; the only neighbour traffic of the stencil is one warp shuffle of E
+// to the right (H update needs E[m-1]) and one of H to the left (E update
+// needs H[m+1]) per cell and step.  The dependency cone shrinks by one cell per
+// side per step, so a tile that loads 32*C cells delivers the 32*C - 2k cells
+// in its middle ("redundant halo"); tiles touching a physical edge keep their
+// edge cells.
+//
+// Per step the operation sequence is the reference's (solver_fdtd.py:457-463):
+//   H^{n-1/2}[m] = H + c' (E[m] - E[m-1])            solver_fdtd.py:53-56
+//   Bloch step with E^{n-1}, p = pol_factor d<mu>     _kernels.py:200-232
+//   E^n[m] = a' E - b'G p + b'/dx (H[m+1] - H[m])      solver_fdtd.py:59-66
+//   edge cells <- (1 - sqrt R) * outgoing char.        solver_fdtd.py:366-378
+//   sources (hard overwrite / soft add), in order      solver_fdtd.py:379-385
+//   non-finite scan, record sampling                   solver_fdtd.py:386-426
+// Built without FMA contraction (exact variant) every value is bit-identical
+// to the reference.
+#include "mbg_kernels.h"
+
+#ifndef MBG_VARIANT
+#error "compile with -DMBG_VARIANT=fast|exact"
+#endif
+
+namespace mbg {
+namespace MBG_VARIANT {
+
+namespace {
+
+constexpr int C = kBlochCellsPerLane;
+constexpr int W = kBlochTile;
+constexpr unsigned kFull = 0xffffffffu;
+
+// _kernels.py:200-232, same expression order
+__device__ __forceinline__ double bloch_cell(const BlochQm &q, double e, double &x, double &y, double &z) {
+    const double x0 = x, y0 = y, z0 = z;
+    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = q.kz * z0 + q.cz;
+    const double ax = q.ax_c + q.ax_s * e, ay = q.ay_c + q.ay_s * e;
+    const double az = q.az_c + q.az_s * e, a0 = q.a0_c + q.a0_s * e;
+    const double qq = ax * ax + ay * ay + az * az;
+    const double u = a0 * a0;
+    const double num = 1.0 + u - qq;
+    const double t1 = 1.0 + qq - u;
+    const double inv = 1.0 / (t1 * t1 + 4.0 * u);
+    const double k1 = (num * num - 4.0 * qq) * inv;
+    const double g = 4.0 * num * inv;
+    const double dotb = 8.0 * inv * (ax * x1 + ay * y1 + az * z1);
+    const double x2 = k1 * x1 + g * (ay * z1 - az * y1) + dotb * ax;
+    const double y2 = k1 * y1 + g * (az * x1 - ax * z1) + dotb * ay;
+    const double z2 = k1 * z1 + g * (ax * y1 - ay * x1) + dotb * az;
+    x = q.fxy * x2;
+    y = q.fxy * y2;
+    z = q.kz * z2 + q.cz;
+    return q.pol_factor * (q.mu_x * (x - x0) + q.mu_y * (y - y0) + q.mu_z * (z - z0));
+}
+
+// density entry (i, j) of a Bloch vector (_kernels.py:530-536)
+__device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, double z, double &re, double &im) {
+    if (i == j) {
+        re = (i == 0) ? 0.5 * (1.0 + z) : 0.5 * (1.0 - z);
+        im = 0.0;
+    } else {
+        re = 0.5 * x;
+        im = (i == 0) ? 0.5 * -y : 0.5 * y;
+    }
+}
+
+template <bool UNI>
+__device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
+                                         int lane) {
+    const Launch &L = P.L;
+    const long long nx = L.num_x;
+    double E[C], H[C], X[C], Y[C], Z[C];
+    int qi[C];  // quantum material of the slot, -1 classical / outside
+    int re_[C], rh_[C];
+    // uniform tiles: one E region and one H region -> scalar coefficients
+    const long long c_first = base < 0 ? 0 : base;
+    const int re_u = region_of(L.rg.e_start, L.rg.n, c_first);
+    const int rh_u = region_of(L.rg.h_start, L.rg.n, c_first < 1 ? 1 : c_first);
+
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        const long long c = base + i * 32 + lane;
+        const long long l = c - L.win_lo;
+        const bool in_e = (l >= 0 && l < L.win_n);
+        E[i] = in_e ? L.e_in[l] : 0.0;
+        H[i] = (l >= 0 && l <= L.win_n) ? L.h_in[l] : 0.0;
+        re_[i] = UNI ? re_u : region_of(L.rg.e_start, L.rg.n, c);
+        rh_[i] = UNI ? rh_u : region_of(L.rg.h_start, L.rg.n, c);
+        qi[i] = (in_e && c >= 0 && c < nx) ? L.rg.qm[re_[i]] : -1;
+        if (qi[i] >= 0) {
+            X[i] = L.s_in[l];
+            Y[i] = L.s_in[L.plane + l];
+            Z[i] = L.s_in[2 * L.plane + l];
+        } else {
+            X[i] = Y[i] = Z[i] = 0.0;
+        }
+    }
+    const bool left_edge = L.has_boundary && base == 0;
+    const bool right_edge = L.has_boundary && base <= nx - 1 && nx - 1 < base + W;
+
+    for (int s = 0; s < L.k; ++s) {
+        const long long n = L.n0 + s;
+        // ---- H update: needs E[m-1] (left neighbour) -----------------------
+        double t[C];
+#pragma unroll
+        for (int i = 0; i < C; ++i) t[i] = __shfl_sync(kFull, E[i], (lane + 31) & 31);
+        double e_right0 = 0.0, h_right0 = 0.0;  // old E[1], H[1] for the left edge
+        if (left_edge) {
+            e_right0 = __shfl_sync(kFull, E[0], (lane + 1) & 31);
+            h_right0 = __shfl_sync(kFull, H[0], (lane + 1) & 31);
+        }
+        double Hn[C], El[C];
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            const long long c = base + i * 32 + lane;
+            El[i] = (lane == 0) ? t[i > 0 ? i - 1 : 0] : t[i];
+            const double ch = UNI ? L.rg.ch[rh_u] : L.rg.ch[rh_[i]];
+            Hn[i] = (c >= 1 && c <= nx - 1) ? H[i] + ch * (E[i] - El[i]) : H[i];
+        }
+        // ---- density step with E^{n-1} and polarisation rate -----------------
+        double p[C];
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            p[i] = 0.0;
+            if (qi[i] >= 0) p[i] = bloch_cell(P.qm[qi[i]], E[i], X[i], Y[i], Z[i]);
+        }
+        // ---- E update: needs H[m+1] (right neighbour) --------------------------
+        double u[C];
+#pragma unroll
+        for (int i = 0; i < C; ++i) u[i] = __shfl_sync(kFull, Hn[i], (lane + 1) & 31);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            const long long c = base + i * 32 + lane;
+            const double hr = (lane == 31) ? u[i < C - 1 ? i + 1 : i] : u[i];
+            const int r = UNI ? re_u : re_[i];
+            const double a = L.rg.a[r], bg = L.rg.bg[r], bdx = L.rg.bdx[r];
+            double en = (nx > 1 && c >= 0 && c < nx) ? a * E[i] - bg * p[i] + bdx * (hr - Hn[i]) : E[i];
+            if (left_edge && i == 0 && lane == 0) {
+                // solver_fdtd.py:372-374
+                const double e_at = L.l_omc * E[0] + L.l_c * e_right0;
+                const double h_at = 0.5 * (h_right0 + hr);
+                en = L.l_hw * (e_at + L.l_z * h_at);
+            }
+            if (right_edge && c == nx - 1) {
+                // solver_fdtd.py:375-377 (E[Nx-2] old is the left neighbour)
+                const double e_at = L.r_omc * E[i] + L.r_c * El[i];
+                const double h_at = 0.5 * (H[i] + Hn[i]);
+                en = L.r_hw * (e_at - L.r_z * h_at);
+            }
+            for (int q = 0; q < L.n_src; ++q) {
+                if (c == L.src_cell[q]) {
+                    const double v = L.src_values[n * L.n_src + q];
+                    en = L.src_hard[q] ? v : en + v;
+                }
+            }
+            E[i] = en;
+            H[i] = Hn[i];
+        }
+        // ---- non-finite scan and records (owned result cells only) --------------
+        const unsigned long long mask = L.step_mask[s];
+        const bool check = (L.check_mask >> s) & 1ull;
+        if (mask || check) {
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const long long c = base + i * 32 + lane;
+                const bool own = c >= t_lo && c < t_hi && c >= L.own_lo && c < L.own_hi;
+                if (!own) continue;
+                if (check && !isfinite(E[i])) atomicMin(L.bad_step, (unsigned long long)n);
+                for (int r = 0; r < L.n_rec; ++r) {
+                    if (!((mask >> r) & 1ull)) continue;
+                    const long long cell = L.rec_cell[r];
+                    if (cell >= 0 && cell != c) continue;
+                    const long long col = cell >= 0 ? 0 : c - L.rec_col0[r];
+                    const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + col;
+                    double vre = 0.0, vim = 0.0;
+                    switch (L.rec_q[r]) {
+                        case MBG_Q_E: vre = E[i]; break;
+                        case MBG_Q_H: vre = H[i]; break;
+                        case MBG_Q_D:
+                            if (qi[i] >= 0) bloch_entry(L.rec_i[r], L.rec_j[r], X[i], Y[i], Z[i], vre, vim);
+                            break;
+                        default:
+                            if (qi[i] >= 0) vre = -Z[i];
+                    }
+                    L.rec_re[r][idx] = vre;
+                    if (L.rec_im[r]) L.rec_im[r][idx] = vim;
+                }
+            }
+        }
+    }
+    // ---- write back the tile's result cells -------------------------------------
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        const long long c = base + i * 32 + lane;
+        if (c < t_lo || c >= t_hi) continue;
+        const long long l = c - L.win_lo;
+        L.e_out[l] = E[i];
+        L.h_out[l] = H[i];
+        if (qi[i] >= 0) {
+            L.s_out[l] = X[i];
+            L.s_out[L.plane + l] = Y[i];
+            L.s_out[2 * L.plane + l] = Z[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32)
+bloch_step_kernel(const __grid_constant__ BlochParams P) {
+    const Launch &L = P.L;
+    const int lane = threadIdx.x & 31;
+    const long long tile = (long long)blockIdx.x * kBlochWarpsPerBlock + (threadIdx.x >> 5);
+    const long long t_lo = L.res_lo + tile * L.tile_own;
+    if (t_lo >= L.res_hi) return;
+    const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
+    // the tile at the physical left edge starts at cell 0 (nothing to its left)
+    const long long base = (t_lo - L.k < 0) ? 0 : t_lo - L.k;
+    // warp-uniform test: one E region and one H region across the tile
+    const long long lo = base, hi = base + W - 1 < L.num_x ? base + W - 1 : L.num_x - 1;
+    const bool uni = region_of(L.rg.e_start, L.rg.n, lo) == region_of(L.rg.e_start, L.rg.n, hi) &&
+                     region_of(L.rg.h_start, L.rg.n, lo < 1 ? 1 : lo) ==
+                         region_of(L.rg.h_start, L.rg.n, hi < 1 ? 1 : hi);
+    if (uni)
+        run_tile<true>(P, t_lo, t_hi, base, lane);
+    else
+        run_tile<false>(P, t_lo, t_hi, base, lane);
+}
+
+}  // namespace
+
+cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st) {
+    const long long blocks = (tiles + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
+    bloch_step_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace MBG_VARIANT
+}  // namespace mbg

@@ -1,0 +1,38 @@
+// Launchers of the step kernels.  Each kernel translation unit is compiled
+// twice: MBG_VARIANT=fast (FMA contraction allowed) and MBG_VARIANT=exact
+// (-fmad=false, IEEE operation order of the reference's numba loops, which
+// makes the two-level path bit-identical to the reference).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "mbg_params.cuh"
+
+namespace mbg {
+
+// tile geometry of the N = 2 kernel: one warp per tile, C cells per lane
+constexpr int kBlochCellsPerLane = 8;
+constexpr int kBlochTile = 32 * kBlochCellsPerLane;
+constexpr int kBlochWarpsPerBlock = 4;
+// dense kernels: one thread per cell, one CTA per tile
+constexpr int kDenseTile = 128;
+
+#define MBG_DECLARE_LAUNCHERS(NS)                                                             \
+    namespace NS {                                                                            \
+    cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st);         \
+    cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \
+    cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStream_t st);   \
+    }
+
+MBG_DECLARE_LAUNCHERS(fast)
+MBG_DECLARE_LAUNCHERS(exact)
+
+// auxiliary kernels (variant independent)
+cudaError_t launch_sample(const Launch &L, const void *qm_words, int levels, int bloch,
+                          long long step, cudaStream_t st);
+cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, int words,
+                                   const double *words_dev, const Regions &rg, long long win_lo,
+                                   cudaStream_t st);
+cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long plane, int words,
+                        long long l0, long long count, double *buf, cudaStream_t st);
+
+}  // namespace mbg

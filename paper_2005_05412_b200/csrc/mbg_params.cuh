@@ -1,0 +1,124 @@
+// Launch parameter blocks of the fused step kernels.
+//
+// Everything a kernel needs is passed by value as a __grid_constant__
+// parameter block (constant bank 0): material coefficients, stepper constants,
+// boundary, source cells, record plans and the per-step sampling masks of the
+// launch.  Constants indexed at compile time become immediate constant-bank
+// operands of the FP64 instructions, and no process-global device state
+// exists, so any number of solver handles can coexist.
+#pragma once
+#include <cstdint>
+
+#include "../../include/mbgpu.h"
+
+namespace mbg {
+
+constexpr int kMaxRegions = MBG_MAX_REGIONS;
+constexpr int kMaxQm = MBG_MAX_QM;
+constexpr int kMaxDenseQm = 2;
+constexpr int kMaxSources = MBG_MAX_SOURCES;
+constexpr int kMaxRecords = MBG_MAX_RECORDS;
+constexpr int kMaxTileSteps = MBG_MAX_TILE_STEPS;
+
+// region table (replaces the reference's per-cell coefficient arrays,
+// solver_fdtd.py:252-268): E cell m belongs to the last region r with
+// e_start[r] <= m; H node m (1..Nx-1) to the last r with h_start[r] <= m
+struct Regions {
+    int n;
+    long long e_start[kMaxRegions];
+    long long h_start[kMaxRegions];
+    double a[kMaxRegions];    // a'
+    double bg[kMaxRegions];   // b' * Gamma
+    double bdx[kMaxRegions];  // b' / dx
+    double ch[kMaxRegions];   // c'
+    int qm[kMaxRegions];      // quantum material index, -1 classical
+};
+
+struct Launch {
+    long long num_x;
+    long long win_lo, win_n;  // window: global cells [win_lo, win_lo + win_n)
+    long long res_lo, res_hi; // cells valid after this launch
+    long long own_lo, own_hi; // cells recorded / scanned here
+    long long n0;             // global step index of the first fused step
+    int k;                    // fused steps in this launch
+    int tile_own;             // result cells per tile
+    long long plane;          // stride between state planes (elements)
+    const double *e_in, *h_in, *s_in;
+    double *e_out, *h_out, *s_out;
+    // boundary terms evaluated as solver_fdtd.py:372-377 does:
+    // e_at = omc*e_edge + c*e_inner; h_at = 0.5*(h_prev + h_new); e = hw*(e_at +/- z*h_at)
+    int has_boundary;
+    double l_omc, l_c, l_hw, l_z;
+    double r_omc, r_c, r_hw, r_z;
+    int n_src;
+    long long src_cell[kMaxSources];
+    int src_hard[kMaxSources];
+    const double *src_values;  // [num_t][n_src]
+    int n_rec;
+    int rec_q[kMaxRecords], rec_i[kMaxRecords], rec_j[kMaxRecords];
+    long long rec_cell[kMaxRecords];  // -1: whole domain
+    long long rec_every[kMaxRecords];
+    long long rec_cols[kMaxRecords];
+    long long rec_col0[kMaxRecords];  // global cell of column 0
+    double *rec_re[kMaxRecords];
+    double *rec_im[kMaxRecords];
+    unsigned long long step_mask[kMaxTileSteps];  // bit r: record r samples at fused step s
+    unsigned long long check_mask;                // bit s: non-finite scan at fused step s
+    unsigned long long *bad_step;
+    Regions rg;
+};
+
+// two-level splitting in Bloch form (_kernels.py:200-232)
+struct BlochQm {
+    double kz, cz, fxy, ax_c, ax_s, ay_c, ay_s, az_c, az_s, a0_c, a0_s, mu_x, mu_y, mu_z, pol_factor;
+};
+
+struct BlochParams {
+    Launch L;
+    int n_qm;
+    BlochQm qm[kMaxQm];
+};
+
+// dipole weights of the polarisation trace (_kernels.py:360-374), stored
+// densely: pol_re/pol_im per upper pair (row-major i<j), pol_dv per diagonal;
+// entries where mu vanishes are 0 and add exact zeros
+template <int N>
+struct PolTerms {
+    static constexpr int kUpper = N * (N - 1) / 2;
+    double pol_re[kUpper], pol_im[kUpper];
+    double pol_dv[N];
+    double pol_factor;
+};
+
+// N-level Strang splitting (_kernels.py:428-439): B = bc + E * bf
+template <int N>
+struct DenseQm {
+    double pop[N * N], coh[N * N];
+    double bc_re[N * N], bc_im[N * N], bf_re[N * N], bf_im[N * N];
+    PolTerms<N> pol;
+};
+
+// N-level RK4 (_kernels.py:549-557): H = h0 - E mu
+template <int N>
+struct Rk4Qm {
+    double h0_re[N * N], h0_im[N * N], mu_re[N * N], mu_im[N * N];
+    double popm[N * N], deph[N * N];
+    double dt;
+    PolTerms<N> pol;
+};
+
+template <int N, class Q>
+struct DenseParams {
+    Launch L;
+    int n_qm;
+    Q qm[kMaxDenseQm];
+};
+
+// shared helpers (host + device)
+__host__ __device__ inline int region_of(const long long *start, int n, long long m) {
+    int r = 0;
+    for (int q = 1; q < kMaxRegions; ++q) r += (q < n && m >= start[q]) ? 1 : 0;
+    return r;
+}
+
+}  // namespace mbg

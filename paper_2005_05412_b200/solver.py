@@ -1,0 +1,258 @@
+"""GPU drop-in for the reference solver (``FdtdSolver``, solver_fdtd.py:198-498).
+
+``GpuFdtdSolver`` keeps the reference's constructor signature, attributes and
+``run()`` contract (one ``Result`` per record in record order, blocking,
+``SolverError`` on a second call or on a non-finite field, validation before
+any work) and replaces the hot loop with the fused sm_100a kernels of
+``libmbgpu.so``.  Setup arithmetic comes from :mod:`.plan` (a restatement of
+``FdtdSolver.__init__``), so every coefficient the kernels see equals the one
+the reference's numba loops see.
+
+Registered names: ``gpu-fdtd-reg-cayley`` (splitting stepper) and
+``gpu-fdtd-rk4``.  :func:`register_with_reference` adds the same names to the
+reference's own registry so ``mblight.create_solver("gpu-fdtd-reg-cayley", ...)``
+and the mblight CLI resolve to this solver.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import sys
+
+import numpy as np
+
+from . import native
+from .errors import NativeError, SolverError
+from .plan import NONFINITE_CHECK_EVERY, build_plan, resolve_threads, unpack_density
+from .setup_model import Result, register_solver
+
+SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
+
+
+def _result_class(scenario):
+    """Results are built with the caller's own ``Result`` type (reference or mirror)."""
+    mod = sys.modules.get(type(scenario).__module__)
+    cls = getattr(mod, "Result", None) if mod is not None else None
+    return cls if isinstance(cls, type) else Result
+
+
+class GpuFdtdSolver:
+    """One simulation run on a B200; same protocol as the reference's ``FdtdSolver``.
+
+    Extra keyword arguments (all optional):
+      ``tile_steps`` -- time steps fused per kernel launch (k; default per N),
+      ``exact``      -- disable FMA contraction (bit-exact two-level path),
+      ``gpu``        -- CUDA device ordinal.
+    """
+
+    def __init__(self, device, scenario, stepper="splitting", threads=None, seed=None,
+                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0):
+        self.plan = build_plan(device, scenario, stepper, seed)
+        self.device = device
+        self.scenario = scenario
+        self.stepper = stepper
+        self.grid = self.plan.grid
+        self.seed = self.plan.seed
+        self.threads = resolve_threads(threads, self.grid.num_x)
+        self.monitor_invariants = monitor_invariants
+        self.invariant_report = None
+        self.tile_steps = tile_steps
+        self.exact = bool(exact)
+        self.gpu = int(gpu)
+        self.results = None
+        self.launches = 0
+        self.kernel_ms = None
+        self._ran = False
+        self._result_cls = _result_class(scenario)
+        if len(self.plan.plans) > native.MAX_RECORDS:
+            raise ValueError(f"the GPU solver supports at most {native.MAX_RECORDS} records")
+        if len(self.plan.src_cells) > native.MAX_SOURCES:
+            raise ValueError(f"the GPU solver supports at most {native.MAX_SOURCES} sources")
+
+    # -- device setup ------------------------------------------------------
+
+    def _grid_struct(self, win=None, own=None):
+        g = self.grid
+        s = native.MbgGrid()
+        s.num_x, s.num_t, s.dt, s.dx = g.num_x, g.num_t, g.dt, g.dx
+        s.levels = self.plan.levels
+        s.stepper = native.MBG_STEPPER[self.stepper]
+        s.tile_steps = int(self.tile_steps or 0)
+        s.exact = 1 if self.exact else 0
+        s.device = self.gpu
+        s.win_lo, s.win_hi = win if win is not None else (0, g.num_x)
+        s.own_lo, s.own_hi = own if own is not None else (s.win_lo, s.win_hi)
+        return s
+
+    def open_handle(self, win=None, own=None) -> native.Handle:
+        """Create the device solver and upload everything but the initial state."""
+        plan = self.plan
+        h = native.Handle(self._grid_struct(win, own))
+        rt = plan.regions
+        keep = [native.i64(rt.e_start), native.i64(rt.h_start), native.f64(rt.coef_a), native.f64(rt.coef_bg),
+                native.f64(rt.coef_bdx), native.f64(rt.coef_ch), native.i32(rt.qm_index)]
+        h.call("mbg_set_regions", len(rt.e_start), native.ptr(keep[0], native._i64p),
+               native.ptr(keep[1], native._i64p), *[native.ptr(a) for a in keep[2:6]],
+               native.ptr(keep[6], native._i32p))
+        for q, qc in enumerate(plan.qm):
+            self._upload_qm(h, q, qc)
+        if plan.boundary is not None:
+            (wl, cl, zl), (wr, cr, zr) = plan.boundary
+            h.call("mbg_set_boundary", wl, cl, zl, wr, cr, zr)
+        cells, hard, vals = native.i64(plan.src_cells), native.i32(plan.src_hard), native.f64(plan.src_values)
+        h.call("mbg_set_sources", len(cells), native.ptr(cells, native._i64p), native.ptr(hard, native._i32p),
+               native.ptr(vals))
+        ps = plan.plans
+        q = native.i32([p.quantity for p in ps])
+        cell = native.i64([-1 if p.cell is None else p.cell for p in ps])
+        ii, jj = native.i32([p.i for p in ps]), native.i32([p.j for p in ps])
+        every = native.i64([p.every for p in ps])
+        h.call("mbg_set_records", len(ps), native.ptr(q, native._i32p), native.ptr(cell, native._i64p),
+               native.ptr(ii, native._i32p), native.ptr(jj, native._i32p), native.ptr(every, native._i64p))
+        return h
+
+    def _upload_qm(self, h, q, qc):
+        # keep temporaries alive through the call
+        if qc.bloch is not None:
+            b = qc.bloch
+            c = native.f64([b[k] for k in ("kz", "cz", "fxy", "ax_c", "ax_s", "ay_c", "ay_s", "az_c", "az_s",
+                                           "a0_c", "a0_s", "mu_x", "mu_y", "mu_z")] + [qc.pol_factor])
+            h.call("mbg_set_qm_bloch", q, native.ptr(c))
+            return
+        args = self._pol_args(qc)
+        if qc.h0 is not None:
+            mats = [native.f64(np.ascontiguousarray(qc.h0, complex).view(np.float64)),
+                    native.f64(np.ascontiguousarray(qc.mu, complex).view(np.float64)),
+                    native.f64(qc.pop_matrix), native.f64(qc.deph_matrix)]
+            h.call("mbg_set_qm_rk4", q, *[native.ptr(m) for m in mats], *args[0])
+        else:
+            mats = [native.f64(qc.pop_half), native.f64(qc.coh_half),
+                    native.f64(np.ascontiguousarray(qc.b_const, complex).view(np.float64)),
+                    native.f64(np.ascontiguousarray(qc.b_field, complex).view(np.float64))]
+            h.call("mbg_set_qm_dense", q, *[native.ptr(m) for m in mats], *args[0])
+
+    @staticmethod
+    def _pol_args(qc):
+        pi = native.i32(qc.pol_i if len(qc.pol_i) else [0])
+        pj = native.i32(qc.pol_j if len(qc.pol_j) else [0])
+        pv = native.f64(np.asarray(qc.pol_v, dtype=complex).view(np.float64) if len(qc.pol_v) else [0.0, 0.0])
+        di = native.i32(qc.pol_di if len(qc.pol_di) else [0])
+        dv = native.f64(qc.pol_dv if len(qc.pol_dv) else [0.0])
+        keep = (pi, pj, pv, di, dv)
+        return ((len(qc.pol_i), native.ptr(pi, native._i32p), native.ptr(pj, native._i32p), native.ptr(pv),
+                 len(qc.pol_di), native.ptr(di, native._i32p), native.ptr(dv), qc.pol_factor), keep)
+
+    def upload_initial_state(self, h, win=None):
+        lo, hi = win if win is not None else (0, self.grid.num_x)
+        e = native.f64(self.plan.e_init[lo:hi])
+        hf = native.f64(self.plan.h_init[lo:hi + 1])
+        h.call("mbg_upload_fields", native.ptr(e), native.ptr(hf))
+        if self.plan.levels:
+            w = native.f64(self.plan.rho_init_packed())
+            h.call("mbg_upload_density", native.ptr(w))
+
+    def download_results(self, h):
+        out = []
+        for r, p in enumerate(self.plan.plans):
+            re = np.zeros((p.rows, p.cols))
+            im = np.zeros((p.rows, p.cols)) if p.is_complex else None
+            h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
+            data = re if im is None else re + 1j * im
+            out.append(p.to_result(self.grid, data, self._result_cls))
+        return out
+
+    # -- run ------------------------------------------------------------------
+
+    def run(self):
+        """Execute the run; returns one Result per record (``solver_fdtd.py:444-455``)."""
+        if self._ran:
+            raise SolverError("run() may only be called once per solver instance")
+        self._ran = True
+        h = self.open_handle()
+        try:
+            self.upload_initial_state(h)
+            self._run_on(h)
+            self.results = self.download_results(h)
+        finally:
+            h.close()
+        return self.results
+
+    def _run_on(self, h, poll_every: int = 1 << 14):
+        """Sample row 0, then advance steps 1..num_t-1 in chunks, polling the
+        device-side non-finite flag between chunks (a chunk is a multiple of the
+        1024-step scan cadence, so the first failing scan is the one reported)."""
+        num_t = self.grid.num_t
+        h.call("mbg_sample", 0)
+        monitor = self._monitor_cadence()
+        if monitor is not None:
+            self._update_invariants(h)
+        chunk = poll_every if monitor is None else max(1, monitor)
+        n = 1
+        h.call("mbg_event_begin")
+        while n < num_t:
+            cnt = min(chunk, num_t - n)
+            h.call("mbg_advance", n, cnt)
+            n += cnt
+            bad = C.c_int64(-1)
+            h.call("mbg_poll_nonfinite", C.byref(bad))
+            if bad.value >= 0:
+                raise SolverError(f"non-finite electric field at step {bad.value}")
+            if monitor is not None and (n - 1) % monitor == 0:
+                self._update_invariants(h)
+        ms = C.c_float(0)
+        h.call("mbg_event_end", C.byref(ms))
+        self.kernel_ms = float(ms.value)
+        launches = C.c_int64(0)
+        h.call("mbg_launch_count", C.byref(launches))
+        self.launches = int(launches.value)
+
+    # -- invariant monitor (solver_fdtd.py:306-308, 425-440) ---------------------
+
+    def _monitor_cadence(self):
+        if not self.monitor_invariants or not self.plan.levels:
+            return None
+        return min((p.every for p in self.plan.plans), default=256)
+
+    def _update_invariants(self, h):
+        plan = self.plan
+        nx = self.grid.num_x
+        words = np.zeros((plan.state_words, nx))
+        h.call("mbg_download_state", native.ptr(words))
+        qcells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in plan.groups]) if plan.groups else np.zeros(0, int)
+        rho = unpack_density(words[:, qcells], plan.levels, plan.stepper)
+        rep = self.invariant_report
+        if rep is None:
+            rep = self.invariant_report = {"max_trace_dev": 0.0, "max_herm_dev": 0.0, "min_eigenvalue": math.inf}
+        if plan.levels == 2 and plan.stepper == "splitting":
+            norms = np.sqrt(np.sum(words[:, qcells] ** 2, axis=0))
+            tr, he, me = 0.0, 0.0, 0.5 * (1.0 - float(np.max(norms)))
+        else:
+            tr = float(np.max(np.abs(np.trace(rho, axis1=1, axis2=2) - 1.0)))
+            adj = rho.conj().transpose(0, 2, 1)
+            he = float(np.max(np.abs(rho - adj)))
+            me = float(np.min(np.linalg.eigvalsh(0.5 * (rho + adj))))
+        rep["max_trace_dev"] = max(rep["max_trace_dev"], tr)
+        rep["max_herm_dev"] = max(rep["max_herm_dev"], he)
+        rep["min_eigenvalue"] = min(rep["min_eigenvalue"], me)
+
+
+def _rk4_factory(device, scenario, **kw):
+    return GpuFdtdSolver(device, scenario, stepper="rk4", **kw)
+
+
+def register(registry_fn=register_solver):
+    registry_fn("gpu-fdtd-reg-cayley", GpuFdtdSolver)
+    registry_fn("gpu-fdtd-rk4", _rk4_factory)
+
+
+def register_with_reference(mblight_module=None):
+    """Register the GPU solver names in the reference's own registry
+    (``mblight.core.register_solver``, core.py:617)."""
+    if mblight_module is None:
+        import mblight as mblight_module  # noqa: PLC0415
+    register(mblight_module.register_solver)
+    return mblight_module
+
+
+register()

@@ -1,0 +1,202 @@
+"""Named parity cases, buildable through either setup API.
+
+Each case is ``name -> (builder(api) -> (device, scenario), stepper)``.  The
+golden generator (``tests/golden/make_golden.py``) runs them through the
+reference ``mblight`` in this container; the tests rebuild the identical
+setups through ``paper_2005_05412_b200`` on any box and compare.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2005_05412_b200 import configs
+
+
+def _diagonal_basis(n):
+    rows = np.zeros((n - 1, n))
+    for k in range(1, n):
+        s = 1.0 / np.sqrt(k * (k + 1))
+        rows[k - 1, :k] = s
+        rows[k - 1, k] = -k * s
+    return rows
+
+
+def random_medium(api, rng, dim, rate_scale=1e11, freq_scale=1e14, dipole_scale=1e-29, density=1e24):
+    """Random valid N-level description; same draw sequence as the reference's
+    test helper ``random_description`` (pkg/tests/conftest.py:49-73)."""
+    n_off = dim * (dim - 1) // 2
+    energies = np.sort(rng.uniform(0.0, 1.0, dim)) * api.HBAR * freq_scale
+    off_h = (rng.standard_normal(n_off) + 1j * rng.standard_normal(n_off)) * api.HBAR * freq_scale * 0.05
+    off_mu = (rng.standard_normal(n_off) + 1j * rng.standard_normal(n_off)) * dipole_scale
+    rates = rng.uniform(0.0, 1.0, (dim, dim)) * rate_scale
+    np.fill_diagonal(rates, 0.0)
+    basis = _diagonal_basis(dim)
+    coeffs = rng.uniform(0.0, 1.0, dim - 1) * rate_scale
+    pairs = [(i, j) for j in range(1, dim) for i in range(j)]
+    deph = np.array([0.5 * np.sum(coeffs * (basis[:, i] - basis[:, j]) ** 2) for i, j in pairs])
+    return api.QmDescription(
+        density, api.QmOperator(energies, off_h), api.QmOperator(np.zeros(dim), off_mu),
+        api.LindbladRelaxation(rates, deph))
+
+
+def random_case(dim, seed, nx=512, end=20e-15, whole=False, stepper="splitting"):
+    def build(api):
+        rng = np.random.default_rng(seed)
+        desc = random_medium(api, rng, dim)
+        act = api.ensure_material(api.Material(f"Rand{dim}_{seed}", qm=desc))
+        vac = api.ensure_material(api.Material("Vacuum"))
+        dev = api.Device(f"rand{dim}")
+        dev.add_region(api.Region("v", vac.id, 0.0, 5e-6))
+        dev.add_region(api.Region("a", act.id, 5e-6, 20e-6))
+        rho0 = np.zeros(dim)
+        rho0[0] = 1.0
+        sce = api.Scenario("s", nx, end, api.QmOperator(rho0))
+        sce.add_source(api.SechPulse("sech", 0.0, "hard", 1e9, 2e14, 5.0, 1e15))
+        iv = 0.0 if whole else 1e-15
+        sce.add_record(api.Record("e", quantity="e", interval=iv))
+        sce.add_record(api.Record("d1n", quantity="d", i=1, j=dim, interval=iv))
+        sce.add_record(api.Record("d22", quantity="d", i=2, j=2, interval=iv, position=12e-6))
+        sce.add_record(api.Record("dn1", quantity="d", i=dim, j=1, interval=iv, position=10e-6))
+        sce.add_record(api.Record("h", quantity="h", interval=iv, position=9e-6))
+        return dev, sce
+    return build, stepper
+
+
+def sit_hard_whole(api):
+    """Ziolkowski-like SIT with a hard source; whole-domain e/inv/h records."""
+    qm = api.two_level_description(1e24, 2.0 * math.pi * 2e14, 6.24e-11, 1.0e10, 1.0e10, -1.0)
+    vac = api.ensure_material(api.Material("Vacuum"))
+    act = api.ensure_material(api.Material("AR_Z", qm=qm))
+    dev = api.Device("Z")
+    dev.add_region(api.Region("l", vac.id, 0.0, 7.5e-6))
+    dev.add_region(api.Region("a", act.id, 7.5e-6, 142.5e-6))
+    dev.add_region(api.Region("r", vac.id, 142.5e-6, 150e-6))
+    sce = api.Scenario("s", 1024, 150e-15, api.QmOperator([1.0, 0.0]),
+                       ic_h_field=api.RandomField(1e-3, seed=5))
+    sce.add_source(api.SechPulse("sech", position=0.0, kind="hard", amplitude=4.2186e9,
+                                 carrier_freq=2e14, envelope_shift=10.0, envelope_rate=2e14))
+    sce.add_record(api.Record("e", quantity="e", interval=5e-15))
+    sce.add_record(api.Record("inv", quantity="inv", interval=5e-15))
+    sce.add_record(api.Record("h", quantity="h", interval=5e-15))
+    sce.add_record(api.Record("d12", quantity="d", i=1, j=2, position=30e-6))
+    sce.add_record(api.Record("d21", quantity="d", i=2, j=1, position=30e-6))
+    sce.add_record(api.Record("h0", quantity="h", position=0.0))
+    return dev, sce
+
+
+def multi_material(api):
+    """Two distinct two-level media, a lossy dielectric, partial mirrors, an
+    off-edge soft source, loss and overlap factors in play."""
+    qa = api.two_level_description(1e24, 2.0 * math.pi * 2e14, 6.24e-11, 1e11, 2e12, -1.0)
+    qb = api.two_level_description(5e23, 2.0 * math.pi * 1.8e14, 8e-11, 1e10, 1e12, 0.5)
+    vac = api.ensure_material(api.Material("Vacuum"))
+    a = api.ensure_material(api.Material("MA", qm=qa))
+    gl = api.ensure_material(api.Material("Glass", rel_permittivity=2.25, losses=500.0))
+    b = api.ensure_material(api.Material("MB", rel_permittivity=1.5, overlap_factor=0.5, losses=1e3, qm=qb))
+    dev = api.Device("multi", bc_left=api.BoundaryReflectivity(0.25), bc_right=api.BoundaryReflectivity(0.64))
+    for name, mat, x0, x1 in (("v", vac, 0.0, 4e-6), ("a", a, 4e-6, 20e-6), ("g", gl, 20e-6, 26e-6),
+                              ("b", b, 26e-6, 40e-6), ("v2", vac, 40e-6, 44e-6)):
+        dev.add_region(api.Region(name, mat.id, x0, x1))
+    sce = api.Scenario("s", 3000, 200e-15, api.QmOperator([0.9, 0.1], [0.2 - 0.1j]),
+                       ic_e_field=api.RandomField(1e5, seed=3))
+    sce.add_source(api.SechPulse("s1", 2e-6, "soft", 3e9, 2e14, 8.0, 1e14))
+    sce.add_source(api.GaussianPulse("s2", 2e-6, "soft", 1e9, 1.8e14, 60e-15, 20e-15))
+    sce.add_record(api.Record("e", quantity="e", interval=20e-15))
+    sce.add_record(api.Record("inv", quantity="inv", interval=20e-15))
+    for x in (1e-6, 10e-6, 23e-6, 30e-6, 43.9e-6):
+        sce.add_record(api.Record(f"e@{x}", quantity="e", position=x))
+        sce.add_record(api.Record(f"d12@{x}", quantity="d", i=1, j=2, position=x, interval=1e-15))
+    return dev, sce
+
+
+def vacuum_sources(api):
+    """No quantum material: reflectivity mix, hard + soft sources, CurveField ICs."""
+    vac = api.ensure_material(api.Material("Vacuum"))
+    die = api.ensure_material(api.Material("Die", rel_permittivity=4.0, rel_permeability=1.2, losses=100.0))
+    dev = api.Device("vac", bc_left=api.BoundaryReflectivity(0.3), bc_right=api.BoundaryReflectivity(0.7))
+    dev.add_region(api.Region("v", vac.id, 0.0, 20e-6))
+    dev.add_region(api.Region("d", die.id, 20e-6, 40e-6))
+    nx = 1500
+    x = np.arange(nx) / (nx - 1)
+    sce = api.Scenario("s", nx, 300e-15, api.QmOperator([1.0, 0.0]),
+                       ic_e_field=api.CurveField(np.sin(7 * np.pi * x) * 1e3),
+                       ic_h_field=api.CurveField(np.cos(5 * np.pi * x)))
+    sce.add_source(api.SechPulse("hard", 10e-6, "hard", 1.0, 2e14, 10.0, 2e14))
+    sce.add_source(api.GaussianPulse("soft", 10e-6, "soft", 2.0, 1e14, 100e-15, 30e-15))
+    sce.add_record(api.Record("e", quantity="e", interval=20e-15))
+    sce.add_record(api.Record("h", quantity="h", interval=20e-15))
+    sce.add_record(api.Record("edge", quantity="e", position=40e-6))
+    return dev, sce
+
+
+def tiny_group(api):
+    """A 20-cell two-level group: the reference steps it with ScalarKernel."""
+    qm = api.two_level_description(1e24, 2.0 * math.pi * 2e14, 6.24e-11, 1e10, 1e11, -1.0)
+    vac = api.ensure_material(api.Material("Vacuum"))
+    act = api.ensure_material(api.Material("Tiny", qm=qm))
+    dev = api.Device("tiny")
+    dev.add_region(api.Region("v", vac.id, 0.0, 10e-6))
+    dev.add_region(api.Region("a", act.id, 10e-6, 10.4e-6))
+    dev.add_region(api.Region("v2", vac.id, 10.4e-6, 20e-6))
+    sce = api.Scenario("s", 1024, 100e-15, api.QmOperator([1.0, 0.0]))
+    sce.add_source(api.SechPulse("s", 0.0, "hard", 4e9, 2e14, 5.0, 2e14))
+    sce.add_record(api.Record("e", quantity="e", interval=2e-15))
+    sce.add_record(api.Record("inv", quantity="inv", position=10.2e-6))
+    return dev, sce
+
+
+CASES = {
+    # BASELINE configs (full or reduced grids)
+    "cfg1_full": (lambda api: configs.cfg1(api), "splitting"),
+    "cfg2_r16": (lambda api: configs.cfg2(api, nx=1 << 16, steps=20000, stress=True), "splitting"),
+    "cfg2_full": (lambda api: configs.cfg2(api), "splitting"),
+    "cfg2_stress_full": (lambda api: configs.cfg2(api, stress=True), "splitting"),
+    "cfg3_r16": (lambda api: configs.cfg3(api, nx=1 << 16, steps=50000, cells=(4096, 12288, 20000)), "splitting"),
+    "cfg3_r16_stress": (lambda api: configs.cfg3(api, nx=1 << 16, steps=50000, stress=True), "splitting"),
+    "cfg4_r14": (lambda api: configs.cfg4(api, nx=1 << 14, steps=100000), "splitting"),
+    # feature coverage
+    "sit_hard_whole": (sit_hard_whole, "splitting"),
+    "multi_material": (multi_material, "splitting"),
+    "vacuum_sources": (vacuum_sources, "splitting"),
+    "tiny_group": (tiny_group, "splitting"),
+}
+for _n in (3, 4, 5, 6, 7, 8):
+    CASES[f"rand{_n}_split"] = random_case(_n, 30 + _n)
+for _n in (2, 3, 4):
+    CASES[f"rand{_n}_rk4"] = random_case(_n, 60 + _n, stepper="rk4")
+CASES["rand2_split"] = random_case(2, 32)
+
+def kernel_case(dim, seed, stepper="splitting", nx=64):
+    """One time step over nx cells with random E: isolates the per-cell
+    stepper (the scenario-level twin of pkg/tests/test_solver.py:437-480)."""
+    def build(api):
+        rng = np.random.default_rng(seed)
+        desc = random_medium(api, rng, dim)
+        a = rng.standard_normal((dim, dim)) + 1j * rng.standard_normal((dim, dim))
+        rho = a @ a.conj().T
+        rho = rho / np.trace(rho).real
+        e_vals = rng.uniform(-5e9, 5e9, nx)
+        act = api.ensure_material(api.Material(f"K{dim}_{seed}", qm=desc))
+        dev = api.Device("k")
+        dev.add_region(api.Region("a", act.id, 0.0, 1e-6))
+        end = 0.5 * (1e-6 / (nx - 1)) / api.C0  # exactly one step
+        sce = api.Scenario("k", nx, end, api.QmOperator.from_matrix(rho), ic_e_field=api.CurveField(e_vals))
+        for i in range(1, dim + 1):
+            for j in range(i, dim + 1):
+                sce.add_record(api.Record(f"d{i}{j}", quantity="d", i=i, j=j))
+        sce.add_record(api.Record(f"d{dim}1", quantity="d", i=dim, j=1))
+        sce.add_record(api.Record("e", quantity="e"))
+        return dev, sce
+    return build, stepper
+
+
+for _n in range(2, 9):
+    CASES[f"kernel{_n}_split"] = kernel_case(_n, 100 + _n)
+for _n in (2, 3, 4, 5):
+    CASES[f"kernel{_n}_rk4"] = kernel_case(_n, 200 + _n, stepper="rk4")
+
+# cases whose reference run takes minutes; generated once, marked slow
+SLOW = {"cfg2_full", "cfg2_stress_full", "cfg3_r16", "cfg3_r16_stress", "cfg4_r14"}
