@@ -1,0 +1,363 @@
+"""Benchmark of the time-stepping core (BASELINE.json metric: cell-updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+
+Workload (BASELINE.json configs[1], "cfg2"): two-level SIT medium, Nx = 2^22
+cells (x N for --gpus N: weak scaling, 2^22 cells per GPU), 20000 time steps
+with T1 = 1 ns / T2 = 1 ps relaxation, seeded synthetic initial inversion,
+3 point records x 4 quantities every 100 steps.  One bench "step" is one full
+20000-time-step run of that scenario from its initial condition: restore the
+initial state (device-to-device), sample row 0, run every fused launch.
+
+``value`` is device time (CUDA events on the launch stream, max over ranks)
+with the state resident in HBM; ``e2e`` times the public API call
+(``GpuFdtdSolver.run``) which uploads the initial fields from the host and
+downloads the records every step.  ``--impl reference`` times the CPU
+restatement of the reference algorithm (oracle/, a port: the reference is
+Python+numba and cannot be shipped to the GPU box) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "cell-updates/sec (fp64, N-level) at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "cell-updates/s"
+
+
+# ----------------------------------------------------------------- helpers --
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_workload(mb, gpus):
+    from paper_2005_05412_b200 import configs
+
+    mb.clear_material_library()
+    if gpus == 1:
+        return configs.cfg2(mb)
+    # weak scaling: 2^22 cells and 150 um per GPU, same medium and grid spacing
+    return configs.cfg2(mb, nx=(1 << 22) * gpus, length_scale=gpus)
+
+
+def algorithmic_per_cell(plan):
+    """bytes B and flops F per cell-update (k = 1)."""
+    nx = plan.grid.num_x
+    qcells = sum(hi - lo for lo, hi, _ in plan.groups)
+    fq = qcells / nx
+    n = plan.levels
+    sn = plan.state_words
+    b = 32 + fq * 16 * sn
+    if n == 2:
+        fn = 82
+    elif n == 0:
+        fn = 9
+    else:
+        nnz_off = int(np.count_nonzero(plan.qm[0].pol_v))
+        nnz_d = len(plan.qm[0].pol_di)
+        fn = 12 * n * n + 4 * n * n
+        fn += sum(6 + (n - k - 1) * (6 + 8 * (n - k - 1) + 8 * n) for k in range(n))
+        fn += sum(6 + n * (8 * (n - 1 - k) + 6) for k in range(n))
+        fn += 8 * n ** 3 + 4 * n * n * (n + 1) + 10 * nnz_off + 3 * nnz_d + 1 + 9
+    f = 9 + fq * (fn - 9)
+    return b, f, fq
+
+
+def measured_hbm_gbs():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config_key):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(config_key, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# -------------------------------------------------------------- reference --
+
+def run_reference(args, world, rank):
+    """CPU restatement of the reference loop (oracle/, kind 'port') on all host cores."""
+    if rank != 0:
+        return 0
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+
+    import paper_2005_05412_b200 as mb
+    from paper_2005_05412_b200.plan import build_plan
+
+    dev, sce = build_workload(mb, args.gpus)
+    plan = build_plan(dev, sce)
+    threads = os.cpu_count() or 1
+    sample = args.cpu_steps
+    nx = plan.grid.num_x
+    for _ in range(args.warmup):
+        orc.OracleRun(plan, threads=threads, step_limit=max(1, sample // 10)).run()
+    t = 0.0
+    for _ in range(args.steps):
+        run = orc.OracleRun(plan, threads=threads, step_limit=sample)
+        t0 = time.perf_counter()
+        bad = run.run()
+        t += time.perf_counter() - t0
+        assert bad == 0
+    value = nx * sample * args.steps / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(plan, args, None),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} of {plan.grid.num_t - 1} time steps at full Nx={nx} per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(plan, args, k):
+    return {
+        "workload": "cfg2 (BASELINE configs[1]): two-level SIT, T1=1ns T2=1ps, Strang splitting, "
+                    "soft sech source, 3 point records x 4 quantities every 100 steps",
+        "num_x": plan.grid.num_x, "time_steps": plan.grid.num_t - 1, "levels": plan.levels,
+        "tile_steps": k, "exact": bool(args.exact),
+        "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single-gpu",
+        "l2": "inputs larger than L2 (E/H/Bloch state ping-pong ~335 MB per GPU vs 126 MB L2)",
+    }
+
+
+# ------------------------------------------------------------------- mine --
+
+def run_mine(args, world, rank, local):
+    import ctypes as C
+
+    import paper_2005_05412_b200 as mb
+    from paper_2005_05412_b200 import native
+
+    dev, sce = build_workload(mb, args.gpus)
+    if world > 1:
+        from paper_2005_05412_b200 import slabs
+        return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT)
+
+    solver = mb.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+    plan = solver.plan
+    num_t = plan.grid.num_t
+    nx = plan.grid.num_x
+    h = solver.open_handle()
+    solver.upload_initial_state(h)
+    h.call("mbg_checkpoint_save")
+    k = C.c_int32(0)
+    h.call("mbg_tile_steps", C.byref(k))
+    k = k.value
+
+    def one_step():
+        h.call("mbg_checkpoint_restore")
+        h.call("mbg_sample", 0)
+        h.call("mbg_advance", 1, num_t - 1)
+
+    for _ in range(args.warmup):
+        one_step()
+    h.call("mbg_synchronize")
+    l0 = C.c_int64(0)
+    h.call("mbg_launch_count", C.byref(l0))
+    with ClockSampler(local) as clocks:
+        h.call("mbg_event_begin")
+        for _ in range(args.steps):
+            one_step()
+        ms = C.c_float(0)
+        h.call("mbg_event_end", C.byref(ms))
+    ms = float(ms.value)
+    l1 = C.c_int64(0)
+    h.call("mbg_launch_count", C.byref(l1))
+    launches = l1.value - l0.value
+    bad = C.c_int64(0)
+    h.call("mbg_poll_nonfinite", C.byref(bad))
+    assert bad.value < 0, "non-finite field in the benchmark run"
+    h.close()
+
+    cell_updates = nx * (num_t - 1) * args.steps
+    value = cell_updates / (ms * 1e-3)
+
+    # roofline of the fused step kernel (dominant: it is every launch but the row-0 sample)
+    b, f, fq = algorithmic_per_cell(plan)
+    peak_fp64 = C.c_double(0)
+    native.load().mbg_fp64_peak(local, C.byref(peak_fp64))
+    peak_fp64 = peak_fp64.value
+    bw, bw_src = measured_hbm_gbs()
+    per_launch_ms = ms / launches
+    cells_per_launch = cell_updates / launches  # = nx * k on average
+    flops_launch = f * cells_per_launch
+    bytes_launch = b * nx
+    t_hbm = bytes_launch / (bw * 1e9)
+    t_fp = flops_launch / (peak_fp64 * 1e12)
+    bound = "fp64" if t_fp >= t_hbm else "hbm"
+    if bound == "fp64":
+        achieved = flops_launch / (per_launch_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+                "frac": achieved / peak_fp64}
+    else:
+        achieved = bytes_launch / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": bw, "unit": "GB/s", "frac": achieved / bw}
+    traffic = ncu_traffic(f"cfg2_k{k}")
+    roof.update({
+        "traffic": traffic,
+        "kernel": "bloch_step_kernel (fused H + Bloch + E + boundary + sources + records, k steps/launch)",
+        "algorithmic_bytes_per_cell_update_k1": b, "algorithmic_flops_per_cell_update": f,
+        "bytes_per_launch": bytes_launch, "flops_per_launch": flops_launch,
+        "launch_ms_avg": per_launch_ms, "hbm_achieved_gbs": bytes_launch / (per_launch_ms * 1e-3) / 1e9,
+        "hbm_peak_gbs": bw, "hbm_peak_source": bw_src, "fp64_peak_tflops": peak_fp64,
+        "fp64_peak_source": "measured in-run (mbg_fp64_peak: DFMA chains on all SMs)",
+        "roofline_cell_updates_per_s": min(bw * 1e9 * k / b, peak_fp64 * 1e12 / f),
+    })
+
+    # e2e through the public API: upload ICs, run, download records, every step
+    e2e_times = []
+    h2d = d2h = 0
+    for it in range(args.warmup + args.steps):
+        mb.clear_material_library()
+        d2, s2 = build_workload(mb, 1)
+        sol = mb.GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+        t0 = time.perf_counter()
+        res = sol.run()
+        dt_run = time.perf_counter() - t0
+        if it >= args.warmup:
+            e2e_times.append(dt_run)
+        if it == 0:
+            p = sol.plan
+            h2d = 8 * (p.grid.num_x + (p.grid.num_x + 1) + 1 + p.state_words + p.src_values.size)
+            d2h = sum(r.data.size * (16 if r.is_complex else 8) for r in res) + 8 * max(1, (num_t - 1) // (1 << 14))
+    e2e_value = cell_updates / sum(e2e_times)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(plan, args.cpu_steps)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(plan, args, k),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches + 2 * args.steps),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(plan, steps):
+    """The oracle (port of the reference loop) on this box's host cores, bounded sample."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as orc
+
+    threads = os.cpu_count() or 1
+    orc.OracleRun(plan, threads=threads, step_limit=5).run()  # warm
+    run = orc.OracleRun(plan, threads=threads, step_limit=steps)
+    t0 = time.perf_counter()
+    bad = run.run()
+    t = time.perf_counter() - t0
+    assert bad == 0
+    return {"value": plan.grid.num_x * steps / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{steps} of {plan.grid.num_t - 1} time steps of the same workload at full "
+                      f"Nx={plan.grid.num_x} ({t:.1f} s, OpenMP C restatement, oracle/mb_oracle.c)"}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("mine", "reference"), default="mine")
+    ap.add_argument("--tile-steps", type=int, default=None)
+    ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=300)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    world, rank, local = dist_env()
+    if world > 1 and args.gpus != world:
+        args.gpus = world
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_mine(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

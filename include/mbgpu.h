@@ -134,6 +134,15 @@ int mbg_halo_words(const mbg_solver *s, int32_t *words);
 int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
 int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
 
+/* device-side checkpoint of E, H and the density state (save / restore the
+ * current buffers; no reference analogue: FdtdSolver has no checkpointing) */
+int mbg_checkpoint_save(mbg_solver *s);
+int mbg_checkpoint_restore(mbg_solver *s);
+
+/* measured FP64 FMA throughput of the device (TFLOP/s), the FP64 roofline
+ * denominator: independent DFMA chains on every SM, timed with CUDA events */
+int mbg_fp64_peak(int device, double *tflops);
+
 /* timing helpers for bench.py: device time of the launches issued by
  * mbg_advance between mark_begin/mark_end (CUDA events on the solver stream) */
 int mbg_event_begin(mbg_solver *s);

@@ -62,6 +62,7 @@ struct mbg_solver {
     double *src_values = nullptr;
     std::vector<Rec> recs;
     unsigned long long *bad = nullptr;
+    double *ck_e = nullptr, *ck_h = nullptr, *ck_s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     long long launches = 0;
     std::string err;
@@ -304,6 +305,9 @@ void mbg_destroy(mbg_solver *s) {
         cudaFree(s->s[b]);
     }
     cudaFree(s->bad);
+    cudaFree(s->ck_e);
+    cudaFree(s->ck_h);
+    cudaFree(s->ck_s);
     cudaFree(s->src_values);
     for (auto &r : s->recs) {
         cudaFree(r.re);
@@ -499,10 +503,11 @@ int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *c
 int mbg_upload_fields(mbg_solver *s, const double *e, const double *h) {
     if (!s || !e || !h) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
-    for (int b = 0; b < 2; ++b) {
-        CK(cudaMemcpyAsync(s->e[b], e, sizeof(double) * s->win_n, cudaMemcpyHostToDevice, s->stream));
-        CK(cudaMemcpyAsync(s->h[b], h, sizeof(double) * (s->win_n + 1), cudaMemcpyHostToDevice, s->stream));
-    }
+    // only the current buffer: every launch writes all of its result cells into
+    // the other one, and node win_hi of H (never updated) is zeroed at create
+    CK(cudaMemcpyAsync(s->e[s->cur], e, sizeof(double) * s->win_n, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->h[s->cur], h, sizeof(double) * (s->win_n + 1), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->h[1 - s->cur] + s->win_n, h + s->win_n, sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return MBG_OK;
 }
@@ -515,8 +520,7 @@ int mbg_upload_density(mbg_solver *s, const double *words) {
     double *w = nullptr;
     CK(cudaMalloc(&w, sizeof(double) * s->words));
     CK(cudaMemcpy(w, words, sizeof(double) * s->words, cudaMemcpyHostToDevice));
-    for (int b = 0; b < 2; ++b)
-        CK(launch_broadcast_state(s->s[b], s->plane, s->win_n, s->words, w, s->rg, s->g.win_lo, s->stream));
+    CK(launch_broadcast_state(s->s[s->cur], s->plane, s->win_n, s->words, w, s->rg, s->g.win_lo, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     cudaFree(w);
     return MBG_OK;
@@ -525,10 +529,9 @@ int mbg_upload_density(mbg_solver *s, const double *words) {
 int mbg_upload_state(mbg_solver *s, const double *planes) {
     if (!s || !planes) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
-    for (int b = 0; b < 2; ++b)
-        for (int w = 0; w < s->words; ++w)
-            CK(cudaMemcpyAsync(s->s[b] + w * s->plane, planes + w * s->win_n, sizeof(double) * s->win_n,
-                               cudaMemcpyHostToDevice, s->stream));
+    for (int w = 0; w < s->words; ++w)
+        CK(cudaMemcpyAsync(s->s[s->cur] + w * s->plane, planes + w * s->win_n, sizeof(double) * s->win_n,
+                           cudaMemcpyHostToDevice, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return MBG_OK;
 }
@@ -658,6 +661,45 @@ static int halo(mbg_solver *s, bool pack, int64_t cell0, int64_t count, uint64_t
 
 int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, true, cell0, count, buf); }
 int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, false, cell0, count, buf); }
+
+int mbg_checkpoint_save(mbg_solver *s) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    const size_t fb = sizeof(double) * (s->win_n + 1);
+    const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
+    if (!s->ck_e) {
+        CK(cudaMalloc(&s->ck_e, fb));
+        CK(cudaMalloc(&s->ck_h, fb));
+        CK(cudaMalloc(&s->ck_s, sb));
+    }
+    CK(cudaMemcpyAsync(s->ck_e, s->e[s->cur], fb, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->ck_h, s->h[s->cur], fb, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->ck_s, s->s[s->cur], sb, cudaMemcpyDeviceToDevice, s->stream));
+    return MBG_OK;
+}
+
+int mbg_checkpoint_restore(mbg_solver *s) {
+    if (!s) return MBG_E_ARG;
+    if (!s->ck_e) return fail(s, MBG_E_STATE, "no checkpoint saved");
+    cudaSetDevice(s->g.device);
+    const size_t fb = sizeof(double) * (s->win_n + 1);
+    const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
+    CK(cudaMemcpyAsync(s->e[s->cur], s->ck_e, fb, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->h[s->cur], s->ck_h, fb, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->s[s->cur], s->ck_s, sb, cudaMemcpyDeviceToDevice, s->stream));
+    CK(cudaMemsetAsync(s->bad, 0xff, sizeof(unsigned long long), s->stream));
+    return MBG_OK;
+}
+
+int mbg_fp64_peak(int device, double *tflops) {
+    mbg_solver *s = nullptr;
+    if (!tflops) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    double ms = 0.0, flops = 0.0;
+    CK(measure_fp64_peak(&ms, &flops));
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return MBG_OK;
+}
 
 int mbg_event_begin(mbg_solver *s) {
     if (!s) return MBG_E_ARG;

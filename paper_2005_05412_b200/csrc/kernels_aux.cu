@@ -88,9 +88,54 @@ __global__ void halo_kernel(bool pack, double *e, double *h, double *s, long lon
         *p = buf[t];
 }
 
+// 16 independent FMA chains per thread keep the DFMA pipe busy
+__global__ void __launch_bounds__(256) fp64_fma_kernel(double *out, int iters, double m, double c) {
+    double a[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = 1e-3 * (threadIdx.x + k);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a[k] = fma(a[k], m, c);
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sum += a[k];
+    if (sum == 12345.678) out[0] = sum;  // keep the chains alive
+}
+
 unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 }  // namespace
+
+cudaError_t measure_fp64_peak(double *ms, double *flops) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double *out = nullptr;
+    cudaError_t err = cudaMalloc(&out, sizeof(double));
+    if (err != cudaSuccess) return err;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        cudaEventRecord(a);
+        fp64_fma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, a, b);
+        if (rep > 0 && t < best) best = t;
+    }
+    err = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *ms = best;
+    *flops = 2.0 * 16.0 * iters * (double)blocks * threads;
+    return err;
+}
 
 cudaError_t launch_sample(const Launch &L, const void *, int levels, int bloch, long long step, cudaStream_t st) {
     if (L.win_n <= 0) return cudaSuccess;

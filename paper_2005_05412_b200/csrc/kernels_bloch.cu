@@ -209,17 +209,131 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
     }
 }
 
-__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32)
-bloch_step_kernel(const __grid_constant__ BlochParams P) {
+// Interior tiles (the overwhelming majority): every slot is a regular cell of
+// the window (1 <= c <= Nx-2), one E region and one H region, no source and no
+// boundary cell.  No per-slot predicates, scalar coefficients, and for a single
+// quantum material the stepper constants are constant-bank operands.
+template <bool QM, bool ONE_QM>
+__device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
+                                              int lane, int r_e, int r_h) {
+    const Launch &L = P.L;
+    const double a = L.rg.a[r_e], bg = L.rg.bg[r_e], bdx = L.rg.bdx[r_e], ch = L.rg.ch[r_h];
+    const int qmi = QM ? (ONE_QM ? 0 : L.rg.qm[r_e]) : 0;
+    const BlochQm &q = P.qm[qmi];
+    const long long l0 = base - L.win_lo + lane;
+    double E[C], H[C], X[C], Y[C], Z[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        E[i] = L.e_in[l0 + i * 32];
+        H[i] = L.h_in[l0 + i * 32];
+        if (QM) {
+            X[i] = L.s_in[l0 + i * 32];
+            Y[i] = L.s_in[L.plane + l0 + i * 32];
+            Z[i] = L.s_in[2 * L.plane + l0 + i * 32];
+        }
+    }
+    for (int s = 0; s < L.k; ++s) {
+        // H update in slot order; lane 0 takes E[m-1] from lane 31 of the previous row
+        double Hn[C];
+        double t_prev = __shfl_sync(kFull, E[0], (lane + 31) & 31);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            const double t_cur = i == 0 ? t_prev : __shfl_sync(kFull, E[i], (lane + 31) & 31);
+            const double el = (lane == 0) ? t_prev : t_cur;
+            Hn[i] = H[i] + ch * (E[i] - el);
+            t_prev = t_cur;
+        }
+        // density step + E update, streaming the H[m+1] shuffles one row ahead
+        double u_cur = __shfl_sync(kFull, Hn[0], (lane + 1) & 31);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            const double p = QM ? bloch_cell(q, E[i], X[i], Y[i], Z[i]) : 0.0;
+            const double u_next = i < C - 1 ? __shfl_sync(kFull, Hn[i + 1], (lane + 1) & 31) : u_cur;
+            const double hr = (lane == 31) ? u_next : u_cur;
+            // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
+            E[i] = QM ? a * E[i] - bg * p + bdx * (hr - Hn[i]) : a * E[i] + bdx * (hr - Hn[i]);
+            H[i] = Hn[i];
+            u_cur = u_next;
+        }
+        const unsigned long long mask = L.step_mask[s];
+        const bool check = (L.check_mask >> s) & 1ull;
+        if (mask || check) {
+            const long long n = L.n0 + s;
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const long long c = base + i * 32 + lane;
+                if (c < t_lo || c >= t_hi || c < L.own_lo || c >= L.own_hi) continue;
+                if (check && !isfinite(E[i])) atomicMin(L.bad_step, (unsigned long long)n);
+                for (int r = 0; r < L.n_rec; ++r) {
+                    if (!((mask >> r) & 1ull)) continue;
+                    const long long cell = L.rec_cell[r];
+                    if (cell >= 0 && cell != c) continue;
+                    const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+                    double vre = 0.0, vim = 0.0;
+                    switch (L.rec_q[r]) {
+                        case MBG_Q_E: vre = E[i]; break;
+                        case MBG_Q_H: vre = H[i]; break;
+                        case MBG_Q_D:
+                            if (QM) bloch_entry(L.rec_i[r], L.rec_j[r], X[i], Y[i], Z[i], vre, vim);
+                            break;
+                        default:
+                            if (QM) vre = -Z[i];
+                    }
+                    L.rec_re[r][idx] = vre;
+                    if (L.rec_im[r]) L.rec_im[r][idx] = vim;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+        const long long c = base + i * 32 + lane;
+        if (c < t_lo || c >= t_hi) continue;
+        const long long l = l0 + i * 32;
+        L.e_out[l] = E[i];
+        L.h_out[l] = H[i];
+        if (QM) {
+            L.s_out[l] = X[i];
+            L.s_out[L.plane + l] = Y[i];
+            L.s_out[2 * L.plane + l] = Z[i];
+        }
+    }
+}
+
+#ifndef MBG_BLOCH_MINB
+#define MBG_BLOCH_MINB 1
+#endif
+// interior tiles: every warp classifies its tile and leaves if it is not interior
+__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
+bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     const Launch &L = P.L;
     const int lane = threadIdx.x & 31;
     const long long tile = (long long)blockIdx.x * kBlochWarpsPerBlock + (threadIdx.x >> 5);
     const long long t_lo = L.res_lo + tile * L.tile_own;
     if (t_lo >= L.res_hi) return;
     const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
-    // the tile at the physical left edge starts at cell 0 (nothing to its left)
-    const long long base = (t_lo - L.k < 0) ? 0 : t_lo - L.k;
-    // warp-uniform test: one E region and one H region across the tile
+    const long long base = tile_base(L, t_lo);
+    if (!tile_is_interior(L, base, W)) return;
+    const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
+    const int qm = L.rg.qm[re];
+    if (qm < 0)
+        interior_tile<false, true>(P, t_lo, t_hi, base, lane, re, rh);
+    else if (P.n_qm == 1)
+        interior_tile<true, true>(P, t_lo, t_hi, base, lane, re, rh);
+    else
+        interior_tile<true, false>(P, t_lo, t_hi, base, lane, re, rh);
+}
+
+// the few remaining tiles (domain/window edges, region interfaces, sources)
+__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32)
+bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ EdgeTiles T) {
+    const Launch &L = P.L;
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x * kBlochWarpsPerBlock + (threadIdx.x >> 5);
+    if (w >= T.n) return;
+    const long long t_lo = L.res_lo + T.tile[w] * L.tile_own;
+    const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
+    const long long base = tile_base(L, t_lo);
     const long long lo = base, hi = base + W - 1 < L.num_x ? base + W - 1 : L.num_x - 1;
     const bool uni = region_of(L.rg.e_start, L.rg.n, lo) == region_of(L.rg.e_start, L.rg.n, hi) &&
                      region_of(L.rg.h_start, L.rg.n, lo < 1 ? 1 : lo) ==
@@ -233,9 +347,28 @@ bloch_step_kernel(const __grid_constant__ BlochParams P) {
 }  // namespace
 
 cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st) {
+    // host-side twin of the device classification: collect the non-interior tiles
+    EdgeTiles T;
+    T.n = 0;
+    const Launch &L = P.L;
+    auto flush = [&]() -> cudaError_t {
+        if (T.n == 0) return cudaSuccess;
+        const int blocks = (T.n + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
+        bloch_edge_kernel<<<blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P, T);
+        T.n = 0;
+        return cudaGetLastError();
+    };
     const long long blocks = (tiles + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
-    bloch_step_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
-    return cudaGetLastError();
+    bloch_interior_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    for (long long t = 0; t < tiles; ++t) {
+        const long long t_lo = L.res_lo + t * L.tile_own;
+        if (tile_is_interior(L, tile_base(L, t_lo), W)) continue;
+        T.tile[T.n++] = t;
+        if (T.n == kMaxEdgeTiles && (err = flush()) != cudaSuccess) return err;
+    }
+    return flush();
 }
 
 }  // namespace MBG_VARIANT

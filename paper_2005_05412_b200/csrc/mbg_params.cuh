@@ -121,4 +121,28 @@ __host__ __device__ inline int region_of(const long long *start, int n, long lon
     return r;
 }
 
+// two-level kernel geometry: tile t covers result cells [t_lo, t_hi) and loads
+// slots [base, base + width); the tile at the physical left edge starts at 0
+__host__ __device__ inline long long tile_base(const Launch &L, long long t_lo) {
+    return (t_lo - L.k < 0) ? 0 : t_lo - L.k;
+}
+
+// interior tile: all slots regular cells (1 <= c <= Nx-2) inside the window,
+// one E region and one H region, no source cell
+__host__ __device__ inline bool tile_is_interior(const Launch &L, long long base, int width) {
+    const long long hi = base + width - 1;
+    if (base < 1 || hi > L.num_x - 2 || base < L.win_lo || hi >= L.win_lo + L.win_n) return false;
+    if (region_of(L.rg.e_start, L.rg.n, base) != region_of(L.rg.e_start, L.rg.n, hi)) return false;
+    if (region_of(L.rg.h_start, L.rg.n, base) != region_of(L.rg.h_start, L.rg.n, hi)) return false;
+    for (int q = 0; q < L.n_src; ++q)
+        if (L.src_cell[q] >= base && L.src_cell[q] <= hi) return false;
+    return true;
+}
+
+constexpr int kMaxEdgeTiles = 128;
+struct EdgeTiles {
+    int n;
+    long long tile[kMaxEdgeTiles];
+};
+
 }  // namespace mbg

@@ -9,6 +9,7 @@ g.build()"`` or ``make -C paper_2005_05412_b200/csrc``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
@@ -16,7 +17,7 @@ import numpy as np
 from .errors import NativeError
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_build" / "libmbgpu.so"
+LIB_PATH = Path(os.environ.get("MBGPU_LIB", PKG / "_build" / "libmbgpu.so"))
 HEADER = PKG.parent / "include" / "mbgpu.h"
 
 MBG_STEPPER = {"splitting": 0, "rk4": 1}
@@ -69,6 +70,9 @@ SIGNATURES = {
     "mbg_halo_words": (C.c_int, [_h, _i32p]),
     "mbg_pack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
     "mbg_unpack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
+    "mbg_checkpoint_save": (C.c_int, [_h]),
+    "mbg_checkpoint_restore": (C.c_int, [_h]),
+    "mbg_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "mbg_event_begin": (C.c_int, [_h]),
     "mbg_event_end": (C.c_int, [_h, C.POINTER(C.c_float)]),
     "mbg_launch_count": (C.c_int, [_h, _i64p]),
