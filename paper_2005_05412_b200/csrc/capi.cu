@@ -211,7 +211,17 @@ cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
         std::memset(&P, 0, sizeof(P));
         P.L = L;
         P.n_qm = (int)s->qm.size();
-        for (int q = 0; q < P.n_qm; ++q) std::memcpy(&P.qm[q], s->qm[q].bloch, sizeof(BlochQm));
+        P.real_dipole = P.n_qm > 0 ? 1 : 0;
+        for (int q = 0; q < P.n_qm; ++q) {
+            BlochQm &b = P.qm[q];
+            std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
+            // _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
+            const bool real = b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 &&
+                              b.a0_s == 0.0 && b.mu_y == 0.0 && b.mu_z == 0.0;
+            P.real_dipole &= real ? 1 : 0;
+            const double u = b.a0_c * b.a0_c;
+            P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c};
+        }
         return s->g.exact ? exact::launch_bloch(P, tiles, s->stream) : fast::launch_bloch(P, tiles, s->stream);
     }
     switch (s->g.levels) {

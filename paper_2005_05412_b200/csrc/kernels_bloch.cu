@@ -35,27 +35,53 @@ constexpr int C = kBlochCellsPerLane;
 constexpr int W = kBlochTile;
 constexpr unsigned kFull = 0xffffffffu;
 
-// _kernels.py:200-232, same expression order
+// _kernels.py:200-232, same expression order (each mad(a, b, c) is the
+// reference's "c + a*b" term)
 __device__ __forceinline__ double bloch_cell(const BlochQm &q, double e, double &x, double &y, double &z) {
     const double x0 = x, y0 = y, z0 = z;
-    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = q.kz * z0 + q.cz;
-    const double ax = q.ax_c + q.ax_s * e, ay = q.ay_c + q.ay_s * e;
-    const double az = q.az_c + q.az_s * e, a0 = q.a0_c + q.a0_s * e;
-    const double qq = ax * ax + ay * ay + az * az;
+    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = mad(q.kz, z0, q.cz);
+    const double ax = mad(q.ax_s, e, q.ax_c), ay = mad(q.ay_s, e, q.ay_c);
+    const double az = mad(q.az_s, e, q.az_c), a0 = mad(q.a0_s, e, q.a0_c);
+    const double qq = mad(az, az, mad(ay, ay, ax * ax));
     const double u = a0 * a0;
     const double num = 1.0 + u - qq;
     const double t1 = 1.0 + qq - u;
-    const double inv = 1.0 / (t1 * t1 + 4.0 * u);
-    const double k1 = (num * num - 4.0 * qq) * inv;
+    const double inv = 1.0 / mad(t1, t1, 4.0 * u);
+    const double k1 = mad(num, num, -(4.0 * qq)) * inv;
     const double g = 4.0 * num * inv;
-    const double dotb = 8.0 * inv * (ax * x1 + ay * y1 + az * z1);
-    const double x2 = k1 * x1 + g * (ay * z1 - az * y1) + dotb * ax;
-    const double y2 = k1 * y1 + g * (az * x1 - ax * z1) + dotb * ay;
-    const double z2 = k1 * z1 + g * (ax * y1 - ay * x1) + dotb * az;
+    const double dotb = 8.0 * inv * mad(az, z1, mad(ay, y1, ax * x1));
+    const double x2 = mad(dotb, ax, mad(g, mad(ay, z1, -(az * y1)), k1 * x1));
+    const double y2 = mad(dotb, ay, mad(g, mad(az, x1, -(ax * z1)), k1 * y1));
+    const double z2 = mad(dotb, az, mad(g, mad(ax, y1, -(ay * x1)), k1 * z1));
     x = q.fxy * x2;
     y = q.fxy * y2;
-    z = q.kz * z2 + q.cz;
-    return q.pol_factor * (q.mu_x * (x - x0) + q.mu_y * (y - y0) + q.mu_z * (z - z0));
+    z = mad(q.kz, z2, q.cz);
+    return q.pol_factor * mad(q.mu_z, z - z0, mad(q.mu_y, y - y0, q.mu_x * (x - x0)));
+}
+
+// Same step for real-dipole / diagonal-H0 media.  Every dropped term is an
+// exact zero in the reference's evaluation (0*E, 0*x), so each nonzero value
+// equals the general formula's bit for bit; only the sign of an exact zero
+// could differ.
+__device__ __forceinline__ double bloch_cell_real(const BlochQm &q, const BlochReal &r, double e, double &x,
+                                                  double &y, double &z) {
+    const double x0 = x, y0 = y, z0 = z;
+    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = mad(q.kz, z0, q.cz);
+    const double ax = q.ax_s * e, az = q.az_c;
+    const double qq = mad(ax, ax, r.az2);
+    const double num = r.c1 - qq;
+    const double t1 = 1.0 + qq - r.u;
+    const double inv = 1.0 / mad(t1, t1, r.c4u);
+    const double k1 = mad(num, num, -(4.0 * qq)) * inv;
+    const double g = 4.0 * num * inv;
+    const double dotb = 8.0 * inv * mad(az, z1, ax * x1);
+    const double x2 = mad(dotb, ax, mad(g, -(az * y1), k1 * x1));
+    const double y2 = mad(g, mad(az, x1, -(ax * z1)), k1 * y1);
+    const double z2 = mad(dotb, az, mad(g, ax * y1, k1 * z1));
+    x = q.fxy * x2;
+    y = q.fxy * y2;
+    z = mad(q.kz, z2, q.cz);
+    return q.pol_factor * (q.mu_x * (x - x0));
 }
 
 // density entry (i, j) of a Bloch vector (_kernels.py:530-536)
@@ -120,14 +146,16 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
             const long long c = base + i * 32 + lane;
             El[i] = (lane == 0) ? t[i > 0 ? i - 1 : 0] : t[i];
             const double ch = UNI ? L.rg.ch[rh_u] : L.rg.ch[rh_[i]];
-            Hn[i] = (c >= 1 && c <= nx - 1) ? H[i] + ch * (E[i] - El[i]) : H[i];
+            Hn[i] = (c >= 1 && c <= nx - 1) ? mad(ch, E[i] - El[i], H[i]) : H[i];
         }
         // ---- density step with E^{n-1} and polarisation rate -----------------
         double p[C];
 #pragma unroll
         for (int i = 0; i < C; ++i) {
             p[i] = 0.0;
-            if (qi[i] >= 0) p[i] = bloch_cell(P.qm[qi[i]], E[i], X[i], Y[i], Z[i]);
+            if (qi[i] >= 0)
+                p[i] = P.real_dipole ? bloch_cell_real(P.qm[qi[i]], P.rq[qi[i]], E[i], X[i], Y[i], Z[i])
+                                     : bloch_cell(P.qm[qi[i]], E[i], X[i], Y[i], Z[i]);
         }
         // ---- E update: needs H[m+1] (right neighbour) --------------------------
         double u[C];
@@ -139,18 +167,18 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
             const double hr = (lane == 31) ? u[i < C - 1 ? i + 1 : i] : u[i];
             const int r = UNI ? re_u : re_[i];
             const double a = L.rg.a[r], bg = L.rg.bg[r], bdx = L.rg.bdx[r];
-            double en = (nx > 1 && c >= 0 && c < nx) ? a * E[i] - bg * p[i] + bdx * (hr - Hn[i]) : E[i];
+            double en = (nx > 1 && c >= 0 && c < nx) ? mad(bdx, hr - Hn[i], mad(a, E[i], -(bg * p[i]))) : E[i];
             if (left_edge && i == 0 && lane == 0) {
                 // solver_fdtd.py:372-374
-                const double e_at = L.l_omc * E[0] + L.l_c * e_right0;
+                const double e_at = mad(L.l_c, e_right0, L.l_omc * E[0]);
                 const double h_at = 0.5 * (h_right0 + hr);
-                en = L.l_hw * (e_at + L.l_z * h_at);
+                en = L.l_hw * mad(L.l_z, h_at, e_at);
             }
             if (right_edge && c == nx - 1) {
                 // solver_fdtd.py:375-377 (E[Nx-2] old is the left neighbour)
-                const double e_at = L.r_omc * E[i] + L.r_c * El[i];
+                const double e_at = mad(L.r_c, El[i], L.r_omc * E[i]);
                 const double h_at = 0.5 * (H[i] + Hn[i]);
-                en = L.r_hw * (e_at - L.r_z * h_at);
+                en = L.r_hw * mad(-L.r_z, h_at, e_at);
             }
             for (int q = 0; q < L.n_src; ++q) {
                 if (c == L.src_cell[q]) {
@@ -213,7 +241,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
 // the window (1 <= c <= Nx-2), one E region and one H region, no source and no
 // boundary cell.  No per-slot predicates, scalar coefficients, and for a single
 // quantum material the stepper constants are constant-bank operands.
-template <bool QM, bool ONE_QM>
+template <bool QM, bool ONE_QM, bool REAL = false>
 __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
                                               int lane, int r_e, int r_h) {
     const Launch &L = P.L;
@@ -240,18 +268,20 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
         for (int i = 0; i < C; ++i) {
             const double t_cur = i == 0 ? t_prev : __shfl_sync(kFull, E[i], (lane + 31) & 31);
             const double el = (lane == 0) ? t_prev : t_cur;
-            Hn[i] = H[i] + ch * (E[i] - el);
+            Hn[i] = mad(ch, E[i] - el, H[i]);
             t_prev = t_cur;
         }
         // density step + E update, streaming the H[m+1] shuffles one row ahead
         double u_cur = __shfl_sync(kFull, Hn[0], (lane + 1) & 31);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
-            const double p = QM ? bloch_cell(q, E[i], X[i], Y[i], Z[i]) : 0.0;
+            double p = 0.0;
+            if (QM) p = REAL ? bloch_cell_real(q, P.rq[qmi], E[i], X[i], Y[i], Z[i])
+                             : bloch_cell(q, E[i], X[i], Y[i], Z[i]);
             const double u_next = i < C - 1 ? __shfl_sync(kFull, Hn[i + 1], (lane + 1) & 31) : u_cur;
             const double hr = (lane == 31) ? u_next : u_cur;
             // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
-            E[i] = QM ? a * E[i] - bg * p + bdx * (hr - Hn[i]) : a * E[i] + bdx * (hr - Hn[i]);
+            E[i] = QM ? mad(bdx, hr - Hn[i], mad(a, E[i], -(bg * p))) : mad(bdx, hr - Hn[i], a * E[i]);
             H[i] = Hn[i];
             u_cur = u_next;
         }
@@ -301,7 +331,7 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
 }
 
 #ifndef MBG_BLOCH_MINB
-#define MBG_BLOCH_MINB 1
+#define MBG_BLOCH_MINB 3
 #endif
 // interior tiles: every warp classifies its tile and leaves if it is not interior
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
@@ -318,6 +348,8 @@ bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     const int qm = L.rg.qm[re];
     if (qm < 0)
         interior_tile<false, true>(P, t_lo, t_hi, base, lane, re, rh);
+    else if (P.n_qm == 1 && P.real_dipole)
+        interior_tile<true, true, true>(P, t_lo, t_hi, base, lane, re, rh);
     else if (P.n_qm == 1)
         interior_tile<true, true>(P, t_lo, t_hi, base, lane, re, rh);
     else

@@ -88,7 +88,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
     for (int i = 0; i < N; ++i) {
         double acc = q.pop[i * N] * A[0];
 #pragma unroll
-        for (int j = 1; j < N; ++j) acc += q.pop[i * N + j] * A[j];
+        for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], A[j], acc);
         B[i] = acc;
     }
 #pragma unroll
@@ -101,20 +101,20 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
     // B(E) = bc + E bf, inverted in place (Gauss-Jordan, no pivoting)
 #pragma unroll
     for (int i = 0; i < N * N; ++i) {
-        G.r(i / N, i % N) = q.bc_re[i] + e * q.bf_re[i];
-        G.m(i / N, i % N) = q.bc_im[i] + e * q.bf_im[i];
+        G.r(i / N, i % N) = mad(e, q.bf_re[i], q.bc_re[i]);
+        G.m(i / N, i % N) = mad(e, q.bf_im[i], q.bc_im[i]);
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double pr = G.r(k, k), pi = G.m(k, k);
-        const double rd = 1.0 / (pr * pr + pi * pi);
+        const double rd = 1.0 / mad(pi, pi, pr * pr);
         const double ir = pr * rd, ii = -pi * rd;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             if (j == k) continue;
             const double xr = G.r(k, j), xi = G.m(k, j);
-            G.r(k, j) = xr * ir - xi * ii;
-            G.m(k, j) = xr * ii + xi * ir;
+            G.r(k, j) = mad(xr, ir, -(xi * ii));
+            G.m(k, j) = mad(xr, ii, xi * ir);
         }
         G.r(k, k) = ir;
         G.m(k, k) = ii;
@@ -126,11 +126,11 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             for (int j = 0; j < N; ++j) {
                 if (j == k) continue;
                 const double kr = G.r(k, j), ki = G.m(k, j);
-                G.r(i, j) -= fr * kr - fi * ki;
-                G.m(i, j) -= fr * ki + fi * kr;
+                G.r(i, j) = mad(-fr, kr, mad(fi, ki, G.r(i, j)));
+                G.m(i, j) = mad(-fr, ki, mad(-fi, kr, G.m(i, j)));
             }
-            G.r(i, k) = -(fr * ir - fi * ii);
-            G.m(i, k) = -(fr * ii + fi * ir);
+            G.r(i, k) = mad(-fr, ir, fi * ii);
+            G.m(i, k) = mad(-fr, ii, -(fi * ir));
         }
     }
     // U = 2G - I
@@ -154,8 +154,8 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
                 double rr, ri;
                 herm<N>(B, m, k, rr, ri);
                 const double ur = G.r(i, m), ui = G.m(i, m);
-                ar += ur * rr - ui * ri;
-                ai += ur * ri + ui * rr;
+                ar = mad(ur, rr, mad(-ui, ri, ar));
+                ai = mad(ur, ri, mad(ui, rr, ai));
             }
             tr[k] = ar;
             ti[k] = ai;
@@ -165,9 +165,9 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             double ar = 0.0, ai = 0.0;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                const double ur = G.r(j, k), ui = -G.m(j, k);
-                ar += tr[k] * ur - ti[k] * ui;
-                ai += tr[k] * ui + ti[k] * ur;
+                const double ur = G.r(j, k), ui = G.m(j, k);  // conj(U_jk) = ur - i ui
+                ar = mad(tr[k], ur, mad(ti[k], ui, ar));
+                ai = mad(ti[k], ur, mad(-tr[k], ui, ai));
             }
             if (j == i) {
                 A[i] = ar;  // raw diagonal; relaxed below
@@ -175,7 +175,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
                 const double c = q.coh[i * N + j];
                 const double fr = ar * c, fi = ai * c;
                 const int p = pair_index(N, i, j);
-                acc_p += 2.0 * (q.pol.pol_re[p] * (fr - A[wre(N, i, j)]) + q.pol.pol_im[p] * (fi - A[wim(N, i, j)]));
+                acc_p += 2.0 * mad(q.pol.pol_im[p], fi - A[wim(N, i, j)], q.pol.pol_re[p] * (fr - A[wre(N, i, j)]));
                 A[wre(N, i, j)] = fr;
                 A[wim(N, i, j)] = fi;
             }
@@ -188,11 +188,11 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
     for (int i = 0; i < N; ++i) {
         double acc = q.pop[i * N] * raw[0];
 #pragma unroll
-        for (int j = 1; j < N; ++j) acc += q.pop[i * N + j] * raw[j];
+        for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], raw[j], acc);
         A[i] = acc;
     }
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc_p += q.pol.pol_dv[i] * (A[i] - od[i]);
+    for (int i = 0; i < N; ++i) acc_p = mad(q.pol.pol_dv[i], A[i] - od[i], acc_p);
     return q.pol.pol_factor * acc_p;
 }
 
@@ -215,20 +215,20 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
                 herm<N>(src, i, k, tr, ti);
                 const double ar = hr[i * N + k], ai = hi[i * N + k];
                 const double br = hr[k * N + j], bi = hi[k * N + j];
-                cr += (ar * sr - ai * si) - (tr * br - ti * bi);
-                ci += (ar * si + ai * sr) - (tr * bi + ti * br);
+                cr += mad(ar, sr, -(ai * si)) - mad(tr, br, -(ti * bi));
+                ci += mad(ar, si, ai * sr) - mad(tr, bi, ti * br);
             }
             // -i/hbar * (cr + i ci) = (ci/hbar, -cr/hbar)
             double dr = ci * kInvHbar, di = -cr * kInvHbar;
             if (i == j) {
                 double acc = q.popm[i * N] * src[0];
 #pragma unroll
-                for (int m = 1; m < N; ++m) acc += q.popm[i * N + m] * src[m];
+                for (int m = 1; m < N; ++m) acc = mad(q.popm[i * N + m], src[m], acc);
                 dst[i] = dr + acc;
             } else {
                 const double g = q.deph[i * N + j];
-                dst[wre(N, i, j)] = dr - g * src[wre(N, i, j)];
-                dst[wim(N, i, j)] = di - g * src[wim(N, i, j)];
+                dst[wre(N, i, j)] = mad(-g, src[wre(N, i, j)], dr);
+                dst[wim(N, i, j)] = mad(-g, src[wim(N, i, j)], di);
             }
         }
 }
@@ -239,8 +239,8 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
     double hr[N * N], hi[N * N];
 #pragma unroll
     for (int i = 0; i < N * N; ++i) {
-        hr[i] = q.h0_re[i] - e * q.mu_re[i];
-        hi[i] = q.h0_im[i] - e * q.mu_im[i];
+        hr[i] = mad(-e, q.mu_re[i], q.h0_re[i]);
+        hi[i] = mad(-e, q.mu_im[i], q.h0_im[i]);
     }
     const double dt = q.dt;
     // k1
@@ -248,19 +248,19 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
         Acc[w] = K[w];
-        S[w] = A[w] + (0.5 * dt) * K[w];
+        S[w] = mad(0.5 * dt, K[w], A[w]);
     }
     master_rhs<N>(q, hr, hi, S, K);  // k2
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-        Acc[w] += 2.0 * K[w];
-        S[w] = A[w] + (0.5 * dt) * K[w];
+        Acc[w] = mad(2.0, K[w], Acc[w]);
+        S[w] = mad(0.5 * dt, K[w], A[w]);
     }
     master_rhs<N>(q, hr, hi, S, K);  // k3
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-        Acc[w] += 2.0 * K[w];
-        S[w] = A[w] + dt * K[w];
+        Acc[w] = mad(2.0, K[w], Acc[w]);
+        S[w] = mad(dt, K[w], A[w]);
     }
     master_rhs<N>(q, hr, hi, S, K);  // k4
     const double sixth = dt / 6.0;
@@ -270,16 +270,16 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
 #pragma unroll
         for (int j = i + 1; j < N; ++j) {
             const int p = pair_index(N, i, j);
-            const double nr = A[wre(N, i, j)] + sixth * (Acc[wre(N, i, j)] + K[wre(N, i, j)]);
-            const double ni = A[wim(N, i, j)] + sixth * (Acc[wim(N, i, j)] + K[wim(N, i, j)]);
-            acc_p += 2.0 * (q.pol.pol_re[p] * (nr - A[wre(N, i, j)]) + q.pol.pol_im[p] * (ni - A[wim(N, i, j)]));
+            const double nr = mad(sixth, Acc[wre(N, i, j)] + K[wre(N, i, j)], A[wre(N, i, j)]);
+            const double ni = mad(sixth, Acc[wim(N, i, j)] + K[wim(N, i, j)], A[wim(N, i, j)]);
+            acc_p += 2.0 * mad(q.pol.pol_im[p], ni - A[wim(N, i, j)], q.pol.pol_re[p] * (nr - A[wre(N, i, j)]));
             A[wre(N, i, j)] = nr;
             A[wim(N, i, j)] = ni;
         }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-        const double nd = A[i] + sixth * (Acc[i] + K[i]);
-        acc_p += q.pol.pol_dv[i] * (nd - A[i]);
+        const double nd = mad(sixth, Acc[i] + K[i], A[i]);
+        acc_p = mad(q.pol.pol_dv[i], nd - A[i], acc_p);
         A[i] = nd;
     }
     return q.pol.pol_factor * acc_p;
@@ -374,22 +374,22 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW) dense_step_kernel(const __
         Ho[b + j] = H;
         __syncthreads();
         const double el = j > 0 ? Es[b + j - 1] : 0.0;
-        const double hn = upd_h ? H + cch * (E - el) : H;
+        const double hn = upd_h ? mad(cch, E - el, H) : H;
         Hs[b + j] = hn;
         double p = 0.0;
         if (qi >= 0) p = cell_step<N, RK4>(P.qm[qi], E, col, rA);
         __syncthreads();
         const double hr = j < W - 1 ? Hs[b + j + 1] : 0.0;
-        double en = upd_e ? ca * E - cbg * p + cbdx * (hr - hn) : E;
+        double en = upd_e ? mad(cbdx, hr - hn, mad(ca, E, -(cbg * p))) : E;
         if (left_edge) {
-            const double e_at = L.l_omc * E + L.l_c * Es[b + 1];
+            const double e_at = mad(L.l_c, Es[b + 1], L.l_omc * E);
             const double h_at = 0.5 * (Ho[b + 1] + hr);
-            en = L.l_hw * (e_at + L.l_z * h_at);
+            en = L.l_hw * mad(L.l_z, h_at, e_at);
         }
         if (right_edge) {
-            const double e_at = L.r_omc * E + L.r_c * el;
+            const double e_at = mad(L.r_c, el, L.r_omc * E);
             const double h_at = 0.5 * (H + hn);
-            en = L.r_hw * (e_at - L.r_z * h_at);
+            en = L.r_hw * mad(-L.r_z, h_at, e_at);
         }
         for (int q = 0; q < L.n_src; ++q) {
             if (c == L.src_cell[q]) {

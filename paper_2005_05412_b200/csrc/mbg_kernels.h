@@ -9,6 +9,19 @@
 
 namespace mbg {
 
+#ifdef __CUDACC__
+// a*b + c.  Fast variant: one fused multiply-add.  Exact variant: a rounded
+// product then a rounded sum -- with IEEE commutativity this is exactly the
+// reference's "c + a*b" / "a*b + c" for every place it is used.
+__device__ __forceinline__ double mad(double a, double b, double c) {
+#if defined(MBG_EXACT) && MBG_EXACT
+    return __dadd_rn(__dmul_rn(a, b), c);
+#else
+    return fma(a, b, c);
+#endif
+}
+#endif
+
 // tile geometry of the N = 2 kernel: one warp per tile, C cells per lane
 constexpr int kBlochCellsPerLane = 8;
 constexpr int kBlochTile = 32 * kBlochCellsPerLane;

@@ -73,10 +73,22 @@ struct BlochQm {
     double kz, cz, fxy, ax_c, ax_s, ay_c, ay_s, az_c, az_s, a0_c, a0_s, mu_x, mu_y, mu_z, pol_factor;
 };
 
+// real dipole and diagonal H0 (every two_level_description medium): ax_c, ay_c,
+// ay_s, az_s, a0_s, mu_y, mu_z vanish, so A = (ax_s E, 0, az_c) with a0 = a0_c
+// constant; the field-independent products are hoisted (same IEEE values)
+struct BlochReal {
+    double u;    // a0_c * a0_c
+    double c1;   // 1.0 + u
+    double c4u;  // 4.0 * u
+    double az2;  // az_c * az_c
+};
+
 struct BlochParams {
     Launch L;
     int n_qm;
+    int real_dipole;  // all materials satisfy the BlochReal pattern
     BlochQm qm[kMaxQm];
+    BlochReal rq[kMaxQm];
 };
 
 // dipole weights of the polarisation trace (_kernels.py:360-374), stored
