@@ -48,6 +48,8 @@ struct mbg_solver {
     int k = 1;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t side = nullptr;  // edge tiles of the two-level kernel
+    cudaEvent_t fork = nullptr, join = nullptr;
     long long win_n = 0, plane = 0;
     double *e[2] = {nullptr, nullptr}, *h[2] = {nullptr, nullptr}, *s[2] = {nullptr, nullptr};
     int cur = 0;
@@ -83,7 +85,7 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
     } while (0)
 
 int default_tile_steps(int levels, int stepper) {
-    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 16;
+    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 24;
     if (levels <= 3) return 8;
     return 4;
 }
@@ -220,9 +222,10 @@ cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
                               b.a0_s == 0.0 && b.mu_y == 0.0 && b.mu_z == 0.0;
             P.real_dipole &= real ? 1 : 0;
             const double u = b.a0_c * b.a0_c;
-            P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c};
+            P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c, 1.0 - u, b.pol_factor * b.mu_x};
         }
-        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream) : fast::launch_bloch(P, tiles, s->stream);
+        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join)
+                          : fast::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join);
     }
     switch (s->g.levels) {
         case 2: return launch_dense_n<2>(s, L, tiles);
@@ -286,6 +289,10 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
     if (cudaSetDevice(g.device) != cudaSuccess) return cleanup(MBG_E_CUDA);
     if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup(MBG_E_CUDA);
     s->own_stream = true;
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup(MBG_E_CUDA);
     const size_t fb = sizeof(double) * (s->win_n + 1);
     const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
     for (int b = 0; b < 2; ++b) {
@@ -325,6 +332,12 @@ void mbg_destroy(mbg_solver *s) {
     }
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->side) {
+        cudaStreamSynchronize(s->side);
+        cudaStreamDestroy(s->side);
+    }
+    if (s->fork) cudaEventDestroy(s->fork);
+    if (s->join) cudaEventDestroy(s->join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }

@@ -84,6 +84,46 @@ __device__ __forceinline__ double bloch_cell_real(const BlochQm &q, const BlochR
     return q.pol_factor * (q.mu_x * (x - x0));
 }
 
+#if !(defined(MBG_EXACT) && MBG_EXACT)
+// 1/d for d >= 1 (the Cayley denominator (1+q-u)^2 + 4u is never below 1):
+// hardware seed + two Newton steps, no special-case branch
+__device__ __forceinline__ double rcp_ge1(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// fast variant of bloch_cell_real: the same rotation regrouped around the
+// field-independent products g*az and 8/den (tolerance-level, not bitwise)
+__device__ __forceinline__ double bloch_cell_real_fast(const BlochQm &q, const BlochReal &r, double e, double &x,
+                                                       double &y, double &z) {
+    const double x0 = x, y0 = y, z0 = z;
+    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = fma(q.kz, z0, q.cz);
+    const double ax = q.ax_s * e, az = q.az_c;
+    const double qq = fma(ax, ax, r.az2);
+    const double num = r.c1 - qq;
+    const double t1 = qq + r.c2;
+    const double inv = rcp_ge1(fma(t1, t1, r.c4u));
+    const double k1 = fma(num, num, -4.0 * qq) * inv;
+    const double g = num * (4.0 * inv);
+    const double gaz = g * az, gax = g * ax;
+    const double dotb = (8.0 * inv) * fma(az, z1, ax * x1);
+    const double x2 = fma(dotb, ax, fma(-gaz, y1, k1 * x1));
+    const double y2 = fma(-gax, z1, fma(gaz, x1, k1 * y1));
+    const double z2 = fma(dotb, az, fma(gax, y1, k1 * z1));
+    x = q.fxy * x2;
+    y = q.fxy * y2;
+    z = fma(q.kz, z2, q.cz);
+    return r.pfmu * (x - x0);
+}
+#define MBG_BLOCH_REAL bloch_cell_real_fast
+#else
+#define MBG_BLOCH_REAL bloch_cell_real
+#endif
+
 // density entry (i, j) of a Bloch vector (_kernels.py:530-536)
 __device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, double z, double &re, double &im) {
     if (i == j) {
@@ -154,7 +194,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         for (int i = 0; i < C; ++i) {
             p[i] = 0.0;
             if (qi[i] >= 0)
-                p[i] = P.real_dipole ? bloch_cell_real(P.qm[qi[i]], P.rq[qi[i]], E[i], X[i], Y[i], Z[i])
+                p[i] = P.real_dipole ? MBG_BLOCH_REAL(P.qm[qi[i]], P.rq[qi[i]], E[i], X[i], Y[i], Z[i])
                                      : bloch_cell(P.qm[qi[i]], E[i], X[i], Y[i], Z[i]);
         }
         // ---- E update: needs H[m+1] (right neighbour) --------------------------
@@ -239,8 +279,10 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
 
 // Interior tiles (the overwhelming majority): every slot is a regular cell of
 // the window (1 <= c <= Nx-2), one E region and one H region, no source and no
-// boundary cell.  No per-slot predicates, scalar coefficients, and for a single
-// quantum material the stepper constants are constant-bank operands.
+// boundary cell.  Blocked layout: lane l holds the C consecutive cells
+// base + l*C .. base + l*C + C-1, so the stencil needs one shuffle of E up and
+// one of H down per lane and step; everything else is in-register.  For a
+// single quantum material the stepper constants are constant-bank operands.
 template <bool QM, bool ONE_QM, bool REAL = false>
 __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
                                               int lane, int r_e, int r_h) {
@@ -248,42 +290,33 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
     const double a = L.rg.a[r_e], bg = L.rg.bg[r_e], bdx = L.rg.bdx[r_e], ch = L.rg.ch[r_h];
     const int qmi = QM ? (ONE_QM ? 0 : L.rg.qm[r_e]) : 0;
     const BlochQm &q = P.qm[qmi];
-    const long long l0 = base - L.win_lo + lane;
+    const long long l0 = base - L.win_lo + (long long)lane * C;
     double E[C], H[C], X[C], Y[C], Z[C];
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-        E[i] = L.e_in[l0 + i * 32];
-        H[i] = L.h_in[l0 + i * 32];
+        E[i] = L.e_in[l0 + i];
+        H[i] = L.h_in[l0 + i];
         if (QM) {
-            X[i] = L.s_in[l0 + i * 32];
-            Y[i] = L.s_in[L.plane + l0 + i * 32];
-            Z[i] = L.s_in[2 * L.plane + l0 + i * 32];
+            X[i] = L.s_in[l0 + i];
+            Y[i] = L.s_in[L.plane + l0 + i];
+            Z[i] = L.s_in[2 * L.plane + l0 + i];
         }
     }
     for (int s = 0; s < L.k; ++s) {
-        // H update in slot order; lane 0 takes E[m-1] from lane 31 of the previous row
-        double Hn[C];
-        double t_prev = __shfl_sync(kFull, E[0], (lane + 31) & 31);
+        // H update (uses E^{n-1}); H is overwritten in place with H^{n-1/2}
+        const double el0 = __shfl_up_sync(kFull, E[C - 1], 1);
 #pragma unroll
-        for (int i = 0; i < C; ++i) {
-            const double t_cur = i == 0 ? t_prev : __shfl_sync(kFull, E[i], (lane + 31) & 31);
-            const double el = (lane == 0) ? t_prev : t_cur;
-            Hn[i] = mad(ch, E[i] - el, H[i]);
-            t_prev = t_cur;
-        }
-        // density step + E update, streaming the H[m+1] shuffles one row ahead
-        double u_cur = __shfl_sync(kFull, Hn[0], (lane + 1) & 31);
+        for (int i = C - 1; i >= 0; --i) H[i] = mad(ch, E[i] - (i == 0 ? el0 : E[i - 1]), H[i]);
+        const double hr_last = __shfl_down_sync(kFull, H[0], 1);
+        // density step + E update, slot by slot
 #pragma unroll
         for (int i = 0; i < C; ++i) {
             double p = 0.0;
-            if (QM) p = REAL ? bloch_cell_real(q, P.rq[qmi], E[i], X[i], Y[i], Z[i])
+            if (QM) p = REAL ? MBG_BLOCH_REAL(q, P.rq[qmi], E[i], X[i], Y[i], Z[i])
                              : bloch_cell(q, E[i], X[i], Y[i], Z[i]);
-            const double u_next = i < C - 1 ? __shfl_sync(kFull, Hn[i + 1], (lane + 1) & 31) : u_cur;
-            const double hr = (lane == 31) ? u_next : u_cur;
+            const double hr = i == C - 1 ? hr_last : H[i + 1];
             // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
-            E[i] = QM ? mad(bdx, hr - Hn[i], mad(a, E[i], -(bg * p))) : mad(bdx, hr - Hn[i], a * E[i]);
-            H[i] = Hn[i];
-            u_cur = u_next;
+            E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bg * p))) : mad(bdx, hr - H[i], a * E[i]);
         }
         const unsigned long long mask = L.step_mask[s];
         const bool check = (L.check_mask >> s) & 1ull;
@@ -291,7 +324,7 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
             const long long n = L.n0 + s;
 #pragma unroll
             for (int i = 0; i < C; ++i) {
-                const long long c = base + i * 32 + lane;
+                const long long c = base + (long long)lane * C + i;
                 if (c < t_lo || c >= t_hi || c < L.own_lo || c >= L.own_hi) continue;
                 if (check && !isfinite(E[i])) atomicMin(L.bad_step, (unsigned long long)n);
                 for (int r = 0; r < L.n_rec; ++r) {
@@ -317,21 +350,20 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
     }
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-        const long long c = base + i * 32 + lane;
+        const long long c = base + (long long)lane * C + i;
         if (c < t_lo || c >= t_hi) continue;
-        const long long l = l0 + i * 32;
-        L.e_out[l] = E[i];
-        L.h_out[l] = H[i];
+        L.e_out[l0 + i] = E[i];
+        L.h_out[l0 + i] = H[i];
         if (QM) {
-            L.s_out[l] = X[i];
-            L.s_out[L.plane + l] = Y[i];
-            L.s_out[2 * L.plane + l] = Z[i];
+            L.s_out[l0 + i] = X[i];
+            L.s_out[L.plane + l0 + i] = Y[i];
+            L.s_out[2 * L.plane + l0 + i] = Z[i];
         }
     }
 }
 
 #ifndef MBG_BLOCH_MINB
-#define MBG_BLOCH_MINB 3
+#define MBG_BLOCH_MINB 4
 #endif
 // interior tiles: every warp classifies its tile and leaves if it is not interior
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
@@ -378,29 +410,37 @@ bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
 
 }  // namespace
 
-cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st) {
+// The edge tiles (a handful of latency-bound warps) run on a side stream,
+// forked from and joined back into the launch stream, so they overlap the
+// interior kernel instead of trailing it.
+cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, cudaStream_t st_edge,
+                         cudaEvent_t fork, cudaEvent_t join) {
+    const Launch &L = P.L;
+    cudaError_t err = cudaEventRecord(fork, st);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(st_edge, fork, 0);
+    if (err != cudaSuccess) return err;
     // host-side twin of the device classification: collect the non-interior tiles
     EdgeTiles T;
     T.n = 0;
-    const Launch &L = P.L;
     auto flush = [&]() -> cudaError_t {
         if (T.n == 0) return cudaSuccess;
         const int blocks = (T.n + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
-        bloch_edge_kernel<<<blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P, T);
+        bloch_edge_kernel<<<blocks, kBlochWarpsPerBlock * 32, 0, st_edge>>>(P, T);
         T.n = 0;
         return cudaGetLastError();
     };
-    const long long blocks = (tiles + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
-    bloch_interior_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
-    cudaError_t err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
     for (long long t = 0; t < tiles; ++t) {
         const long long t_lo = L.res_lo + t * L.tile_own;
         if (tile_is_interior(L, tile_base(L, t_lo), W)) continue;
         T.tile[T.n++] = t;
         if (T.n == kMaxEdgeTiles && (err = flush()) != cudaSuccess) return err;
     }
-    return flush();
+    if ((err = flush()) != cudaSuccess) return err;
+    const long long blocks = (tiles + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
+    bloch_interior_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if ((err = cudaEventRecord(join, st_edge)) != cudaSuccess) return err;
+    return cudaStreamWaitEvent(st, join, 0);
 }
 
 }  // namespace MBG_VARIANT

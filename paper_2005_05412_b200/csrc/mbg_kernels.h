@@ -23,7 +23,10 @@ __device__ __forceinline__ double mad(double a, double b, double c) {
 #endif
 
 // tile geometry of the N = 2 kernel: one warp per tile, C cells per lane
-constexpr int kBlochCellsPerLane = 8;
+#ifndef MBG_BLOCH_C
+#define MBG_BLOCH_C 8
+#endif
+constexpr int kBlochCellsPerLane = MBG_BLOCH_C;
 constexpr int kBlochTile = 32 * kBlochCellsPerLane;
 constexpr int kBlochWarpsPerBlock = 4;
 // dense kernels: one thread per cell, one CTA per tile
@@ -31,7 +34,8 @@ constexpr int kDenseTile = 128;
 
 #define MBG_DECLARE_LAUNCHERS(NS)                                                             \
     namespace NS {                                                                            \
-    cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st);         \
+    cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,          \
+                             cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join);        \
     cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \
     cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStream_t st);   \
     }

@@ -77,10 +77,12 @@ struct BlochQm {
 // ay_s, az_s, a0_s, mu_y, mu_z vanish, so A = (ax_s E, 0, az_c) with a0 = a0_c
 // constant; the field-independent products are hoisted (same IEEE values)
 struct BlochReal {
-    double u;    // a0_c * a0_c
-    double c1;   // 1.0 + u
-    double c4u;  // 4.0 * u
-    double az2;  // az_c * az_c
+    double u;     // a0_c * a0_c
+    double c1;    // 1.0 + u
+    double c4u;   // 4.0 * u
+    double az2;   // az_c * az_c
+    double c2;    // 1.0 - u          (fast variant)
+    double pfmu;  // pol_factor * mu_x (fast variant)
 };
 
 struct BlochParams {
