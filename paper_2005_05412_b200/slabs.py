@@ -1,0 +1,396 @@
+"""Multi-GPU slab decomposition of the time-stepping core.
+
+The 1D domain is cut into G contiguous slabs with the reference's own
+partition rule (``np.linspace(0, Nx, G+1)``, solver_fdtd.py:468 -- there it
+splits cells among CPU worker threads).  Each slab is held on its device as a
+window [own_lo - k, own_hi + k) (clipped at the physical ends): k ghost cells
+per side, k = the temporal tile depth.  One fused launch advances k steps; the
+valid region shrinks by one cell per side per step, so after it exactly the
+owned cells are current and the ghosts are refreshed by a point-to-point
+exchange with the two neighbours -- E, H and every density plane of k cells
+per interface and direction.  There is no other collective on the data path:
+records are gathered once at the end and the non-finite flag is combined with
+one MIN reduction per poll.
+
+Every cell executes the same instruction sequence whatever slab or tile it
+lands in, so results are bitwise independent of G (tested).
+
+Transports:
+  * :class:`LocalTransport` -- all slabs in one process on one device, ghost
+    refresh by device-to-device pack/unpack (single-GPU tests of the slab
+    path, no kernel ever waits on another).
+  * :class:`TorchTransport` -- one process per GPU, ``torch.distributed``
+    batched isend/irecv (NCCL over NVLink on the B200 box, gloo on CPU).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .errors import SolverError
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    world: int
+    own_lo: int
+    own_hi: int
+    win_lo: int
+    win_hi: int
+
+    @property
+    def ghost_left(self) -> int:
+        return self.own_lo - self.win_lo
+
+    @property
+    def ghost_right(self) -> int:
+        return self.win_hi - self.own_hi
+
+
+def partition(num_x: int, world: int, ghost: int) -> list[Slab]:
+    """Contiguous slabs (reference rule, solver_fdtd.py:468) with ``ghost`` cells per side."""
+    if world < 1 or world > num_x:
+        raise ValueError("need 1 <= slabs <= cells")
+    bounds = np.linspace(0, num_x, world + 1).astype(int)
+    slabs = []
+    for r in range(world):
+        lo, hi = int(bounds[r]), int(bounds[r + 1])
+        if hi - lo < ghost and world > 1:
+            raise ValueError(f"slab {r} has {hi - lo} cells, fewer than the ghost width {ghost}")
+        slabs.append(Slab(r, world, lo, hi, max(0, lo - ghost), min(num_x, hi + ghost)))
+    return slabs
+
+
+def exchange_plan(slab: Slab):
+    """(send_left, recv_left, send_right, recv_right) as (cell0, count) or None.
+
+    My left ghost [win_lo, own_lo) is the left neighbour's rightmost owned
+    cells, and what I send left is my first cells [own_lo, own_lo + g) where
+    g is the left neighbour's right ghost width (same partition, same k)."""
+    sl = rl = sr = rr = None
+    if slab.ghost_left:
+        rl = (slab.win_lo, slab.ghost_left)
+        sl = (slab.own_lo, slab.ghost_left)  # neighbour's right ghost has the same width
+    if slab.ghost_right:
+        rr = (slab.own_hi, slab.ghost_right)
+        sr = (slab.own_hi - slab.ghost_right, slab.ghost_right)
+    return sl, rl, sr, rr
+
+
+class SlabState:
+    """One slab on one device: the native handle plus its geometry."""
+
+    def __init__(self, solver, slab: Slab, stream: int = 0):
+        self.solver = solver
+        self.slab = slab
+        self.h = solver.open_handle(win=(slab.win_lo, slab.win_hi), own=(slab.own_lo, slab.own_hi))
+        if stream:
+            self.h.call("mbg_set_stream", stream)
+        solver.upload_initial_state(self.h, win=(slab.win_lo, slab.win_hi))
+        w = C.c_int32(0)
+        self.h.call("mbg_halo_words", C.byref(w))
+        self.words = w.value  # per cell: E, H, state planes
+
+    def sample(self, step):
+        self.h.call("mbg_sample", step)
+
+    def advance(self, first, count):
+        self.h.call("mbg_advance", first, count)
+
+    def pack(self, cell0, count, ptr):
+        self.h.call("mbg_pack_halo", cell0, count, ptr)
+
+    def unpack(self, cell0, count, ptr):
+        self.h.call("mbg_unpack_halo", cell0, count, ptr)
+
+    # transport-facing: device tensors
+    def pack_into(self, cell0, count, tensor):
+        self.pack(cell0, count, tensor.data_ptr())
+
+    def unpack_from(self, cell0, count, tensor):
+        self.unpack(cell0, count, tensor.data_ptr())
+
+    def poll(self) -> int:
+        bad = C.c_int64(-1)
+        self.h.call("mbg_poll_nonfinite", C.byref(bad))
+        return bad.value
+
+    def records(self):
+        """Per record: (rows, cols) arrays of this slab's owned columns."""
+        out = []
+        for r, p in enumerate(self.solver.plan.plans):
+            rows, cols = C.c_int64(0), C.c_int64(0)
+            self.h.call("mbg_record_shape", r, C.byref(rows), C.byref(cols))
+            re = np.zeros((rows.value, cols.value))
+            im = np.zeros((rows.value, cols.value)) if p.is_complex else None
+            self.h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
+            out.append(re if im is None else re + 1j * im)
+        return out
+
+    def close(self):
+        self.h.close()
+
+
+def assemble(plan, slabs, per_slab_records):
+    """Merge slab records into full records (point records from their owner)."""
+    out = []
+    for r, p in enumerate(plan.plans):
+        if p.cell is None:
+            out.append(np.concatenate([recs[r] for recs in per_slab_records], axis=1))
+        else:
+            owner = next(i for i, s in enumerate(slabs) if s.own_lo <= p.cell < s.own_hi)
+            out.append(per_slab_records[owner][r])
+    return out
+
+
+# ---------------------------------------------------------------- transports --
+
+class LocalTransport:
+    """All slabs in this process on one device; ghosts refreshed device-to-device."""
+
+    def __init__(self, states):
+        import torch
+
+        self.states = states
+        words = max(s.words for s in states)
+        k = max(max(s.slab.ghost_left, s.slab.ghost_right) for s in states)
+        self.buf = torch.empty(max(1, words * k), dtype=torch.float64, device=f"cuda:{states[0].solver.gpu}")
+
+    def exchange(self):
+        # sequential per interface: pack the owner's cells, unpack into the ghost
+        ptr = self.buf.data_ptr()
+        for i, st in enumerate(self.states):
+            sl, rl, sr, rr = exchange_plan(st.slab)
+            if rl is not None:
+                left = self.states[i - 1]
+                left.pack(rl[0], rl[1], ptr)
+                st.unpack(rl[0], rl[1], ptr)
+            if rr is not None:
+                right = self.states[i + 1]
+                right.pack(rr[0], rr[1], ptr)
+                st.unpack(rr[0], rr[1], ptr)
+        for st in self.states:
+            st.h.call("mbg_synchronize")
+
+
+class TorchTransport:
+    """One slab per process; neighbours exchange with batched isend/irecv."""
+
+    def __init__(self, state: SlabState, device):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.state = state
+        sl, rl, sr, rr = exchange_plan(state.slab)
+        self.plan = (sl, rl, sr, rr)
+        w = state.words
+
+        def buf(spec):
+            return None if spec is None else torch.empty(w * spec[1], dtype=torch.float64, device=device)
+
+        self.send_l, self.recv_l, self.send_r, self.recv_r = buf(sl), buf(rl), buf(sr), buf(rr)
+
+    def exchange(self):
+        sl, rl, sr, rr = self.plan
+        st, dist = self.state, self.dist
+        rank = st.slab.rank
+        ops = []
+        if sl is not None:
+            st.pack_into(sl[0], sl[1], self.send_l)
+            ops.append(dist.P2POp(dist.isend, self.send_l, rank - 1))
+            ops.append(dist.P2POp(dist.irecv, self.recv_l, rank - 1))
+        if sr is not None:
+            st.pack_into(sr[0], sr[1], self.send_r)
+            ops.append(dist.P2POp(dist.isend, self.send_r, rank + 1))
+            ops.append(dist.P2POp(dist.irecv, self.recv_r, rank + 1))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if rl is not None:
+            st.unpack_from(rl[0], rl[1], self.recv_l)
+        if rr is not None:
+            st.unpack_from(rr[0], rr[1], self.recv_r)
+
+
+# ---------------------------------------------------------------- drivers --
+
+def _step_loop(grid, k, advance, exchange, poll, poll_every=1 << 14):
+    n = 1
+    since = 0
+    while n < grid.num_t:
+        cnt = min(k, grid.num_t - n)
+        advance(n, cnt)
+        exchange()
+        n += cnt
+        since += cnt
+        if since >= poll_every or n >= grid.num_t:
+            since = 0
+            bad = poll()
+            if bad >= 0:
+                raise SolverError(f"non-finite electric field at step {bad}")
+
+
+def run_slabs_local(solver, slabs_count: int):
+    """Run ``solver``'s scenario as ``slabs_count`` slabs on one device (tests)."""
+    if solver._ran:
+        raise SolverError("run() may only be called once per solver instance")
+    solver._ran = True
+    import torch
+
+    k = tile_steps_of(solver)
+    slabs = partition(solver.grid.num_x, slabs_count, k)
+    # one shared stream: every pack, unpack and launch runs in issue order
+    stream = torch.cuda.Stream(device=f"cuda:{solver.gpu}")
+    states = [SlabState(solver, s, stream=stream.cuda_stream) for s in slabs]
+    try:
+        tr = LocalTransport(states)
+        for st in states:
+            st.sample(0)
+
+        def advance(n, cnt):
+            for st in states:
+                st.advance(n, cnt)
+
+        def poll():
+            bads = [b for b in (st.poll() for st in states) if b >= 0]
+            return min(bads) if bads else -1
+
+        _step_loop(solver.grid, k, advance, tr.exchange, poll)
+        recs = assemble(solver.plan, slabs, [st.records() for st in states])
+    finally:
+        for st in states:
+            st.close()
+    solver.results = [p.to_result(solver.grid, d, solver._result_cls) for p, d in zip(solver.plan.plans, recs)]
+    return solver.results
+
+
+def tile_steps_of(solver) -> int:
+    """The k the native solver will use for this scenario (asks the library)."""
+    h = native.Handle(solver._grid_struct())
+    try:
+        k = C.c_int32(0)
+        h.call("mbg_tile_steps", C.byref(k))
+        return k.value
+    finally:
+        h.close()
+
+
+def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None):
+    """This process's slab of a ``world``-way run (torch.distributed initialised).
+    Returns the assembled records on rank 0 and None elsewhere.
+
+    ``state_factory(solver, slab)`` replaces the native slab (tests drive the
+    same host logic with a CPU slab stepper under gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    if k is None:
+        k = tile_steps_of(solver)
+    slabs = partition(solver.grid.num_x, world, k)
+    if state_factory is None:
+        stream = torch.cuda.current_stream(device).cuda_stream
+        st = SlabState(solver, slabs[rank], stream=stream)
+    else:
+        st = state_factory(solver, slabs[rank])
+    try:
+        tr = TorchTransport(st, device)
+        st.sample(0)
+
+        def poll():
+            b = st.poll()
+            t = torch.tensor([b if b >= 0 else 2**62], dtype=torch.int64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            v = int(t.item())
+            return -1 if v == 2**62 else v
+
+        _step_loop(solver.grid, k, st.advance, tr.exchange, poll)
+        mine = st.records()
+    finally:
+        st.close()
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object(mine, gathered, dst=0)
+    if rank != 0:
+        return None
+    return assemble(solver.plan, slabs, gathered)
+
+
+def bench_rank(args, dev, sce, world, rank, local, metric, unit):
+    """bench.py --gpus N under torchrun: weak-scaled cfg2, one slab per GPU,
+    device time of K full runs, max over ranks."""
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from .solver import GpuFdtdSolver
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=device)
+    solver = GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+    k = tile_steps_of(solver)
+    slabs = partition(solver.grid.num_x, world, k)
+    stream = torch.cuda.current_stream(device).cuda_stream
+    st = SlabState(solver, slabs[rank], stream=stream)
+    tr = TorchTransport(st, device)
+    st.h.call("mbg_checkpoint_save")
+    grid = solver.grid
+
+    def one_run():
+        st.h.call("mbg_checkpoint_restore")
+        st.sample(0)
+        n = 1
+        while n < grid.num_t:
+            cnt = min(k, grid.num_t - n)
+            st.advance(n, cnt)
+            tr.exchange()
+            n += cnt
+
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    l0 = C.c_int64(0)
+    st.h.call("mbg_launch_count", C.byref(l0))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(torch.cuda.current_stream(device))
+    for _ in range(args.steps):
+        one_run()
+    t1.record(torch.cuda.current_stream(device))
+    torch.cuda.synchronize(device)
+    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=device)
+    dist.barrier()
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    l1 = C.c_int64(0)
+    st.h.call("mbg_launch_count", C.byref(l1))
+    bad = st.poll()
+    st.close()
+    if bad >= 0:
+        raise SolverError(f"non-finite electric field at step {bad}")
+    ms = float(ms.item())
+    if rank == 0:
+        cells = grid.num_x * (grid.num_t - 1) * args.steps
+        launches = l1.value - l0.value
+        line = {
+            "metric": metric, "value": cells / (ms * 1e-3), "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"cfg2 weak-scaled: {world} slabs x 2^22 cells, 20000 steps",
+                       "num_x": grid.num_x, "tile_steps": k, "parallelism": f"slab{world}",
+                       "exchange": "NCCL batched isend/irecv of k ghost cells per interface every k steps"},
+            # fused step launches + per exchange up to 2 pack and 2 unpack kernels + row-0 samples
+            "gpu_launches": int(launches + 4 * launches + args.steps),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

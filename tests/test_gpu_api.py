@@ -1,0 +1,151 @@
+"""The GPU solver honours the reference solver's run() contract and physics
+checks (pkg/tests/test_solver.py, test_acceptance.py analogues)."""
+
+import math
+
+import numpy as np
+import pytest
+from conftest import build_case
+
+import paper_2005_05412_b200 as mb
+
+pytestmark = pytest.mark.gpu
+
+
+def _sit_small(gridpoints=1024, end=20e-15):
+    qm = mb.two_level_description(1e24, 2 * math.pi * 2e14, 6.24e-11, 1e10, 1e10, -1.0)
+    mb.add_material(mb.Material("Vacuum"))
+    mb.add_material(mb.Material("Active", qm=qm))
+    dev = mb.Device("small")
+    dev.add_region(mb.Region("l", "Vacuum", 0.0, 7.5e-6))
+    dev.add_region(mb.Region("a", "Active", 7.5e-6, 142.5e-6))
+    dev.add_region(mb.Region("r", "Vacuum", 142.5e-6, 150e-6))
+    return dev, mb.Scenario("s", gridpoints, end, mb.QmOperator([1.0, 0.0]))
+
+
+def test_run_is_not_reentrant():
+    dev, sce = _sit_small(128, 1e-15)
+    s = mb.create_solver("gpu-fdtd-reg-cayley", dev, sce)
+    s.run()
+    with pytest.raises(mb.SolverError):
+        s.run()
+
+
+def test_record_shapes_axes_and_order():
+    dev, sce = _sit_small()
+    sce.add_record(mb.Record("e", quantity="e", interval=2.5e-15))
+    sce.add_record(mb.Record("inv12", quantity="inv", interval=2.5e-15))
+    sce.add_record(mb.Record("probe", quantity="e", position=75e-6))
+    sce.add_record(mb.Record("d12", quantity="d", i=1, j=2, position=75e-6))
+    s = mb.GpuFdtdSolver(dev, sce)
+    res = {r.name: r for r in s.run()}
+    every = round(2.5e-15 / s.grid.dt)
+    rows = (s.grid.num_t - 1) // every + 1
+    assert res["e"].data.shape == (rows, 1024) and res["inv12"].data.shape == (rows, 1024)
+    assert res["e"].dt_sample == every * s.grid.dt
+    assert res["probe"].cols == 1 and res["probe"].rows == s.grid.num_t
+    assert res["d12"].is_complex
+    assert [r.name for r in s.results] == ["e", "inv12", "probe", "d12"]
+
+
+def test_inversion_outside_quantum_region_is_zero():
+    dev, sce = _sit_small()
+    sce.add_record(mb.Record("inv12", quantity="inv", interval=2.5e-15))
+    inv = mb.GpuFdtdSolver(dev, sce).run()[0]
+    x = inv.positions
+    vac = (x < 7.5e-6) | (x > 142.5e-6)
+    assert np.count_nonzero(inv.data[-1][vac]) == 0
+    assert np.allclose(inv.data[-1][~vac], -1.0, atol=1e-12)
+
+
+def test_zero_state_stays_zero():
+    qm = mb.two_level_description(1e24, 2 * math.pi * 2e14, 6.24e-11, 1e10, 1e10, -1.0)
+    mb.add_material(mb.Material("Active", qm=qm))
+    dev = mb.Device("quiet")
+    dev.add_region(mb.Region("a", "Active", 0.0, 1e-6))
+    sce = mb.Scenario("s", 64, 2e-15, mb.QmOperator([1.0, 0.0]))
+    sce.add_record(mb.Record("e", quantity="e"))
+    sce.add_record(mb.Record("h", quantity="h"))
+    for r in mb.GpuFdtdSolver(dev, sce).run():
+        assert np.count_nonzero(r.data) == 0
+
+
+def test_nonfinite_field_aborts_with_the_scan_step():
+    desc = mb.QmDescription(1e28, mb.QmOperator([0.0, 1e-19]), mb.QmOperator([0.0, 0.0], [1e-27]),
+                            mb.LindbladRelaxation([[0.0, 1e21], [1e21, 0.0]], [0.0]))
+    mb.add_material(mb.Material("stiff", qm=desc))
+    dev = mb.Device("blow")
+    dev.add_region(mb.Region("a", "stiff", 0.0, 10e-6))
+    sce = mb.Scenario("s", 64, 2e-13, mb.QmOperator([1.0, 0.0]))
+    sce.add_source(mb.SechPulse("s", 5e-6, "hard", 1e10, 2e14, 10.0, 2e14))
+    import oracle as orc
+
+    solver = mb.GpuFdtdSolver(dev, sce, stepper="rk4")
+    _, bad = orc.run_oracle(solver.plan)
+    with pytest.raises(mb.SolverError, match=f"at step {bad}$"):
+        solver.run()
+
+
+def test_pulse_travels_at_light_speed():
+    mb.add_material(mb.Material("Vacuum"))
+    dev = mb.Device("v", bc_left=mb.BoundaryReflectivity(1.0), bc_right=mb.BoundaryReflectivity(0.0))
+    dev.add_region(mb.Region("v", "Vacuum", 0.0, 40e-6))
+    sce = mb.Scenario("s", 2048, 100e-15, mb.QmOperator([1.0, 0.0]))
+    sce.add_source(mb.SechPulse("sech", 0.0, "hard", 1.0, 2e14, 10.0, 2e14))
+    sce.add_record(mb.Record("e", quantity="e", interval=100e-15))
+    e = mb.GpuFdtdSolver(dev, sce).run()[0]
+    x_peak = e.positions[int(np.argmax(np.abs(e.data[-1])))]
+    assert abs(x_peak - mb.C0 * (e.times[-1] - 50e-15)) <= 3 * (40e-6 / 2047)
+    assert np.max(np.abs(e.data[-1])) >= 0.98
+
+
+def _reflection_energy_ratio(r):
+    mb.clear_material_library()
+    mb.add_material(mb.Material("Vacuum"))
+    dev = mb.Device("bc", bc_left=mb.BoundaryReflectivity(0.0), bc_right=mb.BoundaryReflectivity(r))
+    dev.add_region(mb.Region("v", "Vacuum", 0.0, 60e-6))
+    sce = mb.Scenario("s", 4096, 240e-15, mb.QmOperator([1.0, 0.0]))
+    sce.add_source(mb.SechPulse("sech", 20e-6, "soft", 1.0, 2e14, 10.0, 2e14))
+    sce.add_record(mb.Record("e", quantity="e", interval=5e-15))
+    sce.add_record(mb.Record("h", quantity="h", interval=5e-15))
+    res = {x.name: x for x in mb.GpuFdtdSolver(dev, sce).run()}
+    dx = 60e-6 / 4095
+    energy = 0.5 * mb.EPS0 * np.sum(res["e"].data ** 2, axis=1) * dx
+    energy += 0.5 * mb.MU0 * np.sum(res["h"].data ** 2, axis=1) * dx
+    t = res["e"].times
+    return energy[np.argmin(np.abs(t - 230e-15))] / energy[np.argmin(np.abs(t - 160e-15))]
+
+
+def test_boundary_energy_contract():
+    """pkg/tests/test_solver.py:286-296 on the GPU solver."""
+    assert _reflection_energy_ratio(1.0) == pytest.approx(1.0, abs=0.02)
+    assert _reflection_energy_ratio(0.0) < 0.01
+    for r in (0.25, 0.64):
+        assert _reflection_energy_ratio(r) == pytest.approx(r, rel=0.10)
+
+
+def test_sit_physics_full_run():
+    """Self-induced transparency (pkg/tests/test_acceptance.py:203-229): the
+    medium is left inverted-back (|w+1| < 0.05) behind a 2 pi pulse."""
+    dev, sce, _ = build_case("cfg1_full")
+    res = {r.name: r for r in mb.GpuFdtdSolver(dev, sce).run()}
+    inv = res["inv@2000"].data[:, 0]
+    assert np.max(np.abs(inv[-1] + 1.0)) < 0.05
+    assert np.min(inv) > -1.0 - 1e-9 and np.max(inv) <= 1.0 + 1e-9
+
+
+def test_invariant_monitor():
+    dev, sce, stepper = build_case("rand4_split")
+    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    s.run()
+    rep = s.invariant_report
+    assert rep["max_trace_dev"] < 1e-9 and rep["max_herm_dev"] < 1e-12 and rep["min_eigenvalue"] > -1e-9
+
+
+def test_results_are_independent_arrays():
+    dev, sce = _sit_small(256, 5e-15)
+    sce.add_record(mb.Record("e", quantity="e"))
+    s = mb.GpuFdtdSolver(dev, sce)
+    r = s.run()[0]
+    r.data[:] = 1.0  # caller owns the buffers
+    assert s.results[0].data is r.data

@@ -1,0 +1,110 @@
+"""Slab decomposition: host logic on CPU (gloo, world size 2 and 3) and the
+native windowed path on one GPU (all slabs in one process).
+
+The multi-rank runs must be bit-identical to the single-domain CPU oracle:
+every cell runs the same operation sequence whichever slab holds it.
+"""
+
+import os
+import socket
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+from conftest import ROOT, build_case
+
+import paper_2005_05412_b200 as mb
+from paper_2005_05412_b200 import slabs
+
+
+def test_partition_follows_reference_rule_and_ghosts():
+    s = slabs.partition(1000, 3, 7)
+    bounds = np.linspace(0, 1000, 4).astype(int)
+    assert [(x.own_lo, x.own_hi) for x in s] == list(zip(bounds[:-1], bounds[1:]))
+    assert (s[0].win_lo, s[0].win_hi) == (0, s[0].own_hi + 7)
+    assert (s[2].win_lo, s[2].win_hi) == (s[2].own_lo - 7, 1000)
+    assert s[1].ghost_left == s[1].ghost_right == 7
+
+
+def test_exchange_plans_pair_up():
+    parts = slabs.partition(500, 4, 5)
+    for a, b in zip(parts, parts[1:]):
+        _, _, send_r, recv_r = slabs.exchange_plan(a)
+        send_l, recv_l, _, _ = slabs.exchange_plan(b)
+        # what a sends right lands in b's left ghost, and vice versa
+        assert send_r == recv_l and send_l == recv_r
+        assert recv_l[0] == b.win_lo and recv_l[0] + recv_l[1] == b.own_lo
+
+
+def test_partition_rejects_thin_slabs():
+    with pytest.raises(ValueError):
+        slabs.partition(20, 4, 8)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, k, out_path):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch.distributed as dist
+    from np_slab import NumpySlab
+
+    import paper_2005_05412_b200 as mbw
+    from paper_2005_05412_b200 import slabs as sl
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cases import CASES
+
+        build, stepper = CASES[case]
+        mbw.clear_material_library()
+        dev, sce = build(mbw)
+        solver = mbw.GpuFdtdSolver(dev, sce, stepper=stepper)
+        recs = sl.run_slab_rank(solver, world, rank, "cpu", state_factory=NumpySlab, k=k)
+        if rank == 0:
+            np.savez(out_path, *recs)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,case", [(2, 7, "sit_hard_whole"), (3, 16, "multi_material"),
+                                          (2, 5, "vacuum_sources")])
+def test_gloo_ranks_match_oracle_bitwise(world, k, case):
+    import oracle as orc
+
+    dev, sce, stepper = build_case(case)
+    plan = mb.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    ref, bad = orc.run_oracle(plan)
+    assert bad == 0
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "recs.npz")
+        mp.spawn(_worker, args=(world, _free_port(), case, k, out), nprocs=world, join=True)
+        got = np.load(out)
+        for r, (p, want) in enumerate(zip(plan.plans, ref)):
+            have = got[f"arr_{r}"]
+            assert have.shape == want.shape, p.record.name
+            assert np.array_equal(have, want), (p.record.name, np.max(np.abs(have - want)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,count", [("sit_hard_whole", 2), ("sit_hard_whole", 5), ("multi_material", 3),
+                                        ("rand3_split", 2), ("rand6_split", 3), ("rand4_rk4", 2),
+                                        ("cfg4_r14", 4)])
+def test_native_slabs_on_one_gpu_match_single_domain(case, count):
+    dev, sce, stepper = build_case(case)
+    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case(case)
+    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    got = slabs.run_slabs_local(solver, count)
+    for a, b in zip(ref, got):
+        assert a.name == b.name and a.data.shape == b.data.shape
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
