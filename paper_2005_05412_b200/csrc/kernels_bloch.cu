@@ -378,14 +378,16 @@ bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     if (!tile_is_interior(L, base, W)) return;
     const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
     const int qm = L.rg.qm[re];
+    // the density step must be the very same formula the edge kernel uses
+    // (bitwise independence of the tiling), so the real-dipole choice is global
     if (qm < 0)
         interior_tile<false, true>(P, t_lo, t_hi, base, lane, re, rh);
-    else if (P.n_qm == 1 && P.real_dipole)
-        interior_tile<true, true, true>(P, t_lo, t_hi, base, lane, re, rh);
-    else if (P.n_qm == 1)
-        interior_tile<true, true>(P, t_lo, t_hi, base, lane, re, rh);
+    else if (P.real_dipole)
+        P.n_qm == 1 ? interior_tile<true, true, true>(P, t_lo, t_hi, base, lane, re, rh)
+                    : interior_tile<true, false, true>(P, t_lo, t_hi, base, lane, re, rh);
     else
-        interior_tile<true, false>(P, t_lo, t_hi, base, lane, re, rh);
+        P.n_qm == 1 ? interior_tile<true, true, false>(P, t_lo, t_hi, base, lane, re, rh)
+                    : interior_tile<true, false, false>(P, t_lo, t_hi, base, lane, re, rh);
 }
 
 // the few remaining tiles (domain/window edges, region interfaces, sources)

@@ -64,12 +64,13 @@ def test_exact_variant_matches_reference(name):
 
 
 @pytest.mark.parametrize("k", [1, 2, 7, 16, 33, 64])
-def test_tile_depth_is_bitwise_invisible(k):
+@pytest.mark.parametrize("name", ["sit_hard_whole", "multi_material", "vacuum_sources"])
+def test_tile_depth_is_bitwise_invisible(name, k):
     """Temporal tiling recomputes halo cells redundantly; every cell runs the
     same instruction sequence, so results must not depend on k."""
-    _, ref = _run("sit_hard_whole", tile_steps=1)
+    _, ref = _run(name, tile_steps=1)
     mb.clear_material_library()
-    _, got = _run("sit_hard_whole", tile_steps=k)
+    _, got = _run(name, tile_steps=k)
     for a, b in zip(ref, got):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
 
