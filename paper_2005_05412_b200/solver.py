@@ -251,7 +251,12 @@ def register_with_reference(mblight_module=None):
     (``mblight.core.register_solver``, core.py:617)."""
     if mblight_module is None:
         import mblight as mblight_module  # noqa: PLC0415
-    register(mblight_module.register_solver)
+    reg = getattr(mblight_module, "register_solver", None)
+    if reg is None:  # mblight re-exports create_solver but not register_solver
+        from importlib import import_module  # noqa: PLC0415
+
+        reg = import_module(mblight_module.__name__ + ".core").register_solver
+    register(reg)
     return mblight_module
 
 

@@ -169,6 +169,41 @@ for _n in (2, 3, 4):
     CASES[f"rand{_n}_rk4"] = random_case(_n, 60 + _n, stepper="rk4")
 CASES["rand2_split"] = random_case(2, 32)
 
+def song_point(api):
+    """Driven V-type three-level system at a single grid point (the reference's
+    song2005 parameters, setups.py:108-146): the Nx = 1 master-equation mode."""
+    hb, e0 = api.HBAR, api.E0
+    h0 = api.QmOperator([0.0, 2.3717e15 * hb, 2.4165e15 * hb])
+    mu = api.QmOperator([0.0, 0.0, 0.0], [-e0 * 9.2374e-11, -e0 * 9.2374e-11 * math.sqrt(2.0), 0.0])
+    rates = [[0.0, 1e10, 1e10], [1e10, 0.0, 1e10], [1e10, 1e10, 0.0]]
+    qm = api.QmDescription(6e24, h0, mu, api.LindbladRelaxation(rates, [0.0, 0.0, 0.0]))
+    act = api.ensure_material(api.Material("Song3", qm=qm))
+    dev = api.Device("Song")
+    dev.add_region(api.Region("point", act.id, 0.0, 0.0))
+    sce = api.Scenario("s", 1, 80e-15, api.QmOperator([1.0, 0.0, 0.0]), num_timesteps=10000)
+    for i in (1, 2, 3):
+        sce.add_record(api.Record(f"d{i}{i}", quantity="d", i=i, j=i, position=0.0))
+    sce.add_record(api.Record("d12", quantity="d", i=1, j=2, position=0.0))
+    sce.add_record(api.Record("e", quantity="e", position=0.0))
+    sce.add_source(api.SechPulse("sech", position=0.0, kind="hard", amplitude=3.5471e9, carrier_freq=3.8118e14,
+                                 envelope_shift=17.248, envelope_rate=1.76 / 5e-15, carrier_phase=-math.pi / 2.0))
+    return dev, sce
+
+
+def point2(api):
+    """Two-level medium at a single grid point driven by a soft source."""
+    qm = api.two_level_description(1e24, 2.0 * math.pi * 2e14, 6.24e-11, 1e11, 1e12, -1.0)
+    act = api.ensure_material(api.Material("P2", qm=qm))
+    dev = api.Device("p2")
+    dev.add_region(api.Region("point", act.id, 0.0, 0.0))
+    sce = api.Scenario("s", 1, 100e-15, api.QmOperator([1.0, 0.0]), num_timesteps=5000)
+    sce.add_record(api.Record("inv", quantity="inv", position=0.0))
+    sce.add_record(api.Record("d12", quantity="d", i=1, j=2, position=0.0))
+    sce.add_record(api.Record("e", quantity="e", position=0.0))
+    sce.add_source(api.SechPulse("s", 0.0, "soft", 4e9, 2e14, 5.0, 2e14))
+    return dev, sce
+
+
 def kernel_case(dim, seed, stepper="splitting", nx=64):
     """One time step over nx cells with random E: isolates the per-cell
     stepper (the scenario-level twin of pkg/tests/test_solver.py:437-480)."""
@@ -193,6 +228,9 @@ def kernel_case(dim, seed, stepper="splitting", nx=64):
     return build, stepper
 
 
+CASES["song_point"] = (song_point, "splitting")
+CASES["song_point_rk4"] = (song_point, "rk4")
+CASES["point2"] = (point2, "splitting")
 for _n in range(2, 9):
     CASES[f"kernel{_n}_split"] = kernel_case(_n, 100 + _n)
 for _n in (2, 3, 4, 5):

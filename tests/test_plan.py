@@ -178,3 +178,24 @@ def test_plan_from_reference_objects_equals_plan_from_mirror():
                     assert np.array_equal(getattr(qa, f), getattr(qb, f)), f
             assert qa.bloch == qb.bloch
     mblight.clear_material_library()
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not mounted (GPU box)")
+def test_registration_into_the_reference_registry():
+    import os
+
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, str(REF))
+    import mblight
+
+    from cases import CASES
+
+    mb.register_with_reference(mblight)
+    assert {"gpu-fdtd-reg-cayley", "gpu-fdtd-rk4"} <= set(mblight.available_solvers())
+    build, _ = CASES["sit_hard_whole"]
+    mblight.clear_material_library()
+    dev, sce = build(mblight)
+    s = mblight.create_solver("gpu-fdtd-reg-cayley", dev, sce, seed=3)
+    assert isinstance(s, mb.GpuFdtdSolver) and s.seed == 3
+    assert s._result_cls is mblight.Result
+    mblight.clear_material_library()
