@@ -146,13 +146,14 @@ Launch base_launch(const mbg_solver *s) {
 
 template <int N>
 void fill_split(DenseQm<N> &d, const QmHost &h) {
+    // B/2 = bc/2 + E bf/2 (exact halving): its inverse is 2 (I + iA)^-1
     for (int i = 0; i < N * N; ++i) {
         d.pop[i] = h.pop[i];
         d.coh[i] = h.coh[i];
-        d.bc_re[i] = h.bc[2 * i];
-        d.bc_im[i] = h.bc[2 * i + 1];
-        d.bf_re[i] = h.bf[2 * i];
-        d.bf_im[i] = h.bf[2 * i + 1];
+        d.bc_re[i] = 0.5 * h.bc[2 * i];
+        d.bc_im[i] = 0.5 * h.bc[2 * i + 1];
+        d.bf_re[i] = 0.5 * h.bf[2 * i];
+        d.bf_im[i] = 0.5 * h.bf[2 * i + 1];
     }
     for (int p = 0; p < N * (N - 1) / 2; ++p) {
         d.pol.pol_re[p] = h.pol_re[p];

@@ -1,0 +1,492 @@
+// Fused time-step kernels for N-level media, N = 2 (RK4) and 3..8.
+//
+// One thread per cell, one CTA per tile of kDenseTile consecutive cells, k
+// time steps per launch (temporal tiling with redundant halos, as in the
+// two-level kernel).  The per-cell density matrix never leaves the SM while
+// the launch runs: it is Hermitian-packed (N real diagonal words, then re/im
+// of the upper triangle in row-major order) in registers for N <= 4 and in a
+// per-thread shared-memory column for larger N.  E and H live in registers;
+// neighbours are exchanged through two small double-buffered shared arrays
+// (two barriers per step).
+//
+// Splitting step (_kernels.py:87-160, quantum.py:444-460), same mathematics,
+// restructured for registers:
+//   r1 = relax_half(rho)                                    quantum.py:425-428
+//   G  = (I + iA)^-1 by in-place Gauss-Jordan, no pivoting   (|leading minors| >= 1)
+//   U  = 2G - I  ( = (I + iA)^-1 (I - iA), the Cayley unitary of quantum.py:431-441 )
+//   rho' = U r1 U^H row by row (upper triangle), relax_half(rho')
+//   p = pol_factor * [sum_{i<j} 2 Re(mu_ij (rho'-rho)_ji) + sum_i mu_ii (rho'-rho)_ii]
+// RK4 step (_kernels.py:256-332): classical RK4 of the master equation on the
+// packed Hermitian state (the reference symmetrises after each step).
+#pragma once
+#include "mbg_kernels.h"
+
+#ifndef MBG_VARIANT
+#error "compile with -DMBG_VARIANT=fast|exact"
+#endif
+
+namespace mbg {
+namespace MBG_VARIANT {
+namespace dense {
+
+// tile width (threads = cells per CTA); the largest state layouts use 64
+template <int N, bool RK4>
+constexpr int tile_width() { return N >= 7 ? 64 : kDenseTile; }
+
+// packed word index of upper pair (i < j), row-major
+__host__ __device__ constexpr int pair_index(int n, int i, int j) { return i * n - i * (i + 1) / 2 + (j - i - 1); }
+__host__ __device__ constexpr int wre(int n, int i, int j) { return n + 2 * pair_index(n, i, j); }
+__host__ __device__ constexpr int wim(int n, int i, int j) { return n + 2 * pair_index(n, i, j) + 1; }
+
+template <int NW>
+struct RegVec {
+    double v[NW];
+    __device__ __forceinline__ double &operator[](int w) { return v[w]; }
+};
+template <int TW>
+struct SmemVec {
+    double *p;  // this thread's column; word w at p[w * TW]
+    __device__ __forceinline__ double &operator[](int w) { return p[w * TW]; }
+};
+template <int N>
+struct RegMat {
+    double re[N * N], im[N * N];
+    __device__ __forceinline__ double &r(int i, int j) { return re[i * N + j]; }
+    __device__ __forceinline__ double &m(int i, int j) { return im[i * N + j]; }
+};
+template <int N, int TW>
+struct SmemMat {
+    SmemVec<TW> re, im;
+    __device__ __forceinline__ double &r(int i, int j) { return re[i * N + j]; }
+    __device__ __forceinline__ double &m(int i, int j) { return im[i * N + j]; }
+};
+
+// Hermitian element (i, j) of a packed state
+template <int N, class V>
+__device__ __forceinline__ void herm(V &s, int i, int j, double &re, double &im) {
+    if (i == j) {
+        re = s[i];
+        im = 0.0;
+    } else if (i < j) {
+        re = s[wre(N, i, j)];
+        im = s[wim(N, i, j)];
+    } else {
+        re = s[wre(N, j, i)];
+        im = -s[wim(N, j, i)];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
+template <int N, class VA, class VB, class MG>
+__device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G) {
+    double od[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) od[i] = A[i];
+    // relaxation half step -> B
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double acc = q.pop[i * N] * A[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], A[j], acc);
+        B[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+            B[wre(N, i, j)] = A[wre(N, i, j)] * q.coh[i * N + j];
+            B[wim(N, i, j)] = A[wim(N, i, j)] * q.coh[i * N + j];
+        }
+    // G = (B/2)^-1 = 2 (I + iA)^-1: the host halves bc and bf (exact), so the
+    // Gauss-Jordan inverse (in place, no pivoting) is already 2(I + iA)^-1
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) {
+        G.r(i / N, i % N) = mad(e, q.bf_re[i], q.bc_re[i]);
+        G.m(i / N, i % N) = mad(e, q.bf_im[i], q.bc_im[i]);
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const double pr = G.r(k, k), pi = G.m(k, k);
+        const double rd = 1.0 / mad(pi, pi, pr * pr);
+        const double ir = pr * rd, ii = -pi * rd;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (j == k) continue;
+            const double xr = G.r(k, j), xi = G.m(k, j);
+            G.r(k, j) = mad(xr, ir, -(xi * ii));
+            G.m(k, j) = mad(xr, ii, xi * ir);
+        }
+        G.r(k, k) = ir;
+        G.m(k, k) = ii;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            if (i == k) continue;
+            const double fr = G.r(i, k), fi = G.m(i, k);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                if (j == k) continue;
+                const double kr = G.r(k, j), ki = G.m(k, j);
+                G.r(i, j) = mad(-fr, kr, mad(fi, ki, G.r(i, j)));
+                G.m(i, j) = mad(-fr, ki, mad(-fi, kr, G.m(i, j)));
+            }
+            G.r(i, k) = mad(-fr, ir, fi * ii);
+            G.m(i, k) = mad(-fr, ii, -(fi * ir));
+        }
+    }
+    // U = 2(I + iA)^-1 - I = G - I
+#pragma unroll
+    for (int i = 0; i < N; ++i) G.r(i, i) -= 1.0;
+    // rho' = U r1 U^H, one row at a time; second relaxation half step fused
+    double acc_p = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double tr[N], ti[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            double ar = 0.0, ai = 0.0;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+                const double ur = G.r(i, m), ui = G.m(i, m);
+                if (m == k) {  // real diagonal of r1
+                    const double rr = B[m];
+                    ar = mad(ur, rr, ar);
+                    ai = mad(ui, rr, ai);
+                } else {
+                    double rr, ri;
+                    herm<N>(B, m, k, rr, ri);
+                    ar = mad(ur, rr, mad(-ui, ri, ar));
+                    ai = mad(ur, ri, mad(ui, rr, ai));
+                }
+            }
+            tr[k] = ar;
+            ti[k] = ai;
+        }
+#pragma unroll
+        for (int j = i; j < N; ++j) {
+            double ar = 0.0, ai = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const double ur = G.r(j, k), ui = G.m(j, k);  // conj(U_jk) = ur - i ui
+                ar = mad(tr[k], ur, mad(ti[k], ui, ar));
+                if (j != i) ai = mad(ti[k], ur, mad(-tr[k], ui, ai));  // diagonal is real
+            }
+            if (j == i) {
+                A[i] = ar;  // raw diagonal; relaxed below
+            } else {
+                const double c = q.coh[i * N + j];
+                const double fr = ar * c, fi = ai * c;
+                const int p = pair_index(N, i, j);
+                acc_p += 2.0 * mad(q.pol.pol_im[p], fi - A[wim(N, i, j)], q.pol.pol_re[p] * (fr - A[wre(N, i, j)]));
+                A[wre(N, i, j)] = fr;
+                A[wim(N, i, j)] = fi;
+            }
+        }
+    }
+    double raw[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) raw[i] = A[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double acc = q.pop[i * N] * raw[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], raw[j], acc);
+        A[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc_p = mad(q.pol.pol_dv[i], A[i] - od[i], acc_p);
+    return q.pol.pol_factor * acc_p;
+}
+
+// ---------------------------------------------------------------------------
+// RK4: f(src) = -i/hbar [H, src] + D(src) on packed Hermitian states.
+// Only the upper triangle + diagonal of the (Hermitian) derivative is formed.
+template <int N, class VS, class VD>
+__device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, const double *hi, VS &src, VD &dst) {
+    constexpr double kInvHbar = 1.0 / 1.054571817e-34;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i; j < N; ++j) {
+            // [H, S]_ij = sum_k H_ik S_kj - S_ik H_kj
+            double cr = 0.0, ci = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                double sr, si, tr, ti;
+                herm<N>(src, k, j, sr, si);
+                herm<N>(src, i, k, tr, ti);
+                const double ar = hr[i * N + k], ai = hi[i * N + k];
+                const double br = hr[k * N + j], bi = hi[k * N + j];
+                cr += mad(ar, sr, -(ai * si)) - mad(tr, br, -(ti * bi));
+                ci += mad(ar, si, ai * sr) - mad(tr, bi, ti * br);
+            }
+            // -i/hbar * (cr + i ci) = (ci/hbar, -cr/hbar)
+            double dr = ci * kInvHbar, di = -cr * kInvHbar;
+            if (i == j) {
+                double acc = q.popm[i * N] * src[0];
+#pragma unroll
+                for (int m = 1; m < N; ++m) acc = mad(q.popm[i * N + m], src[m], acc);
+                dst[i] = dr + acc;
+            } else {
+                const double g = q.deph[i * N + j];
+                dst[wre(N, i, j)] = mad(-g, src[wre(N, i, j)], dr);
+                dst[wim(N, i, j)] = mad(-g, src[wim(N, i, j)], di);
+            }
+        }
+}
+
+template <int N, class VA, class VB>
+__device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, VB &S, VB &K, VB &Acc) {
+    constexpr int NW = N * N;
+    double hr[N * N], hi[N * N];
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) {
+        hr[i] = mad(-e, q.mu_re[i], q.h0_re[i]);
+        hi[i] = mad(-e, q.mu_im[i], q.h0_im[i]);
+    }
+    const double dt = q.dt;
+    // k1
+    master_rhs<N>(q, hr, hi, A, K);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        Acc[w] = K[w];
+        S[w] = mad(0.5 * dt, K[w], A[w]);
+    }
+    master_rhs<N>(q, hr, hi, S, K);  // k2
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        Acc[w] = mad(2.0, K[w], Acc[w]);
+        S[w] = mad(0.5 * dt, K[w], A[w]);
+    }
+    master_rhs<N>(q, hr, hi, S, K);  // k3
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        Acc[w] = mad(2.0, K[w], Acc[w]);
+        S[w] = mad(dt, K[w], A[w]);
+    }
+    master_rhs<N>(q, hr, hi, S, K);  // k4
+    const double sixth = dt / 6.0;
+    double acc_p = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+            const int p = pair_index(N, i, j);
+            const double nr = mad(sixth, Acc[wre(N, i, j)] + K[wre(N, i, j)], A[wre(N, i, j)]);
+            const double ni = mad(sixth, Acc[wim(N, i, j)] + K[wim(N, i, j)], A[wim(N, i, j)]);
+            acc_p += 2.0 * mad(q.pol.pol_im[p], ni - A[wim(N, i, j)], q.pol.pol_re[p] * (nr - A[wre(N, i, j)]));
+            A[wre(N, i, j)] = nr;
+            A[wim(N, i, j)] = ni;
+        }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const double nd = mad(sixth, Acc[i] + K[i], A[i]);
+        acc_p = mad(q.pol.pol_dv[i], nd - A[i], acc_p);
+        A[i] = nd;
+    }
+    return q.pol.pol_factor * acc_p;
+}
+
+// ---------------------------------------------------------------------------
+// the fused step kernel
+
+template <int N, bool RK4>
+struct Layout {
+    static constexpr int NW = N * N;
+    static constexpr bool kRegState = RK4 ? (N <= 3) : (N <= 4);
+    static constexpr bool kRegG = N <= 6;
+    // smem words per thread: A/B (or A/S/K/Acc for RK4) when not in registers, G when not in regs
+    static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 4 * NW : 2 * NW);
+    static constexpr int kGWords = (RK4 || kRegG) ? 0 : 2 * NW;
+    static constexpr int kFieldWords = 6;  // Es[2], Hs[2], Ho[2]
+    static constexpr int TW = tile_width<N, RK4>();
+    static constexpr size_t smem_bytes() { return sizeof(double) * TW * (kFieldWords + kStateWords + kGWords); }
+};
+
+template <int N, bool RK4, class Q>
+__device__ __forceinline__ double cell_step(const Q &q, double e, double *col, RegVec<N * N> &A) {
+    using Lay = Layout<N, RK4>;
+    constexpr int NW = N * N, TW = Lay::TW;
+    if constexpr (RK4) {
+        if constexpr (Lay::kRegState) {
+            RegVec<NW> S, K, Acc;
+            return rk4_cell<N>(q, e, A, S, K, Acc);
+        } else {
+            SmemVec<TW> As{col}, S{col + NW * TW}, K{col + 2 * NW * TW}, Acc{col + 3 * NW * TW};
+            return rk4_cell<N>(q, e, As, S, K, Acc);
+        }
+    } else {
+        if constexpr (Lay::kRegState) {
+            RegVec<NW> B;
+            RegMat<N> G;
+            return split_cell<N>(q, e, A, B, G);
+        } else if constexpr (Lay::kRegG) {
+            SmemVec<TW> As{col}, B{col + NW * TW};
+            RegMat<N> G;
+            return split_cell<N>(q, e, As, B, G);
+        } else {
+            SmemVec<TW> As{col}, B{col + NW * TW};
+            SmemMat<N, TW> G{{col + 2 * NW * TW}, {col + 3 * NW * TW}};
+            return split_cell<N>(q, e, As, B, G);
+        }
+    }
+}
+
+// One tile of the fused step.  INTERIOR: every cell regular, one E and one H
+// region, no source/boundary (no per-cell predicates, scalar coefficients);
+// ONE_QM: the stepper constants are compile-time offsets into the parameter
+// block (constant-bank operands of the FP64 instructions).
+template <int N, bool RK4, class Q, bool INTERIOR, bool ONE_QM>
+__device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *sm, long long t_lo, long long t_hi,
+                                           long long base) {
+    using Lay = Layout<N, RK4>;
+    constexpr int NW = N * N, W = Lay::TW;
+    double *Es = sm, *Hs = sm + 2 * W, *Ho = sm + 4 * W;
+    double *col = sm + 6 * W + threadIdx.x;  // per-thread state column
+    const Launch &L = P.L;
+    const long long nx = L.num_x;
+    const int j = threadIdx.x;
+    const long long c = base + j;
+    const long long l = c - L.win_lo;
+    const bool in_e = INTERIOR || (l >= 0 && l < L.win_n && c < nx);
+    double E = in_e ? L.e_in[l] : 0.0;
+    double H = (INTERIOR || (l >= 0 && l <= L.win_n)) ? L.h_in[l] : 0.0;
+    const int re = region_of(L.rg.e_start, L.rg.n, INTERIOR ? base : c);
+    const int rh = region_of(L.rg.h_start, L.rg.n, INTERIOR ? base : c);
+    const double ca = L.rg.a[re], cbg = L.rg.bg[re], cbdx = L.rg.bdx[re], cch = L.rg.ch[rh];
+    const int qi = in_e ? L.rg.qm[re] : -1;
+    const Q &q = P.qm[ONE_QM ? 0 : (qi < 0 ? 0 : qi)];
+    RegVec<NW> rA;
+    if (qi >= 0) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const double v = L.s_in[w * L.plane + l];
+            if constexpr (Lay::kRegState) rA[w] = v; else col[w * W] = v;
+        }
+    }
+    const bool upd_h = INTERIOR || (c >= 1 && c <= nx - 1);
+    const bool upd_e = INTERIOR || (nx > 1 && c >= 0 && c < nx);
+    const bool left_edge = !INTERIOR && L.has_boundary && base == 0 && j == 0;
+    const bool right_edge = !INTERIOR && L.has_boundary && c == nx - 1;
+    const bool own = c >= t_lo && c < t_hi && c >= L.own_lo && c < L.own_hi;
+
+    for (int s = 0; s < L.k; ++s) {
+        const long long n = L.n0 + s;
+        const int b = (s & 1) * W;
+        Es[b + j] = E;
+        if (!INTERIOR) Ho[b + j] = H;
+        __syncthreads();
+        const double el = j > 0 ? Es[b + j - 1] : 0.0;
+        const double hn = upd_h ? mad(cch, E - el, H) : H;
+        Hs[b + j] = hn;
+        double p = 0.0;
+        if (qi >= 0) p = cell_step<N, RK4>(q, E, col, rA);
+        __syncthreads();
+        const double hr = j < W - 1 ? Hs[b + j + 1] : 0.0;
+        double en = upd_e ? mad(cbdx, hr - hn, mad(ca, E, -(cbg * p))) : E;
+        if (!INTERIOR) {
+            if (left_edge) {
+                const double e_at = mad(L.l_c, Es[b + 1], L.l_omc * E);
+                const double h_at = 0.5 * (Ho[b + 1] + hr);
+                en = L.l_hw * mad(L.l_z, h_at, e_at);
+            }
+            if (right_edge) {
+                const double e_at = mad(L.r_c, el, L.r_omc * E);
+                const double h_at = 0.5 * (H + hn);
+                en = L.r_hw * mad(-L.r_z, h_at, e_at);
+            }
+            for (int qq = 0; qq < L.n_src; ++qq) {
+                if (c == L.src_cell[qq]) {
+                    const double v = L.src_values[n * L.n_src + qq];
+                    en = L.src_hard[qq] ? v : en + v;
+                }
+            }
+        }
+        E = en;
+        H = hn;
+        const unsigned long long mask = L.step_mask[s];
+        const bool check = (L.check_mask >> s) & 1ull;
+        if ((mask || check) && own) {
+            if (check && !isfinite(E)) atomicMin(L.bad_step, (unsigned long long)n);
+            for (int r = 0; r < L.n_rec; ++r) {
+                if (!((mask >> r) & 1ull)) continue;
+                const long long cell = L.rec_cell[r];
+                if (cell >= 0 && cell != c) continue;
+                const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+                double vre = 0.0, vim = 0.0;
+                const int qq = L.rec_q[r];
+                if (qq == MBG_Q_E) {
+                    vre = E;
+                } else if (qq == MBG_Q_H) {
+                    vre = H;
+                } else if (qi >= 0) {
+                    if constexpr (Lay::kRegState) {
+                        RegVec<NW> &A = rA;
+                        if (qq == MBG_Q_D) {
+                            // runtime (i, j): walk the compile-time index space
+#pragma unroll
+                            for (int a = 0; a < N; ++a)
+#pragma unroll
+                                for (int bb = 0; bb < N; ++bb)
+                                    if (a == L.rec_i[r] && bb == L.rec_j[r]) herm<N>(A, a, bb, vre, vim);
+                        } else {
+                            vre = A[1] - A[0];
+                        }
+                    } else {
+                        SmemVec<W> A{col};
+                        if (qq == MBG_Q_D) {
+                            const int a = L.rec_i[r], bb = L.rec_j[r];
+                            if (a == bb) {
+                                vre = A[a];
+                            } else if (a < bb) {
+                                vre = A[wre(N, a, bb)];
+                                vim = A[wim(N, a, bb)];
+                            } else {
+                                vre = A[wre(N, bb, a)];
+                                vim = -A[wim(N, bb, a)];
+                            }
+                        } else {
+                            vre = A[1] - A[0];
+                        }
+                    }
+                }
+                L.rec_re[r][idx] = vre;
+                if (L.rec_im[r]) L.rec_im[r][idx] = vim;
+            }
+        }
+    }
+    if (c >= t_lo && c < t_hi) {
+        L.e_out[l] = E;
+        L.h_out[l] = H;
+        if (qi >= 0) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                if constexpr (Lay::kRegState) L.s_out[w * L.plane + l] = rA[w];
+                else L.s_out[w * L.plane + l] = col[w * W];
+            }
+        }
+    }
+}
+
+template <int N, bool RK4, class Q>
+__global__ void __launch_bounds__(Layout<N, RK4>::TW) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
+    using Lay = Layout<N, RK4>;
+    extern __shared__ double sm[];
+    const Launch &L = P.L;
+    const long long t_lo = L.res_lo + (long long)blockIdx.x * L.tile_own;
+    if (t_lo >= L.res_hi) return;  // uniform per block
+    const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
+    const long long base = tile_base(L, t_lo);
+    if (tile_is_interior(L, base, Lay::TW)) {
+        if (P.n_qm == 1)
+            dense_tile<N, RK4, Q, true, true>(P, sm, t_lo, t_hi, base);
+        else
+            dense_tile<N, RK4, Q, true, false>(P, sm, t_lo, t_hi, base);
+    } else {
+        dense_tile<N, RK4, Q, false, false>(P, sm, t_lo, t_hi, base);
+    }
+}
+
+}  // namespace dense
+}  // namespace MBG_VARIANT
+}  // namespace mbg

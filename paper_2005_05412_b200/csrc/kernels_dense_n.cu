@@ -1,0 +1,48 @@
+// Instantiation unit of the N-level kernels for N = MBG_LEVELS (one file per
+// N so the heavily unrolled templates compile in parallel).
+#include "kernels_dense.cuh"
+
+#ifndef MBG_LEVELS
+#error "compile with -DMBG_LEVELS=N"
+#endif
+
+namespace mbg {
+namespace MBG_VARIANT {
+namespace dense {
+
+template <int N, bool RK4, class Q>
+static cudaError_t launch_n(const void *params, long long tiles, cudaStream_t st) {
+    const auto &P = *static_cast<const DenseParams<N, Q> *>(params);
+    constexpr size_t smem = Layout<N, RK4>::smem_bytes();
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!configured[dev]) {
+        cudaError_t err = cudaFuncSetAttribute(dense_step_kernel<N, RK4, Q>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        configured[dev] = true;
+    }
+    dense_step_kernel<N, RK4, Q><<<(unsigned)tiles, Layout<N, RK4>::TW, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+#define MBG_CAT2(a, b) a##b
+#define MBG_CAT(a, b) MBG_CAT2(a, b)
+
+cudaError_t MBG_CAT(launch_split_, MBG_LEVELS)(const void *params, long long tiles, cudaStream_t st) {
+#if MBG_LEVELS >= 3
+    return launch_n<MBG_LEVELS, false, DenseQm<MBG_LEVELS>>(params, tiles, st);
+#else
+    return cudaErrorInvalidValue;
+#endif
+}
+
+cudaError_t MBG_CAT(launch_rk4_, MBG_LEVELS)(const void *params, long long tiles, cudaStream_t st) {
+    return launch_n<MBG_LEVELS, true, Rk4Qm<MBG_LEVELS>>(params, tiles, st);
+}
+
+}  // namespace dense
+}  // namespace MBG_VARIANT
+}  // namespace mbg
