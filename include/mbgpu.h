@@ -58,7 +58,7 @@ extern "C" {
 #define MBG_MAX_SOURCES 8
 #define MBG_MAX_RECORDS 64
 #define MBG_MAX_LEVELS 8
-#define MBG_MAX_TILE_STEPS 64
+#define MBG_MAX_TILE_STEPS 128
 
 typedef struct mbg_solver mbg_solver;
 

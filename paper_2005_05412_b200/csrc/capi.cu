@@ -85,13 +85,13 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
     } while (0)
 
 int default_tile_steps(int levels, int stepper) {
-    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 24;
+    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 64;
     if (levels <= 3) return 8;
     return 4;
 }
 
 int tile_width(const mbg_solver *s) {
-    if (s->bloch || s->g.levels == 0) return kBlochTile;
+    if (s->bloch || s->g.levels == 0) return s->g.exact ? exact::bloch_cta_tile() : fast::bloch_cta_tile();
     return s->g.levels >= 7 ? 64 : kDenseTile;
 }
 
@@ -281,7 +281,10 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
     s->plane = (s->win_n + 31) / 32 * 32;  // 256-byte aligned planes
     int k = g.tile_steps > 0 ? g.tile_steps : default_tile_steps(g.levels, g.stepper);
     const int w = tile_width(s);
-    k = std::min(k, std::min(MBG_MAX_TILE_STEPS, (w - 32) / 2));
+    // every tile (and, for the two-level kernel, every warp tile of the edge
+    // kernel) must keep at least 32 result cells
+    const int wmin = (s->bloch || g.levels == 0) ? std::min(w, kBlochTile) : w;
+    k = std::min(k, std::min(MBG_MAX_TILE_STEPS, (wmin - 32) / 2));
     s->k = std::max(k, 1);
     auto cleanup = [&](int code) {
         mbg_destroy(s);
@@ -621,7 +624,7 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
             for (size_t r = 0; r < s->recs.size(); ++r)
                 if (step % s->recs[r].every == 0) m |= 1ull << r;
             L.step_mask[t] = m;
-            if (step % 1024 == 0 || step == s->g.num_t - 1) L.check_mask |= 1ull << t;
+            L.check[t] = (step % 1024 == 0 || step == s->g.num_t - 1) ? 1 : 0;
         }
         const long long tiles = (L.res_hi - L.res_lo + L.tile_own - 1) / L.tile_own;
         CK(launch_step(s, L, tiles));

@@ -231,7 +231,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         }
         // ---- non-finite scan and records (owned result cells only) --------------
         const unsigned long long mask = L.step_mask[s];
-        const bool check = (L.check_mask >> s) & 1ull;
+        const bool check = L.check[s] != 0;
         if (mask || check) {
 #pragma unroll
             for (int i = 0; i < C; ++i) {
@@ -279,18 +279,23 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
 
 // Interior tiles (the overwhelming majority): every slot is a regular cell of
 // the window (1 <= c <= Nx-2), one E region and one H region, no source and no
-// boundary cell.  Blocked layout: lane l holds the C consecutive cells
-// base + l*C .. base + l*C + C-1, so the stencil needs one shuffle of E up and
-// one of H down per lane and step; everything else is in-register.  For a
-// single quantum material the stepper constants are constant-bank operands.
+// boundary cell.  A CTA of 4 warps owns kBlochCtaTile consecutive cells;
+// inside a warp the layout is blocked (lane l holds C consecutive cells), so
+// the stencil needs one shuffle of E up and one of H down per lane and step,
+// and the two cells at each warp seam go through double-buffered shared
+// slots (two barriers per step).  For a single quantum material the stepper
+// constants are constant-bank operands.
 template <bool QM, bool ONE_QM, bool REAL = false>
-__device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
-                                              int lane, int r_e, int r_h) {
+__device__ __forceinline__ void interior_cta(const BlochParams &P, long long t_lo, long long t_hi, long long base,
+                                             int r_e, int r_h) {
+    __shared__ double seam_e[2][kBlochWarpsPerBlock], seam_h[2][kBlochWarpsPerBlock];
     const Launch &L = P.L;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double a = L.rg.a[r_e], bg = L.rg.bg[r_e], bdx = L.rg.bdx[r_e], ch = L.rg.ch[r_h];
     const int qmi = QM ? (ONE_QM ? 0 : L.rg.qm[r_e]) : 0;
     const BlochQm &q = P.qm[qmi];
-    const long long l0 = base - L.win_lo + (long long)lane * C;
+    const long long first = base + (long long)warp * W + (long long)lane * C;  // this lane's first cell
+    const long long l0 = first - L.win_lo;
     double E[C], H[C], X[C], Y[C], Z[C];
 #pragma unroll
     for (int i = 0; i < C; ++i) {
@@ -303,11 +308,18 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
         }
     }
     for (int s = 0; s < L.k; ++s) {
+        const int b = s & 1;
         // H update (uses E^{n-1}); H is overwritten in place with H^{n-1/2}
-        const double el0 = __shfl_up_sync(kFull, E[C - 1], 1);
+        if (lane == 31) seam_e[b][warp] = E[C - 1];
+        double el0 = __shfl_up_sync(kFull, E[C - 1], 1);
+        __syncthreads();
+        if (lane == 0 && warp > 0) el0 = seam_e[b][warp - 1];
 #pragma unroll
         for (int i = C - 1; i >= 0; --i) H[i] = mad(ch, E[i] - (i == 0 ? el0 : E[i - 1]), H[i]);
-        const double hr_last = __shfl_down_sync(kFull, H[0], 1);
+        if (lane == 0) seam_h[b][warp] = H[0];
+        double hr_last = __shfl_down_sync(kFull, H[0], 1);
+        __syncthreads();
+        if (lane == 31 && warp < kBlochWarpsPerBlock - 1) hr_last = seam_h[b][warp + 1];
         // density step + E update, slot by slot
 #pragma unroll
         for (int i = 0; i < C; ++i) {
@@ -319,12 +331,12 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
             E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bg * p))) : mad(bdx, hr - H[i], a * E[i]);
         }
         const unsigned long long mask = L.step_mask[s];
-        const bool check = (L.check_mask >> s) & 1ull;
+        const bool check = L.check[s] != 0;
         if (mask || check) {
             const long long n = L.n0 + s;
 #pragma unroll
             for (int i = 0; i < C; ++i) {
-                const long long c = base + (long long)lane * C + i;
+                const long long c = first + i;
                 if (c < t_lo || c >= t_hi || c < L.own_lo || c >= L.own_hi) continue;
                 if (check && !isfinite(E[i])) atomicMin(L.bad_step, (unsigned long long)n);
                 for (int r = 0; r < L.n_rec; ++r) {
@@ -350,7 +362,7 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
     }
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-        const long long c = base + (long long)lane * C + i;
+        const long long c = first + i;
         if (c < t_lo || c >= t_hi) continue;
         L.e_out[l0 + i] = E[i];
         L.h_out[l0 + i] = H[i];
@@ -362,43 +374,44 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, long long t_
     }
 }
 
+// 16 resident warps per SM (128 registers per thread)
 #ifndef MBG_BLOCH_MINB
-#define MBG_BLOCH_MINB 4
+#define MBG_BLOCH_MINB (16 / MBG_BLOCH_WARPS > 0 ? 16 / MBG_BLOCH_WARPS : 1)
 #endif
-// interior tiles: every warp classifies its tile and leaves if it is not interior
+constexpr int kEdgeWarps = 4;
+// interior tiles: one CTA per tile; the whole CTA leaves if its tile is not
+// interior (the host hands those to the edge kernel)
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
 bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     const Launch &L = P.L;
-    const int lane = threadIdx.x & 31;
-    const long long tile = (long long)blockIdx.x * kBlochWarpsPerBlock + (threadIdx.x >> 5);
-    const long long t_lo = L.res_lo + tile * L.tile_own;
+    const long long t_lo = L.res_lo + (long long)blockIdx.x * L.tile_own;
     if (t_lo >= L.res_hi) return;
     const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
     const long long base = tile_base(L, t_lo);
-    if (!tile_is_interior(L, base, W)) return;
+    if (!tile_is_interior(L, base, kBlochCtaTile)) return;
     const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
     const int qm = L.rg.qm[re];
     // the density step must be the very same formula the edge kernel uses
     // (bitwise independence of the tiling), so the real-dipole choice is global
     if (qm < 0)
-        interior_tile<false, true>(P, t_lo, t_hi, base, lane, re, rh);
+        interior_cta<false, true>(P, t_lo, t_hi, base, re, rh);
     else if (P.real_dipole)
-        P.n_qm == 1 ? interior_tile<true, true, true>(P, t_lo, t_hi, base, lane, re, rh)
-                    : interior_tile<true, false, true>(P, t_lo, t_hi, base, lane, re, rh);
+        P.n_qm == 1 ? interior_cta<true, true, true>(P, t_lo, t_hi, base, re, rh)
+                    : interior_cta<true, false, true>(P, t_lo, t_hi, base, re, rh);
     else
-        P.n_qm == 1 ? interior_tile<true, true, false>(P, t_lo, t_hi, base, lane, re, rh)
-                    : interior_tile<true, false, false>(P, t_lo, t_hi, base, lane, re, rh);
+        P.n_qm == 1 ? interior_cta<true, true, false>(P, t_lo, t_hi, base, re, rh)
+                    : interior_cta<true, false, false>(P, t_lo, t_hi, base, re, rh);
 }
 
-// the few remaining tiles (domain/window edges, region interfaces, sources)
-__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32)
+// the few remaining cells (domain/window edges, region interfaces, sources),
+// one warp per result range of at most 32*C - 2k cells
+__global__ void __launch_bounds__(kEdgeWarps * 32)
 bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ EdgeTiles T) {
     const Launch &L = P.L;
     const int lane = threadIdx.x & 31;
-    const int w = blockIdx.x * kBlochWarpsPerBlock + (threadIdx.x >> 5);
+    const int w = blockIdx.x * kEdgeWarps + (threadIdx.x >> 5);
     if (w >= T.n) return;
-    const long long t_lo = L.res_lo + T.tile[w] * L.tile_own;
-    const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
+    const long long t_lo = T.lo[w], t_hi = T.hi[w];
     const long long base = tile_base(L, t_lo);
     const long long lo = base, hi = base + W - 1 < L.num_x ? base + W - 1 : L.num_x - 1;
     const bool uni = region_of(L.rg.e_start, L.rg.n, lo) == region_of(L.rg.e_start, L.rg.n, hi) &&
@@ -411,6 +424,8 @@ bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
 }
 
 }  // namespace
+
+int bloch_cta_tile() { return kBlochCtaTile; }
 
 // The edge tiles (a handful of latency-bound warps) run on a side stream,
 // forked from and joined back into the launch stream, so they overlap the
@@ -426,20 +441,24 @@ cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,
     T.n = 0;
     auto flush = [&]() -> cudaError_t {
         if (T.n == 0) return cudaSuccess;
-        const int blocks = (T.n + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
-        bloch_edge_kernel<<<blocks, kBlochWarpsPerBlock * 32, 0, st_edge>>>(P, T);
+        const int blocks = (T.n + kEdgeWarps - 1) / kEdgeWarps;
+        bloch_edge_kernel<<<blocks, kEdgeWarps * 32, 0, st_edge>>>(P, T);
         T.n = 0;
         return cudaGetLastError();
     };
+    const long long warp_own = W - 2 * L.k;  // result cells one warp tile can deliver
     for (long long t = 0; t < tiles; ++t) {
         const long long t_lo = L.res_lo + t * L.tile_own;
-        if (tile_is_interior(L, tile_base(L, t_lo), W)) continue;
-        T.tile[T.n++] = t;
-        if (T.n == kMaxEdgeTiles && (err = flush()) != cudaSuccess) return err;
+        if (tile_is_interior(L, tile_base(L, t_lo), kBlochCtaTile)) continue;
+        const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
+        for (long long lo = t_lo; lo < t_hi; lo += warp_own) {
+            T.lo[T.n] = lo;
+            T.hi[T.n] = lo + warp_own < t_hi ? lo + warp_own : t_hi;
+            if (++T.n == kMaxEdgeTiles && (err = flush()) != cudaSuccess) return err;
+        }
     }
     if ((err = flush()) != cudaSuccess) return err;
-    const long long blocks = (tiles + kBlochWarpsPerBlock - 1) / kBlochWarpsPerBlock;
-    bloch_interior_kernel<<<(unsigned)blocks, kBlochWarpsPerBlock * 32, 0, st>>>(P);
+    bloch_interior_kernel<<<(unsigned)tiles, kBlochWarpsPerBlock * 32, 0, st>>>(P);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = cudaEventRecord(join, st_edge)) != cudaSuccess) return err;
     return cudaStreamWaitEvent(st, join, 0);

@@ -405,7 +405,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
         E = en;
         H = hn;
         const unsigned long long mask = L.step_mask[s];
-        const bool check = (L.check_mask >> s) & 1ull;
+        const bool check = L.check[s] != 0;
         if ((mask || check) && own) {
             if (check && !isfinite(E)) atomicMin(L.bad_step, (unsigned long long)n);
             for (int r = 0; r < L.n_rec; ++r) {

@@ -27,13 +27,20 @@ __device__ __forceinline__ double mad(double a, double b, double c) {
 #define MBG_BLOCH_C 8
 #endif
 constexpr int kBlochCellsPerLane = MBG_BLOCH_C;
-constexpr int kBlochTile = 32 * kBlochCellsPerLane;
-constexpr int kBlochWarpsPerBlock = 4;
+constexpr int kBlochTile = 32 * kBlochCellsPerLane;  // one warp
+#ifndef MBG_BLOCH_WARPS
+#define MBG_BLOCH_WARPS 8
+#endif
+constexpr int kBlochWarpsPerBlock = MBG_BLOCH_WARPS;
+// interior tiles are one CTA: the warps side by side exchange their seam cells
+// through shared memory, so the redundant halo is paid once per CTA tile
+constexpr int kBlochCtaTile = kBlochWarpsPerBlock * kBlochTile;
 // dense kernels: one thread per cell, one CTA per tile
 constexpr int kDenseTile = 128;
 
 #define MBG_DECLARE_LAUNCHERS(NS)                                                             \
     namespace NS {                                                                            \
+    int bloch_cta_tile();                                                                     \
     cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,          \
                              cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join);        \
     cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \

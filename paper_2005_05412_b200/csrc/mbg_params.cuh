@@ -63,7 +63,7 @@ struct Launch {
     double *rec_re[kMaxRecords];
     double *rec_im[kMaxRecords];
     unsigned long long step_mask[kMaxTileSteps];  // bit r: record r samples at fused step s
-    unsigned long long check_mask;                // bit s: non-finite scan at fused step s
+    unsigned char check[kMaxTileSteps];           // 1: non-finite scan at fused step s
     unsigned long long *bad_step;
     Regions rg;
 };
@@ -153,10 +153,12 @@ __host__ __device__ inline bool tile_is_interior(const Launch &L, long long base
     return true;
 }
 
+// result ranges [lo, hi) of the non-interior tiles, each processed by one warp
 constexpr int kMaxEdgeTiles = 128;
 struct EdgeTiles {
     int n;
-    long long tile[kMaxEdgeTiles];
+    long long lo[kMaxEdgeTiles];
+    long long hi[kMaxEdgeTiles];
 };
 
 }  // namespace mbg
