@@ -240,6 +240,28 @@ cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
     }
 }
 
+// Device memory comes from the device's default stream-ordered pool with an
+// unbounded release threshold: a new solver for the same workload (every e2e
+// run) reuses the previous one's blocks instead of paying cudaMalloc/cudaFree.
+void configure_pool(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        unsigned long long threshold = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+    }
+    done[device] = true;
+}
+
+cudaError_t dalloc(cudaStream_t st, double **p, size_t bytes) {
+    return cudaMallocAsync(reinterpret_cast<void **>(p), bytes, st);
+}
+
+void dfree(cudaStream_t st, void *p) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 bool window_ok(const mbg_grid *g) {
     return g->win_lo >= 0 && g->win_hi <= g->num_x && g->win_lo < g->win_hi && g->own_lo >= g->win_lo &&
            g->own_hi <= g->win_hi && g->own_lo < g->own_hi;
@@ -297,21 +319,23 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
         cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) != cudaSuccess)
         return cleanup(MBG_E_CUDA);
+    configure_pool(g.device);
     const size_t fb = sizeof(double) * (s->win_n + 1);
     const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
     for (int b = 0; b < 2; ++b) {
-        if (cudaMalloc(&s->e[b], fb) != cudaSuccess || cudaMalloc(&s->h[b], fb) != cudaSuccess ||
-            cudaMalloc(&s->s[b], sb) != cudaSuccess)
+        if (dalloc(s->stream, &s->e[b], fb) != cudaSuccess || dalloc(s->stream, &s->h[b], fb) != cudaSuccess ||
+            dalloc(s->stream, &s->s[b], sb) != cudaSuccess)
             return cleanup(MBG_E_CUDA);
-        cudaMemset(s->e[b], 0, fb);
-        cudaMemset(s->h[b], 0, fb);
-        cudaMemset(s->s[b], 0, sb);
+        cudaMemsetAsync(s->e[b], 0, fb, s->stream);
+        cudaMemsetAsync(s->h[b], 0, fb, s->stream);
+        cudaMemsetAsync(s->s[b], 0, sb, s->stream);
     }
-    if (cudaMalloc(&s->bad, sizeof(unsigned long long)) != cudaSuccess) return cleanup(MBG_E_CUDA);
-    cudaMemset(s->bad, 0xff, sizeof(unsigned long long));
+    if (dalloc(s->stream, reinterpret_cast<double **>(&s->bad), sizeof(unsigned long long)) != cudaSuccess)
+        return cleanup(MBG_E_CUDA);
+    cudaMemsetAsync(s->bad, 0xff, sizeof(unsigned long long), s->stream);
     cudaEventCreate(&s->ev0);
     cudaEventCreate(&s->ev1);
-    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(MBG_E_CUDA);
+    if (cudaStreamSynchronize(s->stream) != cudaSuccess) return cleanup(MBG_E_CUDA);
     *out = s;
     return MBG_OK;
 }
@@ -319,21 +343,23 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
 void mbg_destroy(mbg_solver *s) {
     if (!s) return;
     cudaSetDevice(s->g.device);
-    if (s->stream) cudaStreamSynchronize(s->stream);
+    cudaStream_t st = s->stream;
+    if (st) cudaStreamSynchronize(st);
     for (int b = 0; b < 2; ++b) {
-        cudaFree(s->e[b]);
-        cudaFree(s->h[b]);
-        cudaFree(s->s[b]);
+        dfree(st, s->e[b]);
+        dfree(st, s->h[b]);
+        dfree(st, s->s[b]);
     }
-    cudaFree(s->bad);
-    cudaFree(s->ck_e);
-    cudaFree(s->ck_h);
-    cudaFree(s->ck_s);
-    cudaFree(s->src_values);
+    dfree(st, s->bad);
+    dfree(st, s->ck_e);
+    dfree(st, s->ck_h);
+    dfree(st, s->ck_s);
+    dfree(st, s->src_values);
     for (auto &r : s->recs) {
-        cudaFree(r.re);
-        cudaFree(r.im);
+        dfree(st, r.re);
+        dfree(st, r.im);
     }
+    if (st) cudaStreamSynchronize(st);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->side) {
@@ -477,7 +503,7 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
     if (!s || n < 0) return MBG_E_ARG;
     if (n > kMaxSources) return fail(s, MBG_E_UNSUPPORTED, "too many sources (max 8)");
     cudaSetDevice(s->g.device);
-    cudaFree(s->src_values);
+    dfree(s->stream, s->src_values);
     s->src_values = nullptr;
     s->n_src = n;
     for (int q = 0; q < n; ++q) {
@@ -487,8 +513,9 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
     }
     if (n > 0) {
         const size_t bytes = sizeof(double) * (size_t)n * s->g.num_t;
-        CK(cudaMalloc(&s->src_values, bytes));
-        CK(cudaMemcpy(s->src_values, values, bytes, cudaMemcpyHostToDevice));
+        CK(dalloc(s->stream, &s->src_values, bytes));
+        CK(cudaMemcpyAsync(s->src_values, values, bytes, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
     }
     return MBG_OK;
 }
@@ -499,8 +526,8 @@ int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *c
     if (n > kMaxRecords) return fail(s, MBG_E_UNSUPPORTED, "too many records (max 64)");
     cudaSetDevice(s->g.device);
     for (auto &r : s->recs) {
-        cudaFree(r.re);
-        cudaFree(r.im);
+        dfree(s->stream, r.re);
+        dfree(s->stream, r.im);
     }
     s->recs.assign(n, Rec());
     for (int r = 0; r < n; ++r) {
@@ -517,11 +544,11 @@ int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *c
         R.cols = R.cell >= 0 ? 1 : s->g.own_hi - s->g.own_lo;
         R.col0 = R.cell >= 0 ? R.cell : s->g.own_lo;
         const size_t bytes = sizeof(double) * (size_t)R.rows * R.cols;
-        CK(cudaMalloc(&R.re, bytes));
-        CK(cudaMemset(R.re, 0, bytes));
+        CK(dalloc(s->stream, &R.re, bytes));
+        CK(cudaMemsetAsync(R.re, 0, bytes, s->stream));
         if (R.q == MBG_Q_D && R.i != R.j) {
-            CK(cudaMalloc(&R.im, bytes));
-            CK(cudaMemset(R.im, 0, bytes));
+            CK(dalloc(s->stream, &R.im, bytes));
+            CK(cudaMemsetAsync(R.im, 0, bytes, s->stream));
         }
     }
     return MBG_OK;
@@ -545,11 +572,11 @@ int mbg_upload_density(mbg_solver *s, const double *words) {
     if (s->words == 0) return MBG_OK;
     cudaSetDevice(s->g.device);
     double *w = nullptr;
-    CK(cudaMalloc(&w, sizeof(double) * s->words));
-    CK(cudaMemcpy(w, words, sizeof(double) * s->words, cudaMemcpyHostToDevice));
+    CK(dalloc(s->stream, &w, sizeof(double) * s->words));
+    CK(cudaMemcpyAsync(w, words, sizeof(double) * s->words, cudaMemcpyHostToDevice, s->stream));
     CK(launch_broadcast_state(s->s[s->cur], s->plane, s->win_n, s->words, w, s->rg, s->g.win_lo, s->stream));
+    dfree(s->stream, w);
     CK(cudaStreamSynchronize(s->stream));
-    cudaFree(w);
     return MBG_OK;
 }
 
@@ -695,9 +722,9 @@ int mbg_checkpoint_save(mbg_solver *s) {
     const size_t fb = sizeof(double) * (s->win_n + 1);
     const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
     if (!s->ck_e) {
-        CK(cudaMalloc(&s->ck_e, fb));
-        CK(cudaMalloc(&s->ck_h, fb));
-        CK(cudaMalloc(&s->ck_s, sb));
+        CK(dalloc(s->stream, &s->ck_e, fb));
+        CK(dalloc(s->stream, &s->ck_h, fb));
+        CK(dalloc(s->stream, &s->ck_s, sb));
     }
     CK(cudaMemcpyAsync(s->ck_e, s->e[s->cur], fb, cudaMemcpyDeviceToDevice, s->stream));
     CK(cudaMemcpyAsync(s->ck_h, s->h[s->cur], fb, cudaMemcpyDeviceToDevice, s->stream));
