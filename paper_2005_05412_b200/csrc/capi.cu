@@ -86,13 +86,13 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
 
 int default_tile_steps(int levels, int stepper) {
     if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 64;
-    if (levels <= 3) return 8;
+    if (levels <= 3) return 16;
     return 4;
 }
 
 int tile_width(const mbg_solver *s) {
     if (s->bloch || s->g.levels == 0) return s->g.exact ? exact::bloch_cta_tile() : fast::bloch_cta_tile();
-    return s->g.levels >= 7 ? 64 : kDenseTile;
+    return dense_tile_width(s->g.levels, s->g.stepper == MBG_STEPPER_RK4);
 }
 
 Launch base_launch(const mbg_solver *s) {

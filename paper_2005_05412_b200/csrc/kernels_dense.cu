@@ -20,8 +20,6 @@ MBG_DECL(7)
 MBG_DECL(8)
 }  // namespace dense
 
-int dense_tile_width(int n) { return n >= 7 ? 64 : kDenseTile; }
-
 cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st) {
     switch (n) {
         case 3: return dense::launch_split_3(params, tiles, st);

@@ -1,6 +1,6 @@
 // Fused time-step kernels for N-level media, N = 2 (RK4) and 3..8.
 //
-// One thread per cell, one CTA per tile of kDenseTile consecutive cells, k
+// One thread per cell, one CTA per tile of dense_tile_width consecutive cells, k
 // time steps per launch (temporal tiling with redundant halos, as in the
 // two-level kernel).  The per-cell density matrix never leaves the SM while
 // the launch runs: it is Hermitian-packed (N real diagonal words, then re/im
@@ -31,7 +31,7 @@ namespace dense {
 
 // tile width (threads = cells per CTA); the largest state layouts use 64
 template <int N, bool RK4>
-constexpr int tile_width() { return N >= 7 ? 64 : kDenseTile; }
+constexpr int tile_width() { return dense_tile_width(N, RK4); }
 
 // packed word index of upper pair (i < j), row-major
 __host__ __device__ constexpr int pair_index(int n, int i, int j) { return i * n - i * (i + 1) / 2 + (j - i - 1); }
@@ -469,7 +469,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
 }
 
 template <int N, bool RK4, class Q>
-__global__ void __launch_bounds__(Layout<N, RK4>::TW) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
+__global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
     using Lay = Layout<N, RK4>;
     extern __shared__ double sm[];
     const Launch &L = P.L;

@@ -36,7 +36,10 @@ constexpr int kBlochWarpsPerBlock = MBG_BLOCH_WARPS;
 // through shared memory, so the redundant halo is paid once per CTA tile
 constexpr int kBlochCtaTile = kBlochWarpsPerBlock * kBlochTile;
 // dense kernels: one thread per cell, one CTA per tile
-constexpr int kDenseTile = 128;
+// dense kernels: one thread per cell, one CTA per tile; small N use wide tiles
+// (less redundant halo) at 128 registers, large N narrow tiles (state in smem)
+__host__ __device__ constexpr int dense_tile_width(int n, bool rk4) { return n <= 3 ? 256 : (n <= 6 ? 128 : 64); }
+__host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <= 3 ? 2 : 1; }
 
 #define MBG_DECLARE_LAUNCHERS(NS)                                                             \
     namespace NS {                                                                            \

@@ -131,7 +131,8 @@ struct DenseParams {
 // shared helpers (host + device)
 __host__ __device__ inline int region_of(const long long *start, int n, long long m) {
     int r = 0;
-    for (int q = 1; q < kMaxRegions; ++q) r += (q < n && m >= start[q]) ? 1 : 0;
+#pragma unroll 1
+    for (int q = 1; q < n; ++q) r += m >= start[q] ? 1 : 0;
     return r;
 }
 
