@@ -18,8 +18,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 
-CELL_STEPS = {  # cell-steps per profiled launch (tools/prof_step.py defaults)
-    "cfg2": (1 << 22) * 24, "cfg3": (1 << 23) * 8, "cfg4": (1 << 24) * 4, "cfg5": (1 << 22) * 4,
+CELL_STEPS = {  # cell-steps per profiled launch (tools/prof_step.py defaults: k = 64 / 16 / 4)
+    "cfg2": (1 << 22) * 64, "cfg3": (1 << 23) * 16, "cfg4": (1 << 24) * 4, "cfg5": (1 << 22) * 4,
 }
 
 
