@@ -23,6 +23,7 @@
  *   mbg_advance           the step loop (phase1/2 + after_*)       solver_fdtd.py:457-463
  *   mbg_poll_nonfinite    SolverError("non-finite ... at step n")  solver_fdtd.py:386-388
  *   mbg_download_record   plan.to_result                           solver_fdtd.py:164-172
+ *   mbg_invariants        DensityKernel.invariant_stats            _kernels.py:394-401, 541-546
  *   mbg_pack_halo/unpack  (new) slab ghost exchange, no reference analogue
  *
  * Conventions: every function returns 0 on success or a negative MBG_E_*
@@ -124,6 +125,10 @@ int mbg_sample(mbg_solver *s, int64_t step);
 int mbg_advance(mbg_solver *s, int64_t first_step, int64_t n_steps); /* async */
 int mbg_synchronize(mbg_solver *s);
 int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step); /* syncs; -1 when all finite */
+/* invariant monitor of the current state (_kernels.py:394-401, solver_fdtd.py:428-440):
+ * out[0] max |trace - 1|, out[1] max Hermiticity deviation, out[2] min eigenvalue
+ * over the owned quantum cells (+inf when there are none) */
+int mbg_invariants(mbg_solver *s, double *out);
 int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols);
 int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im);
 

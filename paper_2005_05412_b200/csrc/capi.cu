@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -676,6 +677,32 @@ int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step) {
     CK(cudaMemcpyAsync(&v, s->bad, sizeof(v), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     *bad_step = v == ~0ull ? -1 : (int64_t)v;
+    return MBG_OK;
+}
+
+static double from_key(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    std::memcpy(&v, &b, sizeof(v));
+    return v;
+}
+
+int mbg_invariants(mbg_solver *s, double *out) {
+    if (!s || !out) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    unsigned long long init[3] = {0, 0, ~0ull}, *d = nullptr;
+    init[0] = init[1] = 0x8000000000000000ull;  // key of +0.0
+    CK(dalloc(s->stream, reinterpret_cast<double **>(&d), sizeof(init)));
+    CK(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
+    const Launch L = base_launch(s);
+    if (s->words > 0) CK(launch_invariants(L, s->g.levels, s->bloch ? 1 : 0, d, s->stream));
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+    dfree(s->stream, d);
+    CK(cudaStreamSynchronize(s->stream));
+    out[0] = from_key(h[0]);
+    out[1] = 0.0;  // Hermitian-packed state: exactly Hermitian
+    out[2] = h[2] == ~0ull ? INFINITY : from_key(h[2]);
     return MBG_OK;
 }
 

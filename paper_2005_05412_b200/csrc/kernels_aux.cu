@@ -103,6 +103,90 @@ __global__ void __launch_bounds__(256) fp64_fma_kernel(double *out, int iters, d
     if (sum == 12345.678) out[0] = sum;  // keep the chains alive
 }
 
+// ---- invariant monitor (solver_fdtd.py:428-440, _kernels.py:394-401, 541-546) ----
+// order-preserving uint64 key of a double (for atomicMin / atomicMax)
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    const unsigned long long b = __double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// smallest eigenvalue of a complex Hermitian n x n matrix (n <= 8) through the
+// real symmetric 2n x 2n embedding [[Re, -Im], [Im, Re]] and cyclic Jacobi
+__device__ double min_eigenvalue(const double *re, const double *im, int n) {
+    double a[16][16];
+    const int m = 2 * n;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            a[i][j] = a[i + n][j + n] = re[i * n + j];
+            a[i + n][j] = im[i * n + j];
+            a[i][j + n] = -im[i * n + j];
+        }
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, scale = 0.0;
+        for (int p = 0; p < m; ++p) {
+            scale += a[p][p] * a[p][p];
+            for (int q = p + 1; q < m; ++q) off += a[p][q] * a[p][q];
+        }
+        if (off <= 1e-32 * (scale + 1e-300)) break;
+        for (int p = 0; p < m; ++p)
+            for (int q = p + 1; q < m; ++q) {
+                const double apq = a[p][q];
+                if (apq == 0.0) continue;
+                const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+                for (int k = 0; k < m; ++k) {
+                    const double akp = a[k][p], akq = a[k][q];
+                    a[k][p] = c * akp - sn * akq;
+                    a[k][q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < m; ++k) {
+                    const double apk = a[p][k], aqk = a[q][k];
+                    a[p][k] = c * apk - sn * aqk;
+                    a[q][k] = sn * apk + c * aqk;
+                }
+            }
+    }
+    double mn = a[0][0];
+    for (int p = 1; p < m; ++p) mn = fmin(mn, a[p][p]);
+    return mn;
+}
+
+__global__ void invariants_kernel(const Launch L, int levels, int bloch, unsigned long long *out) {
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L.win_n) return;
+    const long long c = L.win_lo + l;
+    if (c < L.own_lo || c >= L.own_hi) return;
+    if (L.rg.qm[region_of(L.rg.e_start, L.rg.n, c)] < 0) return;
+    const double *s = L.s_in + l;
+    const long long P = L.plane;
+    double trace_dev = 0.0, min_eig;
+    if (bloch) {
+        // eigenvalues (1 +- |v|)/2; trace and Hermiticity exact in this form
+        const double x = s[0], y = s[P], z = s[2 * P];
+        min_eig = 0.5 * (1.0 - sqrt(x * x + y * y + z * z));
+    } else {
+        const int n = levels;
+        double re[64], im[64], tr = 0.0;
+        for (int i = 0; i < n; ++i) {
+            re[i * n + i] = s[i * P];
+            im[i * n + i] = 0.0;
+            tr += re[i * n + i];
+        }
+        for (int i = 0; i < n; ++i)
+            for (int j = i + 1; j < n; ++j) {
+                const int w = n + 2 * pair_index(n, i, j);
+                re[i * n + j] = re[j * n + i] = s[w * P];
+                im[i * n + j] = s[(w + 1) * P];
+                im[j * n + i] = -s[(w + 1) * P];
+            }
+        trace_dev = fabs(tr - 1.0);
+        min_eig = min_eigenvalue(re, im, n);
+    }
+    atomicMax(&out[0], dkey(trace_dev));
+    atomicMin(&out[2], dkey(min_eig));
+}
+
 unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 }  // namespace
@@ -135,6 +219,12 @@ cudaError_t measure_fp64_peak(double *ms, double *flops) {
     *ms = best;
     *flops = 2.0 * 16.0 * iters * (double)blocks * threads;
     return err;
+}
+
+cudaError_t launch_invariants(const Launch &L, int levels, int bloch, unsigned long long *out, cudaStream_t st) {
+    if (L.win_n <= 0) return cudaSuccess;
+    invariants_kernel<<<blocks_for(L.win_n, 128), 128, 0, st>>>(L, levels, bloch, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sample(const Launch &L, const void *, int levels, int bloch, long long step, cudaStream_t st) {

@@ -62,6 +62,10 @@ cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, 
 cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long plane, int words,
                         long long l0, long long count, double *buf, cudaStream_t st);
 
+// invariant monitor: out[0] max |trace - 1|, out[1] max Hermiticity deviation
+// (0: packed storage), out[2] min eigenvalue, as order-preserving uint64 keys
+cudaError_t launch_invariants(const Launch &L, int levels, int bloch, unsigned long long *out, cudaStream_t st);
+
 // FP64 roofline denominator: best-of-5 DFMA throughput (ms of the best launch, flops per launch)
 cudaError_t measure_fp64_peak(double *ms, double *flops);
 

@@ -65,6 +65,7 @@ SIGNATURES = {
     "mbg_advance": (C.c_int, [_h, C.c_int64, C.c_int64]),
     "mbg_synchronize": (C.c_int, [_h]),
     "mbg_poll_nonfinite": (C.c_int, [_h, _i64p]),
+    "mbg_invariants": (C.c_int, [_h, _dp]),
     "mbg_record_shape": (C.c_int, [_h, C.c_int32, _i64p, _i64p]),
     "mbg_download_record": (C.c_int, [_h, C.c_int32, _dp, _dp]),
     "mbg_halo_words": (C.c_int, [_h, _i32p]),

@@ -23,8 +23,8 @@ import sys
 import numpy as np
 
 from . import native
-from .errors import NativeError, SolverError
-from .plan import NONFINITE_CHECK_EVERY, build_plan, resolve_threads, unpack_density
+from .errors import SolverError
+from .plan import build_plan, resolve_threads
 from .setup_model import Result, register_solver
 
 SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
@@ -215,26 +215,15 @@ class GpuFdtdSolver:
         return min((p.every for p in self.plan.plans), default=256)
 
     def _update_invariants(self, h):
-        plan = self.plan
-        nx = self.grid.num_x
-        words = np.zeros((plan.state_words, nx))
-        h.call("mbg_download_state", native.ptr(words))
-        qcells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in plan.groups]) if plan.groups else np.zeros(0, int)
-        rho = unpack_density(words[:, qcells], plan.levels, plan.stepper)
+        """Device reduction over every quantum cell (mbg_invariants)."""
+        out = np.zeros(3)
+        h.call("mbg_invariants", native.ptr(out))
         rep = self.invariant_report
         if rep is None:
             rep = self.invariant_report = {"max_trace_dev": 0.0, "max_herm_dev": 0.0, "min_eigenvalue": math.inf}
-        if plan.levels == 2 and plan.stepper == "splitting":
-            norms = np.sqrt(np.sum(words[:, qcells] ** 2, axis=0))
-            tr, he, me = 0.0, 0.0, 0.5 * (1.0 - float(np.max(norms)))
-        else:
-            tr = float(np.max(np.abs(np.trace(rho, axis1=1, axis2=2) - 1.0)))
-            adj = rho.conj().transpose(0, 2, 1)
-            he = float(np.max(np.abs(rho - adj)))
-            me = float(np.min(np.linalg.eigvalsh(0.5 * (rho + adj))))
-        rep["max_trace_dev"] = max(rep["max_trace_dev"], tr)
-        rep["max_herm_dev"] = max(rep["max_herm_dev"], he)
-        rep["min_eigenvalue"] = min(rep["min_eigenvalue"], me)
+        rep["max_trace_dev"] = max(rep["max_trace_dev"], float(out[0]))
+        rep["max_herm_dev"] = max(rep["max_herm_dev"], float(out[1]))
+        rep["min_eigenvalue"] = min(rep["min_eigenvalue"], float(out[2]))
 
 
 def _rk4_factory(device, scenario, **kw):

@@ -149,3 +149,44 @@ def test_results_are_independent_arrays():
     r = s.run()[0]
     r.data[:] = 1.0  # caller owns the buffers
     assert s.results[0].data is r.data
+
+
+@pytest.mark.parametrize("case", ["rand3_split", "rand6_split", "rand8_split", "rand4_rk4", "multi_material"])
+def test_device_invariant_monitor_matches_numpy(case):
+    """mbg_invariants (device reduction + Jacobi eigenvalues) vs numpy eigvalsh
+    of the downloaded state (the reference's invariant_stats, _kernels.py:394-401)."""
+    from paper_2005_05412_b200 import native
+    from paper_2005_05412_b200.plan import unpack_density
+
+    dev, sce, stepper = build_case(case)
+    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    h = s.open_handle()
+    s.upload_initial_state(h)
+    h.call("mbg_sample", 0)
+    h.call("mbg_advance", 1, min(200, s.grid.num_t - 1))
+    out = np.zeros(3)
+    h.call("mbg_invariants", native.ptr(out))
+    words = np.zeros((s.plan.state_words, s.grid.num_x))
+    h.call("mbg_download_state", native.ptr(words))
+    h.close()
+    cells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in s.plan.groups])
+    rho = unpack_density(words[:, cells], s.plan.levels, s.plan.stepper)
+    if s.plan.levels == 2 and stepper == "splitting":
+        want_eig = 0.5 * (1.0 - np.max(np.sqrt(np.sum(words[:, cells] ** 2, axis=0))))
+        want_tr = 0.0
+    else:
+        want_eig = np.min(np.linalg.eigvalsh(rho))
+        want_tr = np.max(np.abs(np.trace(rho, axis1=1, axis2=2).real - 1.0))
+    assert out[0] == pytest.approx(want_tr, abs=1e-15)
+    assert out[1] == 0.0
+    assert out[2] == pytest.approx(want_eig, abs=1e-13)
+
+
+def test_sit_run_invariants_like_the_acceptance_suite():
+    """pkg/tests/test_acceptance.py:74-116: trace < 1e-9, Hermiticity < 1e-12,
+    eigenvalues > -1e-9 over the full transparency run (monitor at record cadence)."""
+    dev, sce, _ = build_case("sit_hard_whole")
+    s = mb.create_solver("gpu-fdtd-reg-cayley", dev, sce, monitor_invariants=True)
+    s.run()
+    rep = s.invariant_report
+    assert rep["max_trace_dev"] < 1e-9 and rep["max_herm_dev"] < 1e-12 and rep["min_eigenvalue"] > -1e-9
