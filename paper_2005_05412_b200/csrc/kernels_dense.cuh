@@ -235,36 +235,95 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
         }
 }
 
+// Same derivative for N >= 4 with H = h0 - E mu formed row by row on the fly
+// (a full H would hold 2N^2 doubles in registers).  The empty asm on the
+// field value keeps the compiler from caching H rows across (i, j) pairs.
+template <int N, class VS, class VD>
+__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VS &src, VD &dst) {
+    constexpr double kInvHbar = 1.0 / 1.054571817e-34;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        double ei = e;
+        asm volatile("" : "+d"(ei));
+        double ar[N], ai[N];  // row i of H
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            ar[k] = mad(-ei, q.mu_re[i * N + k], q.h0_re[i * N + k]);
+            ai[k] = mad(-ei, q.mu_im[i * N + k], q.h0_im[i * N + k]);
+        }
+#pragma unroll
+        for (int j = i; j < N; ++j) {
+            double ej = ei;
+            asm volatile("" : "+d"(ej));
+            double cr = 0.0, ci = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                double sr, si, tr, ti;
+                herm<N>(src, k, j, sr, si);
+                herm<N>(src, i, k, tr, ti);
+                // H_kj = conj(H_jk) (H is exactly Hermitian)
+                const double br = mad(-ej, q.mu_re[j * N + k], q.h0_re[j * N + k]);
+                const double bi = -mad(-ej, q.mu_im[j * N + k], q.h0_im[j * N + k]);
+                cr += mad(ar[k], sr, -(ai[k] * si)) - mad(tr, br, -(ti * bi));
+                ci += mad(ar[k], si, ai[k] * sr) - mad(tr, bi, ti * br);
+            }
+            double dr = ci * kInvHbar, di = -cr * kInvHbar;
+            if (i == j) {
+                double acc = q.popm[i * N] * src[0];
+#pragma unroll
+                for (int m = 1; m < N; ++m) acc = mad(q.popm[i * N + m], src[m], acc);
+                dst[i] = dr + acc;
+            } else {
+                const double g = q.deph[i * N + j];
+                dst[wre(N, i, j)] = mad(-g, src[wre(N, i, j)], dr);
+                dst[wim(N, i, j)] = mad(-g, src[wim(N, i, j)], di);
+            }
+        }
+    }
+}
+
+template <int N, class VS, class VD>
+__device__ __forceinline__ void rhs(const Rk4Qm<N> &q, double e, const double *hr, const double *hi, VS &src,
+                                    VD &dst) {
+    if constexpr (N >= 4)
+        master_rhs_rows<N>(q, e, src, dst);
+    else
+        master_rhs<N>(q, hr, hi, src, dst);
+}
+
 template <int N, class VA, class VB>
 __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, VB &S, VB &K, VB &Acc) {
     constexpr int NW = N * N;
-    double hr[N * N], hi[N * N];
+    constexpr int NH = N >= 4 ? 1 : N * N;
+    double hr[NH], hi[NH];
+    if constexpr (N < 4) {
 #pragma unroll
-    for (int i = 0; i < N * N; ++i) {
-        hr[i] = mad(-e, q.mu_re[i], q.h0_re[i]);
-        hi[i] = mad(-e, q.mu_im[i], q.h0_im[i]);
+        for (int i = 0; i < N * N; ++i) {
+            hr[i] = mad(-e, q.mu_re[i], q.h0_re[i]);
+            hi[i] = mad(-e, q.mu_im[i], q.h0_im[i]);
+        }
     }
     const double dt = q.dt;
     // k1
-    master_rhs<N>(q, hr, hi, A, K);
+    rhs<N>(q, e, hr, hi, A, K);
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
         Acc[w] = K[w];
         S[w] = mad(0.5 * dt, K[w], A[w]);
     }
-    master_rhs<N>(q, hr, hi, S, K);  // k2
+    rhs<N>(q, e, hr, hi, S, K);  // k2
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
         Acc[w] = mad(2.0, K[w], Acc[w]);
         S[w] = mad(0.5 * dt, K[w], A[w]);
     }
-    master_rhs<N>(q, hr, hi, S, K);  // k3
+    rhs<N>(q, e, hr, hi, S, K);  // k3
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
         Acc[w] = mad(2.0, K[w], Acc[w]);
         S[w] = mad(dt, K[w], A[w]);
     }
-    master_rhs<N>(q, hr, hi, S, K);  // k4
+    rhs<N>(q, e, hr, hi, S, K);  // k4
     const double sixth = dt / 6.0;
     double acc_p = 0.0;
 #pragma unroll

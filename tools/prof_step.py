@@ -21,6 +21,7 @@ ap.add_argument("config", nargs="?", default="cfg2")
 ap.add_argument("--steps", type=int, default=0)
 ap.add_argument("--tile-steps", type=int, default=None)
 ap.add_argument("--exact", action="store_true")
+ap.add_argument("--stepper", default="splitting")
 ap.add_argument("--nx", type=int, default=0)
 ap.add_argument("--no-warm", action="store_true", help="single pass (for ncu)")
 a = ap.parse_args()
@@ -30,7 +31,7 @@ if a.config == "cfg5":
     dev, sce = configs.cfg5(mb, steps=total)
 else:
     dev, sce = getattr(configs, a.config)(mb, **kw, **({"steps": total} if a.config != "cfg1" else {}))
-sol = mb.GpuFdtdSolver(dev, sce, tile_steps=a.tile_steps, exact=a.exact)
+sol = mb.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact)
 h = sol.open_handle()
 sol.upload_initial_state(h)
 k = C.c_int32(0)
@@ -45,6 +46,6 @@ h.call("mbg_event_begin")
 h.call("mbg_advance", 1, steps)
 ms = C.c_float(0)
 h.call("mbg_event_end", C.byref(ms))
-print(f"{a.config}: nx={sol.grid.num_x} k={k.value} steps={steps} device {ms.value:.3f} ms "
+print(f"{a.config}/{a.stepper}: nx={sol.grid.num_x} k={k.value} steps={steps} device {ms.value:.3f} ms "
       f"-> {sol.grid.num_x * steps / (ms.value * 1e-3):.3e} cell-updates/s")
 h.close()
