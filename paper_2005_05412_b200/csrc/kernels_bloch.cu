@@ -135,19 +135,25 @@ __device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, do
     }
 }
 
+// General tile (domain/window ends, region interfaces, source cells): cyclic
+// layout (slot i*32 + lane), every per-slot property decided once per launch
+// and kept as bit masks; UNI tiles (one E and one H region) take scalar
+// coefficients and one material, the rare interface tiles look them up per slot.
 template <bool UNI>
 __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
                                          int lane) {
     const Launch &L = P.L;
     const long long nx = L.num_x;
     double E[C], H[C], X[C], Y[C], Z[C];
-    int qi[C];  // quantum material of the slot, -1 classical / outside
-    int re_[C], rh_[C];
-    // uniform tiles: one E region and one H region -> scalar coefficients
+    int qi[C];  // quantum material of the slot, -1 classical / outside (used when !UNI)
+    double ca[C], cbg[C], cbdx[C], cch[C];
+    unsigned hmask = 0, emask = 0, qmask = 0, rmask = 0, smask = 0;
     const long long c_first = base < 0 ? 0 : base;
     const int re_u = region_of(L.rg.e_start, L.rg.n, c_first);
     const int rh_u = region_of(L.rg.h_start, L.rg.n, c_first < 1 ? 1 : c_first);
-
+    const int qu = L.rg.qm[re_u];
+    const bool right_edge = L.has_boundary && base <= nx - 1 && nx - 1 < base + W;
+    const bool left_edge = L.has_boundary && base == 0;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
         const long long c = base + i * 32 + lane;
@@ -155,9 +161,20 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         const bool in_e = (l >= 0 && l < L.win_n);
         E[i] = in_e ? L.e_in[l] : 0.0;
         H[i] = (l >= 0 && l <= L.win_n) ? L.h_in[l] : 0.0;
-        re_[i] = UNI ? re_u : region_of(L.rg.e_start, L.rg.n, c);
-        rh_[i] = UNI ? rh_u : region_of(L.rg.h_start, L.rg.n, c);
-        qi[i] = (in_e && c >= 0 && c < nx) ? L.rg.qm[re_[i]] : -1;
+        const int re = UNI ? re_u : region_of(L.rg.e_start, L.rg.n, c);
+        const int rh = UNI ? rh_u : region_of(L.rg.h_start, L.rg.n, c);
+        if (!UNI) {
+            ca[i] = L.rg.a[re];
+            cbg[i] = L.rg.bg[re];
+            cbdx[i] = L.rg.bdx[re];
+            cch[i] = L.rg.ch[rh];
+        }
+        qi[i] = (in_e && c >= 0 && c < nx) ? L.rg.qm[re] : -1;
+        hmask |= (c >= 1 && c <= nx - 1) ? 1u << i : 0u;
+        emask |= (nx > 1 && c >= 0 && c < nx) ? 1u << i : 0u;
+        qmask |= qi[i] >= 0 ? 1u << i : 0u;
+        rmask |= (right_edge && c == nx - 1) ? 1u << i : 0u;
+        for (int q = 0; q < L.n_src; ++q) smask |= c == L.src_cell[q] ? 1u << i : 0u;
         if (qi[i] >= 0) {
             X[i] = L.s_in[l];
             Y[i] = L.s_in[L.plane + l];
@@ -166,8 +183,8 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
             X[i] = Y[i] = Z[i] = 0.0;
         }
     }
-    const bool left_edge = L.has_boundary && base == 0;
-    const bool right_edge = L.has_boundary && base <= nx - 1 && nx - 1 < base + W;
+    const double ua = L.rg.a[re_u], ubg = L.rg.bg[re_u], ubdx = L.rg.bdx[re_u], uch = L.rg.ch[rh_u];
+    const int qs = qu < 0 ? 0 : qu;
 
     for (int s = 0; s < L.k; ++s) {
         const long long n = L.n0 + s;
@@ -183,19 +200,19 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         double Hn[C], El[C];
 #pragma unroll
         for (int i = 0; i < C; ++i) {
-            const long long c = base + i * 32 + lane;
             El[i] = (lane == 0) ? t[i > 0 ? i - 1 : 0] : t[i];
-            const double ch = UNI ? L.rg.ch[rh_u] : L.rg.ch[rh_[i]];
-            Hn[i] = (c >= 1 && c <= nx - 1) ? mad(ch, E[i] - El[i], H[i]) : H[i];
+            Hn[i] = ((hmask >> i) & 1u) ? mad(UNI ? uch : cch[i], E[i] - El[i], H[i]) : H[i];
         }
         // ---- density step with E^{n-1} and polarisation rate -----------------
         double p[C];
 #pragma unroll
         for (int i = 0; i < C; ++i) {
             p[i] = 0.0;
-            if (qi[i] >= 0)
-                p[i] = P.real_dipole ? MBG_BLOCH_REAL(P.qm[qi[i]], P.rq[qi[i]], E[i], X[i], Y[i], Z[i])
-                                     : bloch_cell(P.qm[qi[i]], E[i], X[i], Y[i], Z[i]);
+            if ((qmask >> i) & 1u) {
+                const int qq = UNI ? qs : qi[i];
+                p[i] = P.real_dipole ? MBG_BLOCH_REAL(P.qm[qq], P.rq[qq], E[i], X[i], Y[i], Z[i])
+                                     : bloch_cell(P.qm[qq], E[i], X[i], Y[i], Z[i]);
+            }
         }
         // ---- E update: needs H[m+1] (right neighbour) --------------------------
         double u[C];
@@ -203,27 +220,30 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         for (int i = 0; i < C; ++i) u[i] = __shfl_sync(kFull, Hn[i], (lane + 1) & 31);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
-            const long long c = base + i * 32 + lane;
             const double hr = (lane == 31) ? u[i < C - 1 ? i + 1 : i] : u[i];
-            const int r = UNI ? re_u : re_[i];
-            const double a = L.rg.a[r], bg = L.rg.bg[r], bdx = L.rg.bdx[r];
-            double en = (nx > 1 && c >= 0 && c < nx) ? mad(bdx, hr - Hn[i], mad(a, E[i], -(bg * p[i]))) : E[i];
+            double en = E[i];
+            if ((emask >> i) & 1u)
+                en = UNI ? mad(ubdx, hr - Hn[i], mad(ua, E[i], -(ubg * p[i])))
+                         : mad(cbdx[i], hr - Hn[i], mad(ca[i], E[i], -(cbg[i] * p[i])));
             if (left_edge && i == 0 && lane == 0) {
                 // solver_fdtd.py:372-374
                 const double e_at = mad(L.l_c, e_right0, L.l_omc * E[0]);
                 const double h_at = 0.5 * (h_right0 + hr);
                 en = L.l_hw * mad(L.l_z, h_at, e_at);
             }
-            if (right_edge && c == nx - 1) {
+            if ((rmask >> i) & 1u) {
                 // solver_fdtd.py:375-377 (E[Nx-2] old is the left neighbour)
                 const double e_at = mad(L.r_c, El[i], L.r_omc * E[i]);
                 const double h_at = 0.5 * (H[i] + Hn[i]);
                 en = L.r_hw * mad(-L.r_z, h_at, e_at);
             }
-            for (int q = 0; q < L.n_src; ++q) {
-                if (c == L.src_cell[q]) {
-                    const double v = L.src_values[n * L.n_src + q];
-                    en = L.src_hard[q] ? v : en + v;
+            if ((smask >> i) & 1u) {
+                const long long c = base + i * 32 + lane;
+                for (int q = 0; q < L.n_src; ++q) {
+                    if (c == L.src_cell[q]) {
+                        const double v = L.src_values[n * L.n_src + q];
+                        en = L.src_hard[q] ? v : en + v;
+                    }
                 }
             }
             E[i] = en;
