@@ -352,7 +352,11 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     world, rank, local = dist_env()
-    if world > 1 and args.gpus != world:
+    if args.gpus != world:
+        # one process per GPU: the driver launches --gpus N under torchrun
+        if world == 1 and args.gpus > 1:
+            print(f"bench.py: --gpus {args.gpus} needs torchrun --nproc-per-node {args.gpus}; "
+                  "running the 1-GPU workload", file=sys.stderr)
         args.gpus = world
     if args.impl == "reference":
         return run_reference(args, world, rank)

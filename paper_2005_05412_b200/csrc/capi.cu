@@ -615,16 +615,32 @@ int mbg_sample(mbg_solver *s, int64_t step) {
     if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
     cudaSetDevice(s->g.device);
     const Launch L = base_launch(s);
-    CK(launch_sample(L, nullptr, s->g.levels, s->bloch ? 1 : 0, step, s->stream));
+    CK(launch_sample(L, s->g.levels, s->bloch ? 1 : 0, step, s->stream));
+    return MBG_OK;
+}
+
+// every quantum material a region refers to must have constants of the
+// solver's stepper kind (otherwise a kernel would read an empty slot)
+static int check_ready(mbg_solver *s) {
+    if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
+    const int limit = (s->bloch || s->g.levels == 0) ? kMaxQm : kMaxDenseQm;
+    if ((int)s->qm.size() > limit) return fail(s, MBG_E_UNSUPPORTED, "too many quantum materials for this kernel");
+    for (int r = 0; r < s->rg.n; ++r) {
+        const int q = s->rg.qm[r];
+        if (q < 0) continue;
+        if (s->g.levels == 0) return fail(s, MBG_E_STATE, "region has a quantum material but levels == 0");
+        if (q >= (int)s->qm.size() || s->qm[q].n != s->g.levels)
+            return fail(s, MBG_E_STATE, "quantum constants not set for a material the regions use");
+        const QmHost &h = s->qm[q];
+        const bool ok = s->bloch ? (!h.dense && !h.rk4) : (s->g.stepper == MBG_STEPPER_RK4 ? h.rk4 : h.dense);
+        if (!ok) return fail(s, MBG_E_STATE, "quantum constants do not match the stepper");
+    }
     return MBG_OK;
 }
 
 int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     if (!s) return MBG_E_ARG;
-    if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
-    if ((s->bloch || s->g.levels >= 3 || s->g.stepper == MBG_STEPPER_RK4) && s->g.levels > 0 &&
-        s->qm.empty())
-        return fail(s, MBG_E_STATE, "quantum constants not set");
+    if (int rc = check_ready(s)) return rc;
     if (first < 1 || n_steps < 0 || first + n_steps > s->g.num_t)
         return fail(s, MBG_E_ARG, "step range outside 1 .. num_t-1");
     const long long ghost_l = s->g.own_lo - s->g.win_lo, ghost_r = s->g.win_hi - s->g.own_hi;

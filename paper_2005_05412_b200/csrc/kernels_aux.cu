@@ -227,7 +227,7 @@ cudaError_t launch_invariants(const Launch &L, int levels, int bloch, unsigned l
     return cudaGetLastError();
 }
 
-cudaError_t launch_sample(const Launch &L, const void *, int levels, int bloch, long long step, cudaStream_t st) {
+cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, cudaStream_t st) {
     if (L.win_n <= 0) return cudaSuccess;
     sample_kernel<<<blocks_for(L.win_n, 256), 256, 0, st>>>(L, levels, bloch, step);
     return cudaGetLastError();

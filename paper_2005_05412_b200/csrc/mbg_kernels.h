@@ -54,8 +54,7 @@ MBG_DECLARE_LAUNCHERS(fast)
 MBG_DECLARE_LAUNCHERS(exact)
 
 // auxiliary kernels (variant independent)
-cudaError_t launch_sample(const Launch &L, const void *qm_words, int levels, int bloch,
-                          long long step, cudaStream_t st);
+cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, cudaStream_t st);
 cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, int words,
                                    const double *words_dev, const Regions &rg, long long win_lo,
                                    cudaStream_t st);

@@ -113,7 +113,7 @@ class GpuFdtdSolver:
         return h
 
     def _upload_qm(self, h, q, qc):
-        # keep temporaries alive through the call
+        # the numpy temporaries below stay referenced until each call returns
         if qc.bloch is not None:
             b = qc.bloch
             c = native.f64([b[k] for k in ("kz", "cz", "fxy", "ax_c", "ax_s", "ay_c", "ay_s", "az_c", "az_s",
