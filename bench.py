@@ -314,7 +314,7 @@ def run_mine(args, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(plan, args, k),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches + 2 * args.steps),
+        "gpu_launches": int(launches),  # fused step + edge-tile + row-0 sample kernels (library count)
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),

@@ -152,6 +152,7 @@ int mbg_fp64_peak(int device, double *tflops);
  * mbg_advance between mark_begin/mark_end (CUDA events on the solver stream) */
 int mbg_event_begin(mbg_solver *s);
 int mbg_event_end(mbg_solver *s, float *ms);
+/* kernels this handle has launched so far (step, edge, sample and halo kernels) */
 int mbg_launch_count(const mbg_solver *s, int64_t *launches);
 
 #ifdef __cplusplus

@@ -209,7 +209,8 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
+cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles, int *kernels) {
+    *kernels = 1;
     if (s->bloch || s->g.levels == 0) {
         BlochParams P;
         std::memset(&P, 0, sizeof(P));
@@ -226,8 +227,8 @@ cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles) {
             const double u = b.a0_c * b.a0_c;
             P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c, 1.0 - u, b.pol_factor * b.mu_x};
         }
-        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join)
-                          : fast::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join);
+        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels)
+                          : fast::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels);
     }
     switch (s->g.levels) {
         case 2: return launch_dense_n<2>(s, L, tiles);
@@ -616,6 +617,7 @@ int mbg_sample(mbg_solver *s, int64_t step) {
     cudaSetDevice(s->g.device);
     const Launch L = base_launch(s);
     CK(launch_sample(L, s->g.levels, s->bloch ? 1 : 0, step, s->stream));
+    ++s->launches;
     return MBG_OK;
 }
 
@@ -671,8 +673,9 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
             L.check[t] = (step % 1024 == 0 || step == s->g.num_t - 1) ? 1 : 0;
         }
         const long long tiles = (L.res_hi - L.res_lo + L.tile_own - 1) / L.tile_own;
-        CK(launch_step(s, L, tiles));
-        ++s->launches;
+        int kernels = 0;
+        CK(launch_step(s, L, tiles, &kernels));
+        s->launches += kernels;
         s->cur ^= 1;
         n += kk;
     }
@@ -753,6 +756,7 @@ static int halo(mbg_solver *s, bool pack, int64_t cell0, int64_t count, uint64_t
     cudaSetDevice(s->g.device);
     CK(launch_halo(pack, s->e[s->cur], s->h[s->cur], s->s[s->cur], s->plane, s->words, l0, count,
                    reinterpret_cast<double *>(buf), s->stream));
+    ++s->launches;
     return MBG_OK;
 }
 

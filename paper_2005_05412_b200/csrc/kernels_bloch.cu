@@ -451,8 +451,9 @@ int bloch_cta_tile() { return kBlochCtaTile; }
 // forked from and joined back into the launch stream, so they overlap the
 // interior kernel instead of trailing it.
 cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, cudaStream_t st_edge,
-                         cudaEvent_t fork, cudaEvent_t join) {
+                         cudaEvent_t fork, cudaEvent_t join, int *kernels) {
     const Launch &L = P.L;
+    *kernels = 1;
     cudaError_t err = cudaEventRecord(fork, st);
     if (err == cudaSuccess) err = cudaStreamWaitEvent(st_edge, fork, 0);
     if (err != cudaSuccess) return err;
@@ -463,6 +464,7 @@ cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,
         if (T.n == 0) return cudaSuccess;
         const int blocks = (T.n + kEdgeWarps - 1) / kEdgeWarps;
         bloch_edge_kernel<<<blocks, kEdgeWarps * 32, 0, st_edge>>>(P, T);
+        ++*kernels;
         T.n = 0;
         return cudaGetLastError();
     };

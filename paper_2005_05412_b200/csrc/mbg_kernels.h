@@ -45,7 +45,8 @@ __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <
     namespace NS {                                                                            \
     int bloch_cta_tile();                                                                     \
     cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,          \
-                             cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join);        \
+                             cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join,         \
+                             int *kernels);                                                    \
     cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \
     cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStream_t st);   \
     }

@@ -387,8 +387,8 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
             "config": {"workload": f"cfg2 weak-scaled: {world} slabs x 2^22 cells, 20000 steps",
                        "num_x": grid.num_x, "tile_steps": k, "parallelism": f"slab{world}",
                        "exchange": "NCCL batched isend/irecv of k ghost cells per interface every k steps"},
-            # fused step launches + per exchange up to 2 pack and 2 unpack kernels + row-0 samples
-            "gpu_launches": int(launches + 4 * launches + args.steps),
+            # this rank's kernels (step, edge, sample, halo pack/unpack; library count)
+            "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
