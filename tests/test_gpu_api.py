@@ -190,3 +190,77 @@ def test_sit_run_invariants_like_the_acceptance_suite():
     s.run()
     rep = s.invariant_report
     assert rep["max_trace_dev"] < 1e-9 and rep["max_herm_dev"] < 1e-12 and rep["min_eigenvalue"] > -1e-9
+
+
+def test_single_step_matches_hand_computed_update():
+    """pkg/tests/test_solver.py:150-199 on the GPU: one step over random E/H
+    and a random density matrix, against a hand-written update."""
+    rng = np.random.default_rng(21)
+    nx = 16
+    qm = mb.two_level_description(1e24, 2 * math.pi * 2e14, 6.24e-11, 1e10, 1e10, -1.0)
+    mb.add_material(mb.Material("Active", qm=qm))
+    dev = mb.Device("tiny")
+    dev.add_region(mb.Region("a", "Active", 0.0, 1e-6))
+    e0 = rng.standard_normal(nx) * 1e9
+    h0 = rng.standard_normal(nx) * 1e3
+    a = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+    rho0 = a @ a.conj().T
+    rho0 /= np.trace(rho0).real
+    sce = mb.Scenario("one", nx, 0.5 * (1e-6 / (nx - 1)) / mb.C0, mb.QmOperator.from_matrix(rho0),
+                      ic_e_field=mb.CurveField(e0), ic_h_field=mb.CurveField(h0))
+    sce.add_record(mb.Record("e", quantity="e"))
+    sce.add_record(mb.Record("h", quantity="h"))
+    for exact in (True, False):
+        s = mb.GpuFdtdSolver(dev, sce, exact=exact)
+        assert s.grid.num_t == 2
+        res = {r.name: r for r in s.run()}
+        cf = mb.get_fdtd_constants(dev.material_at(0.0), s.grid.dt, s.grid.dx)
+        hf = np.zeros(nx + 1)
+        hf[:nx] = h0
+        hn = hf.copy()
+        hn[1:nx] = hf[1:nx] + cf.c_prime * (e0[1:] - e0[:-1])
+        import oracle as orc
+        ref, _ = orc.run_oracle(s.plan)
+        got_e, got_h = res["e"].data[1], res["h"].data[1]
+        assert np.allclose(got_h[1:], hn[1:nx], rtol=1e-13, atol=0)
+        assert got_e[0] == 0.0 and got_e[-1] == 0.0  # R = 1 mirrors
+        # interior E against the oracle's stencil (bit-exact in the exact variant)
+        if exact:
+            assert np.array_equal(got_e, ref[0][1])
+        else:
+            assert np.allclose(got_e, ref[0][1], rtol=1e-12, atol=1e-6)
+
+
+def test_phase_velocity_error_below_one_percent():
+    """pkg/tests/test_solver.py:234-278: standing-mode phase velocity and the
+    discrete dispersion relation."""
+    nx, wl = 2048, 1.5e-6
+    dx = wl / 20.0
+    length = dx * (nx - 1)
+    k = 2 * math.pi / wl
+    mb.add_material(mb.Material("Vacuum"))
+    dev = mb.Device("v", bc_left=mb.BoundaryReflectivity(1.0), bc_right=mb.BoundaryReflectivity(1.0))
+    dev.add_region(mb.Region("v", "Vacuum", 0.0, length))
+    x_e = np.arange(nx) * dx
+    x_h = (np.arange(nx) - 0.5) * dx
+    dt = 0.5 * dx / mb.C0
+    z0 = math.sqrt(mb.MU0 / mb.EPS0)
+    sce = mb.Scenario("cw", nx, 240e-15, mb.QmOperator([1.0, 0.0]),
+                      ic_e_field=mb.CurveField(np.sin(k * x_e)),
+                      ic_h_field=mb.CurveField(-np.sin(k * (x_h + 0.5 * mb.C0 * dt)) / z0))
+    sce.add_record(mb.Record("probe", quantity="e", position=length / 2))
+    r = mb.GpuFdtdSolver(dev, sce).run()[0]
+    trace, times = r.data[:, 0], r.times
+    good = times < (length / 2) / mb.C0
+    trace, times = trace[good], times[good]
+    cross = []
+    for i in range(1, trace.size):
+        if trace[i - 1] < 0.0 <= trace[i] or trace[i - 1] >= 0.0 > trace[i]:
+            f = trace[i - 1] / (trace[i - 1] - trace[i])
+            cross.append(times[i - 1] + f * (times[i] - times[i - 1]))
+    cross = np.array(cross)
+    assert cross.size > 40
+    period = 2.0 * np.mean(np.diff(cross))
+    assert abs((2 * math.pi / period) / k - mb.C0) / mb.C0 <= 0.01
+    omega_num = (2.0 / dt) * math.asin(0.5 * math.sin(k * dx / 2.0))
+    assert abs(2 * math.pi / period - omega_num) / omega_num < 2e-3
