@@ -76,6 +76,21 @@ __device__ __forceinline__ void herm(V &s, int i, int j, double &re, double &im)
     }
 }
 
+// 1/d for a normal positive d (|pivot|^2 of (I + iA)/2 is >= 1/4): the fast
+// variant uses the hardware seed + two Newton steps, no special-case branch
+__device__ __forceinline__ double recip_pos(double d) {
+#if defined(MBG_EXACT) && MBG_EXACT
+    return 1.0 / d;
+#else
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
 template <int N, class VA, class VB, class MG>
@@ -108,7 +123,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const double pr = G.r(k, k), pi = G.m(k, k);
-        const double rd = 1.0 / mad(pi, pi, pr * pr);
+        const double rd = recip_pos(mad(pi, pi, pr * pr));
         const double ir = pr * rd, ii = -pi * rd;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
