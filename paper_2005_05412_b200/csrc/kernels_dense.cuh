@@ -253,9 +253,13 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
 // Same derivative for N >= 4 with H = h0 - E mu formed row by row on the fly
 // (a full H would hold 2N^2 doubles in registers).  The empty asm on the
 // field value keeps the compiler from caching H rows across (i, j) pairs.
-template <int N, class VS, class VD>
-__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VS &src, VD &dst) {
+template <int N, class VS0, class VD>
+__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VS0 &src0, VD &dst) {
     constexpr double kInvHbar = 1.0 / 1.054571817e-34;
+    // one pass over the shared-memory state into registers: every entry is used 2N times
+    RegVec<N * N> src;
+#pragma unroll
+    for (int w = 0; w < N * N; ++w) src[w] = src0[w];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double ei = e;

@@ -1,0 +1,24 @@
+"""Small runs covering every kernel family, for compute-sanitizer (memcheck/racecheck)."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import paper_2005_05412_b200 as mb  # noqa: E402
+from cases import CASES  # noqa: E402
+from paper_2005_05412_b200 import slabs  # noqa: E402
+
+for name in ["sit_hard_whole", "multi_material", "vacuum_sources", "rand3_split", "rand5_split", "rand8_split",
+             "rand2_rk4", "rand4_rk4", "kernel6_split", "song_point", "point2", "tiny_group"]:
+    mb.clear_material_library()
+    build, stepper = CASES[name]
+    dev, sce = build(mb)
+    mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True).run()
+    print("ok", name, flush=True)
+mb.clear_material_library()
+build, stepper = CASES["multi_material"]
+dev, sce = build(mb)
+slabs.run_slabs_local(mb.GpuFdtdSolver(dev, sce, stepper=stepper), 3)
+print("ok slabs", flush=True)
