@@ -271,8 +271,10 @@ def run_slabs_local(solver, slabs_count: int):
 
 
 def tile_steps_of(solver) -> int:
-    """The k the native solver will use for this scenario (asks the library)."""
-    h = native.Handle(solver._grid_struct())
+    """The k the native solver will use for this scenario (asks the library
+    through a throw-away handle on a tiny window, so nothing big is allocated)."""
+    w = min(solver.grid.num_x, 1024)
+    h = native.Handle(solver._grid_struct(win=(0, w), own=(0, w)))
     try:
         k = C.c_int32(0)
         h.call("mbg_tile_steps", C.byref(k))
