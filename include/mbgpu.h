@@ -54,9 +54,9 @@ extern "C" {
 #define MBG_Q_D 2
 #define MBG_Q_INV 3
 
-#define MBG_MAX_REGIONS 16
+#define MBG_MAX_REGIONS 128
 #define MBG_MAX_QM 4
-#define MBG_MAX_SOURCES 8
+#define MBG_MAX_SOURCES 32
 #define MBG_MAX_RECORDS 64
 #define MBG_MAX_LEVELS 8
 #define MBG_MAX_TILE_STEPS 128

@@ -398,7 +398,7 @@ int mbg_tile_steps(const mbg_solver *s, int32_t *k) {
 int mbg_set_regions(mbg_solver *s, int32_t n, const int64_t *e_start, const int64_t *h_start, const double *a,
                     const double *bg, const double *bdx, const double *ch, const int32_t *qm_index) {
     if (!s || n < 1) return fail(s, MBG_E_ARG, "need at least one region");
-    if (n > kMaxRegions) return fail(s, MBG_E_UNSUPPORTED, "too many regions (max 16)");
+    if (n > kMaxRegions) return fail(s, MBG_E_UNSUPPORTED, "too many regions (max 128)");
     Regions &rg = s->rg;
     std::memset(&rg, 0, sizeof(rg));
     rg.n = n;
@@ -503,7 +503,7 @@ int mbg_set_boundary(mbg_solver *s, double wl, double cl, double zl, double wr, 
 
 int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t *hard, const double *values) {
     if (!s || n < 0) return MBG_E_ARG;
-    if (n > kMaxSources) return fail(s, MBG_E_UNSUPPORTED, "too many sources (max 8)");
+    if (n > kMaxSources) return fail(s, MBG_E_UNSUPPORTED, "too many sources (max 32)");
     cudaSetDevice(s->g.device);
     dfree(s->stream, s->src_values);
     s->src_values = nullptr;

@@ -129,11 +129,19 @@ struct DenseParams {
 };
 
 // shared helpers (host + device)
+// last region r with start[r] <= m (0 if none); starts are non-decreasing,
+// empty regions repeat a start and are skipped by taking the last match
 __host__ __device__ inline int region_of(const long long *start, int n, long long m) {
-    int r = 0;
+    int lo = 0, hi = n - 1;
 #pragma unroll 1
-    for (int q = 1; q < n; ++q) r += m >= start[q] ? 1 : 0;
-    return r;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (start[mid] <= m)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
 }
 
 // two-level kernel geometry: tile t covers result cells [t_lo, t_hi) and loads

@@ -21,7 +21,7 @@ LIB_PATH = Path(os.environ.get("MBGPU_LIB", PKG / "_build" / "libmbgpu.so"))
 HEADER = PKG.parent / "include" / "mbgpu.h"
 
 MBG_STEPPER = {"splitting": 0, "rk4": 1}
-MAX_REGIONS, MAX_QM, MAX_SOURCES, MAX_RECORDS, MAX_LEVELS, MAX_TILE_STEPS = 16, 4, 8, 64, 8, 128
+MAX_REGIONS, MAX_QM, MAX_SOURCES, MAX_RECORDS, MAX_LEVELS, MAX_TILE_STEPS = 128, 4, 32, 64, 8, 128
 
 
 class MbgGrid(C.Structure):

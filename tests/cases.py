@@ -204,6 +204,32 @@ def point2(api):
     return dev, sce
 
 
+def bragg_stack(api):
+    """A 100-layer periodic stack (the reference's material library exists for
+    such structures, core.py:1-9) around a two-level slab: 103 regions."""
+    qm = api.two_level_description(1e24, 2.0 * math.pi * 2e14, 6.24e-11, 1e10, 1e11, -1.0)
+    lo = api.ensure_material(api.Material("LowN", rel_permittivity=1.0))
+    hi = api.ensure_material(api.Material("HighN", rel_permittivity=2.25, losses=50.0))
+    act = api.ensure_material(api.Material("BraggActive", qm=qm))
+    dev = api.Device("bragg", bc_left=api.BoundaryReflectivity(0.0), bc_right=api.BoundaryReflectivity(0.5))
+    x = 0.0
+    dev.add_region(api.Region("lead", lo.id, 0.0, 5e-6))
+    x = 5e-6
+    for k in range(100):
+        w = 0.25e-6 if k % 2 == 0 else 0.1667e-6
+        dev.add_region(api.Region(f"l{k}", (hi if k % 2 == 0 else lo).id, x, x + w))
+        x = x + w
+    dev.add_region(api.Region("slab", act.id, x, x + 10e-6))
+    x = x + 10e-6
+    dev.add_region(api.Region("tail", lo.id, x, x + 5e-6))
+    sce = api.Scenario("s", 4000, 250e-15, api.QmOperator([1.0, 0.0]))
+    sce.add_source(api.SechPulse("s", 1e-6, "soft", 4e9, 2e14, 8.0, 1e14))
+    sce.add_record(api.Record("e", quantity="e", interval=25e-15))
+    sce.add_record(api.Record("inv", quantity="inv", interval=25e-15))
+    sce.add_record(api.Record("probe", quantity="e", position=3e-6))
+    return dev, sce
+
+
 def kernel_case(dim, seed, stepper="splitting", nx=64):
     """One time step over nx cells with random E: isolates the per-cell
     stepper (the scenario-level twin of pkg/tests/test_solver.py:437-480)."""
@@ -228,6 +254,7 @@ def kernel_case(dim, seed, stepper="splitting", nx=64):
     return build, stepper
 
 
+CASES["bragg_stack"] = (bragg_stack, "splitting")
 CASES["song_point"] = (song_point, "splitting")
 CASES["song_point_rk4"] = (song_point, "rk4")
 CASES["point2"] = (point2, "splitting")

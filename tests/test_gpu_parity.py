@@ -20,7 +20,7 @@ TOL = 1e-9
 # cases whose arithmetic the exact variant reproduces bit for bit: the Bloch
 # splitting kernel and the pure FDTD path (tiny_group excluded: the reference
 # steps groups of <= 32 cells with numpy's ScalarKernel, _kernels.py:404-425)
-BITWISE = {"cfg1_full", "cfg2_r16", "cfg2_full", "cfg2_stress_full", "sit_hard_whole", "multi_material",
+BITWISE = {"cfg1_full", "cfg2_r16", "cfg2_full", "cfg2_stress_full", "sit_hard_whole", "multi_material", "bragg_stack",
            "vacuum_sources", "rand2_split", "kernel2_split"}
 ALL = sorted(CASES)
 
