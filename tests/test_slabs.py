@@ -108,3 +108,53 @@ def test_native_slabs_on_one_gpu_match_single_domain(case, count):
     for a, b in zip(ref, got):
         assert a.name == b.name and a.data.shape == b.data.shape
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
+
+
+def _nccl_single(fn):
+    """Run fn() inside a one-rank NCCL process group (the only NCCL shape one GPU allows)."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        return fn()
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_run_slab_rank_nccl_world_one_matches_single_domain():
+    """The torch.distributed driver of the native slab path (stream hand-off,
+    TorchTransport, MIN reduction of the scan flag, gather of records)."""
+    import torch
+
+    dev, sce, stepper = build_case("multi_material")
+    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case("multi_material")
+    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    recs = _nccl_single(lambda: slabs.run_slab_rank(solver, 1, 0, torch.device("cuda", 0)))
+    for a, b in zip(ref, recs):
+        assert np.array_equal(a.data, b), a.name
+
+
+@pytest.mark.gpu
+def test_bench_rank_prints_a_line(capsys, monkeypatch):
+    """bench.py's multi-GPU code path on one rank (NCCL world size 1)."""
+    import json
+    import types
+
+    from paper_2005_05412_b200 import configs
+
+    args = types.SimpleNamespace(tile_steps=None, exact=False, steps=1, warmup=1)
+    mb.clear_material_library()
+    dev, sce = configs.cfg2(mb, nx=1 << 16, steps=512)
+    # bench_rank initialises (and destroys) its own process group
+    for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(_free_port())), ("RANK", "0"),
+                     ("WORLD_SIZE", "1")):
+        monkeypatch.setenv(key, val)
+    slabs.bench_rank(args, dev, sce, 1, 0, 0, "m", "cell-updates/s")
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
