@@ -95,9 +95,6 @@ __device__ __forceinline__ double recip_pos(double d) {
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
 template <int N, class VA, class VB, class MG>
 __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G) {
-    double od[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) od[i] = A[i];
     // relaxation half step -> B
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -153,7 +150,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
 #pragma unroll
     for (int i = 0; i < N; ++i) G.r(i, i) -= 1.0;
     // rho' = U r1 U^H, one row at a time; second relaxation half step fused
-    double acc_p = 0.0;
+    double acc_p = 0.0, raw[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double tr[N], ti[N];
@@ -187,7 +184,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
                 if (j != i) ai = mad(ti[k], ur, mad(-tr[k], ui, ai));  // diagonal is real
             }
             if (j == i) {
-                A[i] = ar;  // raw diagonal; relaxed below
+                raw[i] = ar;  // raw diagonal; relaxed below (A keeps the old one until then)
             } else {
                 const double c = q.coh[i * N + j];
                 const double fr = ar * c, fi = ai * c;
@@ -198,18 +195,19 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             }
         }
     }
-    double raw[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) raw[i] = A[i];
+    double nd[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double acc = q.pop[i * N] * raw[0];
 #pragma unroll
         for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], raw[j], acc);
-        A[i] = acc;
+        nd[i] = acc;
     }
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc_p = mad(q.pol.pol_dv[i], A[i] - od[i], acc_p);
+    for (int i = 0; i < N; ++i) {
+        acc_p = mad(q.pol.pol_dv[i], nd[i] - A[i], acc_p);
+        A[i] = nd[i];
+    }
     return q.pol.pol_factor * acc_p;
 }
 
