@@ -61,6 +61,10 @@ extern "C" {
 #define MBG_MAX_LEVELS 8
 #define MBG_MAX_TILE_STEPS 128
 
+/* mbg_grid.flags: one kernel launch per k fused steps instead of the
+   persistent wavefront launch (two-level / classical, non-windowed solvers) */
+#define MBG_FLAG_PER_LAUNCH 1
+
 typedef struct mbg_solver mbg_solver;
 
 typedef struct {
@@ -72,7 +76,7 @@ typedef struct {
     int32_t tile_steps; /* k: time steps fused per kernel launch (0 = default) */
     int32_t exact;      /* 1: no FMA contraction (bit-exact to the reference for N = 2) */
     int32_t device;     /* CUDA device ordinal */
-    int32_t reserved;
+    int32_t flags;      /* MBG_FLAG_* */
     int64_t win_lo, win_hi; /* cells held on this device (slab incl. ghosts) */
     int64_t own_lo, own_hi; /* cells owned (recorded, scanned) by this device */
 } mbg_grid;

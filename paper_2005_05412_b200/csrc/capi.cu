@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -67,6 +68,10 @@ struct mbg_solver {
     unsigned long long *bad = nullptr;
     double *ck_e = nullptr, *ck_h = nullptr, *ck_s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned *wave = nullptr;  // persistent launch: [0] ticket, [1] stall, [2..] done flags
+    long long wave_cap = 0;
+    WaveItem *wave_items = nullptr;  // work items of one chunk (fixed per solver)
+    long long wave_n = 0;
     long long launches = 0;
     std::string err;
 };
@@ -209,24 +214,29 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
     return cudaErrorInvalidValue;
 }
 
+BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
+    BlochParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.L = L;
+    P.n_qm = (int)s->qm.size();
+    P.real_dipole = P.n_qm > 0 ? 1 : 0;
+    for (int q = 0; q < P.n_qm; ++q) {
+        BlochQm &b = P.qm[q];
+        std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
+        // _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
+        const bool real = b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 && b.a0_s == 0.0 &&
+                          b.mu_y == 0.0 && b.mu_z == 0.0;
+        P.real_dipole &= real ? 1 : 0;
+        const double u = b.a0_c * b.a0_c;
+        P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c, 1.0 - u, b.pol_factor * b.mu_x};
+    }
+    return P;
+}
+
 cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles, int *kernels) {
     *kernels = 1;
     if (s->bloch || s->g.levels == 0) {
-        BlochParams P;
-        std::memset(&P, 0, sizeof(P));
-        P.L = L;
-        P.n_qm = (int)s->qm.size();
-        P.real_dipole = P.n_qm > 0 ? 1 : 0;
-        for (int q = 0; q < P.n_qm; ++q) {
-            BlochQm &b = P.qm[q];
-            std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
-            // _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
-            const bool real = b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 &&
-                              b.a0_s == 0.0 && b.mu_y == 0.0 && b.mu_z == 0.0;
-            P.real_dipole &= real ? 1 : 0;
-            const double u = b.a0_c * b.a0_c;
-            P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c, 1.0 - u, b.pol_factor * b.mu_x};
-        }
+        const BlochParams P = bloch_params(s, L);
         return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels)
                           : fast::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels);
     }
@@ -353,6 +363,8 @@ void mbg_destroy(mbg_solver *s) {
         dfree(st, s->s[b]);
     }
     dfree(st, s->bad);
+    dfree(st, s->wave);
+    dfree(st, s->wave_items);
     dfree(st, s->ck_e);
     dfree(st, s->ck_h);
     dfree(st, s->ck_s);
@@ -640,6 +652,126 @@ static int check_ready(mbg_solver *s) {
     return MBG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// the whole step range in one persistent launch (kernels_bloch.cu, BlochWave)
+int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
+    const int k = s->k;
+    Launch L = base_launch(s);
+    L.n0 = first;
+    L.k = k;
+    L.res_lo = 0;
+    L.res_hi = s->g.num_x;
+    L.tile_own = tw - 2 * k;
+    if (!s->wave_items) {
+        // interior CTA tiles as they are; a non-interior tile split into items
+        // of at most one round of warp ranges (host twin of the kernels'
+        // classification, the same as launch_bloch's)
+        const long long ct = (L.res_hi - L.res_lo + L.tile_own - 1) / L.tile_own;
+        const long long warp_own = kBlochTile - 2 * k;
+        std::vector<WaveItem> items;
+        for (long long t = 0; t < ct; ++t) {
+            const long long t_lo = L.res_lo + t * L.tile_own;
+            const long long t_hi = std::min(t_lo + L.tile_own, L.res_hi);
+            if (tile_is_interior(L, tile_base(L, t_lo), tw)) {
+                items.push_back(WaveItem{t_lo, t_hi, 0, 0});
+                continue;
+            }
+            for (long long lo = t_lo; lo < t_hi; lo += kBlochWarpsPerBlock * warp_own)
+                items.push_back(WaveItem{lo, std::min(lo + kBlochWarpsPerBlock * warp_own, t_hi), 1, 0});
+        }
+        // every item but the last must span >= k cells (dependencies j-1 .. j+1)
+        std::vector<WaveItem> merged;
+        for (size_t j = 0; j < items.size(); ++j) {
+            const bool last = j + 1 == items.size();
+            if (!merged.empty() && (items[j].hi - items[j].lo < k && !last ||
+                                    merged.back().hi - merged.back().lo < k)) {
+                merged.back().hi = items[j].hi;
+                merged.back().edge = 1;
+            } else {
+                merged.push_back(items[j]);
+            }
+        }
+        CK(dalloc(s->stream, reinterpret_cast<double **>(&s->wave_items), sizeof(WaveItem) * merged.size()));
+        CK(cudaMemcpyAsync(s->wave_items, merged.data(), sizeof(WaveItem) * merged.size(), cudaMemcpyHostToDevice,
+                           s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        s->wave_n = (long long)merged.size();
+    }
+    const long long tiles = s->wave_n;
+    const long long n_chunks = (n_steps + k - 1) / k;
+    // [ticket, stall, done flags][masks (8 B per step)][checks (1 B per step)], in 4-byte words
+    const long long flags = 2 + n_chunks * tiles;
+    const long long mask_off = (flags + 1) / 2 * 2, check_off = mask_off + 2 * n_chunks * k;
+    const long long need = check_off + (n_chunks * k + 3) / 4;
+    if (need > s->wave_cap) {
+        dfree(s->stream, s->wave);
+        s->wave = nullptr;
+        s->wave_cap = 0;
+        CK(dalloc(s->stream, reinterpret_cast<double **>(&s->wave), sizeof(unsigned) * need));
+        s->wave_cap = need;
+    }
+    CK(cudaMemsetAsync(s->wave, 0, sizeof(unsigned) * flags, s->stream));
+    auto *masks = reinterpret_cast<unsigned long long *>(s->wave + mask_off);
+    auto *checks = reinterpret_cast<unsigned char *>(s->wave + check_off);
+    BlochWave V;
+    std::memset(&V, 0, sizeof(V));
+    V.n_chunks = (int)n_chunks;
+    V.last_steps = (int)(n_steps - (n_chunks - 1) * k);
+    V.tiles = tiles;
+    V.items = s->wave_items;
+    V.n0 = first;
+    V.last_step = s->g.num_t - 1;
+    V.masks = masks;
+    V.checks = checks;
+    for (int b = 0; b < 2; ++b) {
+        V.e[b] = s->e[b];
+        V.h[b] = s->h[b];
+        V.s[b] = s->s[b];
+    }
+    V.cur = s->cur;
+    V.ticket = s->wave;
+    V.stall = s->wave + 1;
+    V.done = s->wave + 2;
+    CK(s->g.exact ? exact::launch_wave_masks(L, n_steps, V.last_step, masks, checks, s->stream)
+                  : fast::launch_wave_masks(L, n_steps, V.last_step, masks, checks, s->stream));
+    const BlochParams P = bloch_params(s, L);
+    const char *trace_path = std::getenv("MBG_WAVE_TRACE");  // debug: per-item timeline
+    const size_t trace_bytes = sizeof(unsigned long long) * 4 * n_chunks * tiles;
+    if (trace_path) CK(cudaMalloc(reinterpret_cast<void **>(&V.trace), trace_bytes));
+    CK(s->g.exact ? exact::launch_bloch_wave(P, V, s->stream) : fast::launch_bloch_wave(P, V, s->stream));
+    if (trace_path) {
+        std::vector<unsigned long long> h(trace_bytes / sizeof(unsigned long long));
+        CK(cudaMemcpyAsync(h.data(), V.trace, trace_bytes, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        CK(cudaFree(V.trace));
+        if (FILE *f = std::fopen(trace_path, "wb")) {
+            const long long hdr[2] = {n_chunks, tiles};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(h.data(), 1, trace_bytes, f);
+            std::fclose(f);
+        }
+    }
+    s->launches += 1;
+    if (n_chunks & 1) s->cur ^= 1;
+    return MBG_OK;
+}
+
+// after a stream synchronize: a persistent launch that gave up waiting is an error
+int check_stall(mbg_solver *s) {
+    if (!s->wave) return MBG_OK;
+    unsigned v = 0;
+    CK(cudaMemcpy(&v, s->wave + 1, sizeof(v), cudaMemcpyDeviceToHost));
+    if (v) return fail(s, MBG_E_CUDA, "persistent step kernel: dependency wait timed out");
+    return MBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     if (!s) return MBG_E_ARG;
     if (int rc = check_ready(s)) return rc;
@@ -654,6 +786,8 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     }
     cudaSetDevice(s->g.device);
     const int tw = tile_width(s);
+    if (!windowed && (s->bloch || s->g.levels == 0) && !(s->g.flags & MBG_FLAG_PER_LAUNCH) && n_steps > s->k)
+        return advance_wave(s, first, n_steps, tw);
     long long n = first;
     const long long end = first + n_steps;
     while (n < end) {
@@ -686,7 +820,7 @@ int mbg_synchronize(mbg_solver *s) {
     if (!s) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
     CK(cudaStreamSynchronize(s->stream));
-    return MBG_OK;
+    return check_stall(s);
 }
 
 int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step) {
@@ -696,7 +830,7 @@ int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step) {
     CK(cudaMemcpyAsync(&v, s->bad, sizeof(v), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     *bad_step = v == ~0ull ? -1 : (int64_t)v;
-    return MBG_OK;
+    return check_stall(s);
 }
 
 static double from_key(unsigned long long k) {

@@ -35,6 +35,26 @@ constexpr int C = kBlochCellsPerLane;
 constexpr int W = kBlochTile;
 constexpr unsigned kFull = 0xffffffffu;
 
+// One fused chunk of k steps: where it reads and writes, its first step and
+// per-step record masks / scan flags.  Per-launch kernels point it at the
+// launch parameters, the persistent kernel at its chunk's slice.
+struct Chunk {
+    const double *e_in, *h_in, *s_in;
+    double *e_out, *h_out, *s_out;
+    long long n0;
+    int steps;
+    const unsigned long long *mask;
+    const unsigned char *check;
+};
+
+__device__ __forceinline__ Chunk launch_chunk(const Launch &L) {
+    return Chunk{L.e_in, L.h_in, L.s_in, L.e_out, L.h_out, L.s_out, L.n0, L.k, L.step_mask, L.check};
+}
+
+// field / state loads bypass L1 (streamed once per chunk; in the persistent
+// kernel another CTA of the same launch produced them)
+__device__ __forceinline__ double ld(const double *p) { return __ldcg(p); }
+
 // _kernels.py:200-232, same expression order (each mad(a, b, c) is the
 // reference's "c + a*b" term)
 __device__ __forceinline__ double bloch_cell(const BlochQm &q, double e, double &x, double &y, double &z) {
@@ -86,18 +106,19 @@ __device__ __forceinline__ double bloch_cell_real(const BlochQm &q, const BlochR
 
 #if !(defined(MBG_EXACT) && MBG_EXACT)
 // 1/d for d >= 1 (the Cayley denominator (1+q-u)^2 + 4u is never below 1):
-// hardware seed + two Newton steps, no special-case branch
+// hardware seed refined by one cubically convergent step r + r(e + e^2),
+// e = 1 - d r (seed error 2^-22 -> below double rounding), no special cases
 __device__ __forceinline__ double rcp_ge1(double d) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-    double e = fma(-d, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-d, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-d, r, 1.0);
+    return fma(r, fma(e, e, e), r);
 }
 
 // fast variant of bloch_cell_real: the same rotation regrouped around the
-// field-independent products g*az and 8/den (tolerance-level, not bitwise)
+// field-independent products g*az and 8/den (tolerance-level, not bitwise).
+// Returns x - x0: the factor pol_factor*mu_x is folded into the E update's
+// coefficient (pol_coef)
 __device__ __forceinline__ double bloch_cell_real_fast(const BlochQm &q, const BlochReal &r, double e, double &x,
                                                        double &y, double &z) {
     const double x0 = x, y0 = y, z0 = z;
@@ -117,12 +138,21 @@ __device__ __forceinline__ double bloch_cell_real_fast(const BlochQm &q, const B
     x = q.fxy * x2;
     y = q.fxy * y2;
     z = fma(q.kz, z2, q.cz);
-    return r.pfmu * (x - x0);
+    return x - x0;
 }
 #define MBG_BLOCH_REAL bloch_cell_real_fast
+#define MBG_POL_FOLD 1
 #else
 #define MBG_BLOCH_REAL bloch_cell_real
+#define MBG_POL_FOLD 0
 #endif
+
+// coefficient of the polarisation term in the E update (b' G, times the
+// real-dipole factor the fast cell function leaves out); interior and edge
+// paths form it from the same operands, so their E values agree bitwise
+__device__ __forceinline__ double pol_coef(double bg, const BlochReal &r, bool real) {
+    return (MBG_POL_FOLD && real) ? bg * r.pfmu : bg;
+}
 
 // density entry (i, j) of a Bloch vector (_kernels.py:530-536)
 __device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, double z, double &re, double &im) {
@@ -140,8 +170,8 @@ __device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, do
 // and kept as bit masks; UNI tiles (one E and one H region) take scalar
 // coefficients and one material, the rare interface tiles look them up per slot.
 template <bool UNI>
-__device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, long long t_hi, long long base,
-                                         int lane) {
+__device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
+                                         long long base, int lane) {
     const Launch &L = P.L;
     const long long nx = L.num_x;
     double E[C], H[C], X[C], Y[C], Z[C];
@@ -159,8 +189,8 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         const long long c = base + i * 32 + lane;
         const long long l = c - L.win_lo;
         const bool in_e = (l >= 0 && l < L.win_n);
-        E[i] = in_e ? L.e_in[l] : 0.0;
-        H[i] = (l >= 0 && l <= L.win_n) ? L.h_in[l] : 0.0;
+        E[i] = in_e ? ld(K.e_in + l) : 0.0;
+        H[i] = (l >= 0 && l <= L.win_n) ? ld(K.h_in + l) : 0.0;
         const int re = UNI ? re_u : region_of(L.rg.e_start, L.rg.n, c);
         const int rh = UNI ? rh_u : region_of(L.rg.h_start, L.rg.n, c);
         if (!UNI) {
@@ -176,18 +206,19 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         rmask |= (right_edge && c == nx - 1) ? 1u << i : 0u;
         for (int q = 0; q < L.n_src; ++q) smask |= c == L.src_cell[q] ? 1u << i : 0u;
         if (qi[i] >= 0) {
-            X[i] = L.s_in[l];
-            Y[i] = L.s_in[L.plane + l];
-            Z[i] = L.s_in[2 * L.plane + l];
+            X[i] = ld(K.s_in + l);
+            Y[i] = ld(K.s_in + L.plane + l);
+            Z[i] = ld(K.s_in + 2 * L.plane + l);
         } else {
             X[i] = Y[i] = Z[i] = 0.0;
         }
     }
     const double ua = L.rg.a[re_u], ubg = L.rg.bg[re_u], ubdx = L.rg.bdx[re_u], uch = L.rg.ch[rh_u];
     const int qs = qu < 0 ? 0 : qu;
+    const double ubgp = pol_coef(ubg, P.rq[qs], P.real_dipole);
 
-    for (int s = 0; s < L.k; ++s) {
-        const long long n = L.n0 + s;
+    for (int s = 0; s < K.steps; ++s) {
+        const long long n = K.n0 + s;
         // ---- H update: needs E[m-1] (left neighbour) -----------------------
         double t[C];
 #pragma unroll
@@ -223,8 +254,9 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
             const double hr = (lane == 31) ? u[i < C - 1 ? i + 1 : i] : u[i];
             double en = E[i];
             if ((emask >> i) & 1u)
-                en = UNI ? mad(ubdx, hr - Hn[i], mad(ua, E[i], -(ubg * p[i])))
-                         : mad(cbdx[i], hr - Hn[i], mad(ca[i], E[i], -(cbg[i] * p[i])));
+                en = UNI ? mad(ubdx, hr - Hn[i], mad(ua, E[i], -(ubgp * p[i])))
+                         : mad(cbdx[i], hr - Hn[i],
+                               mad(ca[i], E[i], -(pol_coef(cbg[i], P.rq[qi[i] < 0 ? 0 : qi[i]], P.real_dipole) * p[i])));
             if (left_edge && i == 0 && lane == 0) {
                 // solver_fdtd.py:372-374
                 const double e_at = mad(L.l_c, e_right0, L.l_omc * E[0]);
@@ -250,8 +282,8 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
             H[i] = Hn[i];
         }
         // ---- non-finite scan and records (owned result cells only) --------------
-        const unsigned long long mask = L.step_mask[s];
-        const bool check = L.check[s] != 0;
+        const unsigned long long mask = K.mask[s];
+        const bool check = K.check[s] != 0;
         if (mask || check) {
 #pragma unroll
             for (int i = 0; i < C; ++i) {
@@ -287,12 +319,12 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
         const long long c = base + i * 32 + lane;
         if (c < t_lo || c >= t_hi) continue;
         const long long l = c - L.win_lo;
-        L.e_out[l] = E[i];
-        L.h_out[l] = H[i];
+        K.e_out[l] = E[i];
+        K.h_out[l] = H[i];
         if (qi[i] >= 0) {
-            L.s_out[l] = X[i];
-            L.s_out[L.plane + l] = Y[i];
-            L.s_out[2 * L.plane + l] = Z[i];
+            K.s_out[l] = X[i];
+            K.s_out[L.plane + l] = Y[i];
+            K.s_out[2 * L.plane + l] = Z[i];
         }
     }
 }
@@ -305,29 +337,37 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, long long t_lo, l
 // and the two cells at each warp seam go through double-buffered shared
 // slots (two barriers per step).  For a single quantum material the stepper
 // constants are constant-bank operands.
-template <bool QM, bool ONE_QM, bool REAL = false>
-__device__ __forceinline__ void interior_cta(const BlochParams &P, long long t_lo, long long t_hi, long long base,
-                                             int r_e, int r_h) {
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
+// hook(): runs once the tile's loads are in flight, before the first step
+// (the persistent kernel stages its step masks and claims its next item there)
+template <bool QM, bool ONE_QM, bool REAL = false, class Hook = NoHook>
+__device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
+                                             long long base, int r_e, int r_h, const Hook &hook = Hook()) {
     __shared__ double seam_e[2][kBlochWarpsPerBlock], seam_h[2][kBlochWarpsPerBlock];
     const Launch &L = P.L;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double a = L.rg.a[r_e], bg = L.rg.bg[r_e], bdx = L.rg.bdx[r_e], ch = L.rg.ch[r_h];
     const int qmi = QM ? (ONE_QM ? 0 : L.rg.qm[r_e]) : 0;
     const BlochQm &q = P.qm[qmi];
+    const double bgp = pol_coef(bg, P.rq[qmi], REAL);
     const long long first = base + (long long)warp * W + (long long)lane * C;  // this lane's first cell
     const long long l0 = first - L.win_lo;
     double E[C], H[C], X[C], Y[C], Z[C];
 #pragma unroll
     for (int i = 0; i < C; ++i) {
-        E[i] = L.e_in[l0 + i];
-        H[i] = L.h_in[l0 + i];
+        E[i] = ld(K.e_in + l0 + i);
+        H[i] = ld(K.h_in + l0 + i);
         if (QM) {
-            X[i] = L.s_in[l0 + i];
-            Y[i] = L.s_in[L.plane + l0 + i];
-            Z[i] = L.s_in[2 * L.plane + l0 + i];
+            X[i] = ld(K.s_in + l0 + i);
+            Y[i] = ld(K.s_in + L.plane + l0 + i);
+            Z[i] = ld(K.s_in + 2 * L.plane + l0 + i);
         }
     }
-    for (int s = 0; s < L.k; ++s) {
+    hook();
+    for (int s = 0; s < K.steps; ++s) {
         const int b = s & 1;
         // H update (uses E^{n-1}); H is overwritten in place with H^{n-1/2}
         if (lane == 31) seam_e[b][warp] = E[C - 1];
@@ -348,12 +388,12 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, long long t_l
                              : bloch_cell(q, E[i], X[i], Y[i], Z[i]);
             const double hr = i == C - 1 ? hr_last : H[i + 1];
             // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
-            E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bg * p))) : mad(bdx, hr - H[i], a * E[i]);
+            E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bgp * p))) : mad(bdx, hr - H[i], a * E[i]);
         }
-        const unsigned long long mask = L.step_mask[s];
-        const bool check = L.check[s] != 0;
+        const unsigned long long mask = K.mask[s];
+        const bool check = K.check[s] != 0;
         if (mask || check) {
-            const long long n = L.n0 + s;
+            const long long n = K.n0 + s;
 #pragma unroll
             for (int i = 0; i < C; ++i) {
                 const long long c = first + i;
@@ -384,12 +424,12 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, long long t_l
     for (int i = 0; i < C; ++i) {
         const long long c = first + i;
         if (c < t_lo || c >= t_hi) continue;
-        L.e_out[l0 + i] = E[i];
-        L.h_out[l0 + i] = H[i];
+        K.e_out[l0 + i] = E[i];
+        K.h_out[l0 + i] = H[i];
         if (QM) {
-            L.s_out[l0 + i] = X[i];
-            L.s_out[L.plane + l0 + i] = Y[i];
-            L.s_out[2 * L.plane + l0 + i] = Z[i];
+            K.s_out[l0 + i] = X[i];
+            K.s_out[L.plane + l0 + i] = Y[i];
+            K.s_out[2 * L.plane + l0 + i] = Z[i];
         }
     }
 }
@@ -399,6 +439,47 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, long long t_l
 #define MBG_BLOCH_MINB (16 / MBG_BLOCH_WARPS > 0 ? 16 / MBG_BLOCH_WARPS : 1)
 #endif
 constexpr int kEdgeWarps = 4;
+// interior CTA tile: dispatch on the medium (the density step must be the very
+// same formula the edge path uses -- bitwise independence of the tiling -- so
+// the real-dipole choice is global)
+template <class Hook = NoHook>
+__device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
+                                              long long base, const Hook &hook = Hook()) {
+    const Launch &L = P.L;
+    const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
+    const int qm = L.rg.qm[re];
+    if (qm < 0)
+        interior_cta<false, true>(P, K, t_lo, t_hi, base, re, rh, hook);
+    else if (P.real_dipole)
+        P.n_qm == 1 ? interior_cta<true, true, true>(P, K, t_lo, t_hi, base, re, rh, hook)
+                    : interior_cta<true, false, true>(P, K, t_lo, t_hi, base, re, rh, hook);
+    else
+        P.n_qm == 1 ? interior_cta<true, true, false>(P, K, t_lo, t_hi, base, re, rh, hook)
+                    : interior_cta<true, false, false>(P, K, t_lo, t_hi, base, re, rh, hook);
+}
+
+// one warp over the result range [t_lo, t_hi) of at most 32*C - 2k cells
+__device__ __forceinline__ void edge_range(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
+                                           int lane) {
+    const Launch &L = P.L;
+    const long long base = tile_base(L, t_lo);
+    const long long lo = base, hi = base + W - 1 < L.num_x ? base + W - 1 : L.num_x - 1;
+    const bool uni = region_of(L.rg.e_start, L.rg.n, lo) == region_of(L.rg.e_start, L.rg.n, hi) &&
+                     region_of(L.rg.h_start, L.rg.n, lo < 1 ? 1 : lo) ==
+                         region_of(L.rg.h_start, L.rg.n, hi < 1 ? 1 : hi);
+    if (uni)
+        run_tile<true>(P, K, t_lo, t_hi, base, lane);
+    else
+        run_tile<false>(P, K, t_lo, t_hi, base, lane);
+}
+
+// the persistent kernel's rare edge items: a call keeps the general path's
+// register allocation (and spills) out of the interior path
+__device__ __noinline__ void edge_range_call(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
+                                             int lane) {
+    edge_range(P, K, t_lo, t_hi, lane);
+}
+
 // interior tiles: one CTA per tile; the whole CTA leaves if its tile is not
 // interior (the host hands those to the edge kernel)
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
@@ -409,38 +490,143 @@ bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
     const long long base = tile_base(L, t_lo);
     if (!tile_is_interior(L, base, kBlochCtaTile)) return;
-    const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
-    const int qm = L.rg.qm[re];
-    // the density step must be the very same formula the edge kernel uses
-    // (bitwise independence of the tiling), so the real-dipole choice is global
-    if (qm < 0)
-        interior_cta<false, true>(P, t_lo, t_hi, base, re, rh);
-    else if (P.real_dipole)
-        P.n_qm == 1 ? interior_cta<true, true, true>(P, t_lo, t_hi, base, re, rh)
-                    : interior_cta<true, false, true>(P, t_lo, t_hi, base, re, rh);
-    else
-        P.n_qm == 1 ? interior_cta<true, true, false>(P, t_lo, t_hi, base, re, rh)
-                    : interior_cta<true, false, false>(P, t_lo, t_hi, base, re, rh);
+    interior_tile(P, launch_chunk(L), t_lo, t_hi, base);
 }
 
 // the few remaining cells (domain/window edges, region interfaces, sources),
 // one warp per result range of at most 32*C - 2k cells
 __global__ void __launch_bounds__(kEdgeWarps * 32)
 bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ EdgeTiles T) {
-    const Launch &L = P.L;
-    const int lane = threadIdx.x & 31;
     const int w = blockIdx.x * kEdgeWarps + (threadIdx.x >> 5);
     if (w >= T.n) return;
-    const long long t_lo = T.lo[w], t_hi = T.hi[w];
-    const long long base = tile_base(L, t_lo);
-    const long long lo = base, hi = base + W - 1 < L.num_x ? base + W - 1 : L.num_x - 1;
-    const bool uni = region_of(L.rg.e_start, L.rg.n, lo) == region_of(L.rg.e_start, L.rg.n, hi) &&
-                     region_of(L.rg.h_start, L.rg.n, lo < 1 ? 1 : lo) ==
-                         region_of(L.rg.h_start, L.rg.n, hi < 1 ? 1 : hi);
-    if (uni)
-        run_tile<true>(P, t_lo, t_hi, base, lane);
-    else
-        run_tile<false>(P, t_lo, t_hi, base, lane);
+    edge_range(P, launch_chunk(P.L), T.lo[w], T.hi[w], threadIdx.x & 31);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// record masks / scan flags of every step of a persistent launch, one thread
+// per step (the per-launch path computes them on the host: solver_fdtd.py:386-393)
+__global__ void wave_mask_kernel(const __grid_constant__ Launch L, long long n_steps, long long last_step,
+                                 unsigned long long *masks, unsigned char *checks) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n_steps) return;
+    const long long n = L.n0 + i;
+    unsigned long long m = 0;
+    for (int r = 0; r < L.n_rec; ++r)
+        if (n % L.rec_every[r] == 0) m |= 1ull << r;
+    masks[i] = m;
+    checks[i] = (n % 1024 == 0 || n == last_step) ? 1 : 0;
+}
+
+// item's dependencies: items t-1 .. t+1 of the previous chunk.  One pass
+// (three acquire loads in flight) or, with wait, spin until they are done.
+__device__ bool deps_done(const BlochWave &V, long long item, bool wait) {
+    const long long c = item / V.tiles, t = item - c * V.tiles;
+    if (c == 0) return true;
+    const unsigned *prev = V.done + (c - 1) * V.tiles;
+    const long long a = t > 0 ? t - 1 : t, b = t + 1 < V.tiles ? t + 1 : t;
+    unsigned long long deadline = 0;
+    for (;;) {
+        const unsigned fa = ld_acquire(prev + a), ft = ld_acquire(prev + t), fb = ld_acquire(prev + b);
+        if (fa && ft && fb) return true;
+        if (!wait) return false;
+        if (ld_acquire(V.stall)) return false;
+        const unsigned long long now = global_ns();
+        if (deadline == 0) {
+            deadline = now + 10000000000ull;
+        } else if (now > deadline) {
+            atomicExch(V.stall, 1u);
+            return false;
+        }
+        __nanosleep(100);
+    }
+}
+
+// Persistent wavefront kernel (see BlochWave).  A CTA claims its next item
+// when it starts the current one and checks the next item's dependencies
+// while its warps finish, so between two items there are only the two
+// barriers and the release.  Deadlock-free: an item only waits on items with
+// smaller tickets, every claimed ticket belongs to a resident CTA, and a CTA
+// releases its current item before it waits for its next one.  A wait longer
+// than 10 s (a bug, never the schedule) raises the stall flag and every CTA
+// drains without waiting.
+__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
+bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ BlochWave V) {
+    __shared__ unsigned item_s, next_s;
+    __shared__ unsigned long long mask_s[kMaxTileSteps];
+    __shared__ unsigned char check_s[kMaxTileSteps];
+    const Launch &L = P.L;
+    const long long items = (long long)V.n_chunks * V.tiles;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long warp_own = W - 2 * L.k;
+    if (threadIdx.x == 0) {
+        item_s = atomicAdd(V.ticket, 1u);
+        deps_done(V, item_s, true);
+    }
+    __syncthreads();
+    for (;;) {
+        const long long item = item_s;
+        if (item >= items) return;
+        if (V.trace && threadIdx.x == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            V.trace[4 * item] = V.trace[4 * item + 1] = global_ns();
+            V.trace[4 * item + 3] = sm | ((unsigned long long)blockIdx.x << 32);
+        }
+        const int c = (int)(item / V.tiles);
+        const long long t = item - (long long)c * V.tiles;
+        const long long k0 = (long long)c * L.k;
+        const int steps = c == V.n_chunks - 1 ? V.last_steps : L.k;
+        const int buf = (V.cur + c) & 1;
+        const Chunk K{V.e[buf],     V.h[buf],     V.s[buf], V.e[buf ^ 1], V.h[buf ^ 1],
+                      V.s[buf ^ 1], V.n0 + k0,    steps,    mask_s,       check_s};
+        // with the tile loads in flight: claim the next item, stage the masks
+        // (read after the first step's barriers)
+        const auto hook = [&]() {
+            if (threadIdx.x == 0) next_s = atomicAdd(V.ticket, 1u);
+            if (threadIdx.x < steps) {
+                mask_s[threadIdx.x] = V.masks[k0 + threadIdx.x];
+                check_s[threadIdx.x] = V.checks[k0 + threadIdx.x];
+            }
+        };
+        const WaveItem it = V.items[t];
+        if (!it.edge) {
+            interior_tile(P, K, it.lo, it.hi, tile_base(L, it.lo), hook);
+        } else {
+            hook();
+            __syncthreads();
+            const long long n_sub = (it.hi - it.lo + warp_own - 1) / warp_own;
+            for (long long u = warp; u < n_sub; u += kBlochWarpsPerBlock) {
+                const long long lo = it.lo + u * warp_own;
+                edge_range_call(P, K, lo, lo + warp_own < it.hi ? lo + warp_own : it.hi, lane);
+            }
+        }
+        const unsigned next = next_s;  // thread 0 wrote it before the tile's barriers
+        const bool ready = threadIdx.x == 0 && next < items ? deps_done(V, next, false) : true;
+        __syncthreads();  // every write of the item precedes the release; item_s may be reused
+        if (threadIdx.x == 0) {
+            if (V.trace) V.trace[4 * item + 2] = global_ns();
+            __threadfence();
+            st_release(V.done + item, 1u);
+            if (!ready) deps_done(V, next, true);
+            item_s = next;
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace
@@ -484,6 +670,27 @@ cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = cudaEventRecord(join, st_edge)) != cudaSuccess) return err;
     return cudaStreamWaitEvent(st, join, 0);
+}
+
+cudaError_t launch_wave_masks(const Launch &L, long long n_steps, long long last_step, unsigned long long *masks,
+                              unsigned char *checks, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((n_steps + 255) / 256);
+    wave_mask_kernel<<<blocks, 256, 0, st>>>(L, n_steps, last_step, masks, checks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bloch_wave(const BlochParams &P, const BlochWave &V, cudaStream_t st) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bloch_wave_kernel, kBlochWarpsPerBlock * 32, 0);
+    if (err != cudaSuccess) return err;
+    const long long items = (long long)V.n_chunks * V.tiles;
+    const long long slots = (long long)sms * (per_sm > 0 ? per_sm : 1);
+    const unsigned grid = (unsigned)(items < slots ? items : slots);
+    bloch_wave_kernel<<<grid, kBlochWarpsPerBlock * 32, 0, st>>>(P, V);
+    return cudaGetLastError();
 }
 
 }  // namespace MBG_VARIANT

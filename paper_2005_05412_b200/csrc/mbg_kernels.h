@@ -41,12 +41,49 @@ constexpr int kBlochCtaTile = kBlochWarpsPerBlock * kBlochTile;
 __host__ __device__ constexpr int dense_tile_width(int n, bool rk4) { return n <= 3 ? 256 : (n <= 6 ? 128 : 64); }
 __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <= 3 ? 2 : 1; }
 
+// One persistent launch of the two-level kernel over many fused chunks
+// (non-windowed solvers): work items (chunk c, tile t) are claimed in
+// chunk-major ticket order; item (c, t) waits until (c-1, t-1..t+1) are done,
+// so chunk c overlaps the tail of chunk c-1 and there is no launch gap or
+// wave-quantisation tail per chunk.  Chunk c reads buffer (cur + c) & 1 and
+// writes the other one.  Launch geometry (k, tile_own) is the one in P.L;
+// chunk c runs steps n0 + c*k .. (the last chunk may be shorter).
+// result range [lo, hi) of one work item: an interior CTA tile, or up to a
+// few warp ranges of a non-interior tile (split so that those slower general
+// path items do not become a serial chain through the wavefront); every item
+// but the last is at least k cells long, so item j only reads cells of the
+// previous chunk's items j-1 .. j+1
+struct WaveItem {
+    long long lo, hi;
+    int edge, pad;
+};
+
+struct BlochWave {
+    int n_chunks;
+    int last_steps;              // steps of the last chunk (<= P.L.k)
+    long long tiles;             // work items per chunk
+    const WaveItem *items;       // [tiles]
+    long long n0;                // first step of chunk 0
+    long long last_step;         // num_t - 1 (always scanned)
+    const unsigned long long *masks;  // [n_chunks * k] record masks of every step (wave_masks)
+    const unsigned char *checks;      // [n_chunks * k] non-finite scan flags
+    double *e[2], *h[2], *s[2];
+    int cur;                     // buffer holding the state at step n0 - 1
+    unsigned int *ticket;        // claim counter (zeroed before the launch)
+    unsigned int *done;          // [n_chunks * tiles] completion flags (zeroed)
+    unsigned int *stall;         // set if a dependency wait timed out
+    unsigned long long *trace;   // debug: per item {claimed, deps met, done, sm} ns (null: off)
+};
+
 #define MBG_DECLARE_LAUNCHERS(NS)                                                             \
     namespace NS {                                                                            \
     int bloch_cta_tile();                                                                     \
     cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,          \
                              cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join,         \
                              int *kernels);                                                    \
+    cudaError_t launch_bloch_wave(const BlochParams &P, const BlochWave &V, cudaStream_t st);     \
+    cudaError_t launch_wave_masks(const Launch &L, long long n_steps, long long last_step,          \
+                                  unsigned long long *masks, unsigned char *checks, cudaStream_t st); \
     cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \
     cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStream_t st);   \
     }

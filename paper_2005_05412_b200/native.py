@@ -21,6 +21,7 @@ LIB_PATH = Path(os.environ.get("MBGPU_LIB", PKG / "_build" / "libmbgpu.so"))
 HEADER = PKG.parent / "include" / "mbgpu.h"
 
 MBG_STEPPER = {"splitting": 0, "rk4": 1}
+MBG_FLAG_PER_LAUNCH = 1
 MAX_REGIONS, MAX_QM, MAX_SOURCES, MAX_RECORDS, MAX_LEVELS, MAX_TILE_STEPS = 128, 4, 32, 64, 8, 128
 
 
@@ -28,7 +29,7 @@ class MbgGrid(C.Structure):
     _fields_ = [
         ("num_x", C.c_int64), ("num_t", C.c_int64), ("dt", C.c_double), ("dx", C.c_double),
         ("levels", C.c_int32), ("stepper", C.c_int32), ("tile_steps", C.c_int32),
-        ("exact", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32),
+        ("exact", C.c_int32), ("device", C.c_int32), ("flags", C.c_int32),
         ("win_lo", C.c_int64), ("win_hi", C.c_int64), ("own_lo", C.c_int64), ("own_hi", C.c_int64),
     ]
 

@@ -43,11 +43,13 @@ class GpuFdtdSolver:
     Extra keyword arguments (all optional):
       ``tile_steps`` -- time steps fused per kernel launch (k; default per N),
       ``exact``      -- disable FMA contraction (bit-exact two-level path),
-      ``gpu``        -- CUDA device ordinal.
+      ``gpu``        -- CUDA device ordinal,
+      ``persistent`` -- two-level / classical runs: one persistent wavefront
+                        launch per advance (False: one launch per k steps).
     """
 
     def __init__(self, device, scenario, stepper="splitting", threads=None, seed=None,
-                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0):
+                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=True):
         self.plan = build_plan(device, scenario, stepper, seed)
         self.device = device
         self.scenario = scenario
@@ -60,6 +62,7 @@ class GpuFdtdSolver:
         self.tile_steps = tile_steps
         self.exact = bool(exact)
         self.gpu = int(gpu)
+        self.persistent = bool(persistent)
         self.results = None
         self.launches = 0
         self.kernel_ms = None
@@ -83,6 +86,7 @@ class GpuFdtdSolver:
         s.tile_steps = int(self.tile_steps or 0)
         s.exact = 1 if self.exact else 0
         s.device = self.gpu
+        s.flags = 0 if self.persistent else native.MBG_FLAG_PER_LAUNCH
         s.win_lo, s.win_hi = win if win is not None else (0, g.num_x)
         s.own_lo, s.own_hi = own if own is not None else (s.win_lo, s.win_hi)
         return s

@@ -75,6 +75,19 @@ def test_tile_depth_is_bitwise_invisible(name, k):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
 
 
+@pytest.mark.parametrize("k", [None, 1, 5, 64, 112])
+@pytest.mark.parametrize("name", ["sit_hard_whole", "multi_material", "vacuum_sources", "bragg_stack", "cfg2_r16"])
+def test_persistent_wavefront_matches_per_launch(name, k):
+    """The persistent kernel (one launch, chunk-major work items waiting on
+    their neighbours of the previous chunk) against one launch per k steps."""
+    _, ref = _run(name, tile_steps=k, persistent=False)
+    mb.clear_material_library()
+    solver, got = _run(name, tile_steps=k)
+    assert solver.launches < solver.grid.num_t // 2
+    for a, b in zip(ref, got):
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
+
+
 @pytest.mark.parametrize("name,k", [("rand3_split", 5), ("rand6_split", 3), ("rand4_rk4", 6), ("cfg4_r14", 7)])
 def test_tile_depth_dense_kernels(name, k):
     _, ref = _run(name, tile_steps=1)

@@ -23,6 +23,7 @@ ap.add_argument("--tile-steps", type=int, default=None)
 ap.add_argument("--exact", action="store_true")
 ap.add_argument("--stepper", default="splitting")
 ap.add_argument("--nx", type=int, default=0)
+ap.add_argument("--per-launch", action="store_true", help="one launch per k steps (no persistent kernel)")
 ap.add_argument("--no-warm", action="store_true", help="single pass (for ncu)")
 a = ap.parse_args()
 kw = {"nx": a.nx} if a.nx else {}
@@ -31,7 +32,8 @@ if a.config == "cfg5":
     dev, sce = configs.cfg5(mb, steps=total)
 else:
     dev, sce = getattr(configs, a.config)(mb, **kw, **({"steps": total} if a.config != "cfg1" else {}))
-sol = mb.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact)
+sol = mb.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact,
+                       persistent=not a.per_launch)
 h = sol.open_handle()
 sol.upload_initial_state(h)
 k = C.c_int32(0)
