@@ -57,6 +57,8 @@ struct mbg_solver {
     int cur = 0;
     Regions rg{};
     bool have_regions = false;
+    bool state_set = false;  // the density state was uploaded (or mapped into the frame)
+    bool frame_on = false;   // the device state is in the relaxed frame (BlochFrame)
     std::vector<QmHost> qm;
     bool has_boundary = false;
     double bnd[6] = {};
@@ -91,7 +93,7 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
     } while (0)
 
 int default_tile_steps(int levels, int stepper) {
-    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 64;
+    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 80;
     if (levels <= 3) return 16;
     return 4;
 }
@@ -214,6 +216,39 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
     return cudaErrorInvalidValue;
 }
 
+// _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
+bool real_dipole(const BlochQm &b) {
+    return b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 && b.a0_s == 0.0 && b.mu_y == 0.0 &&
+           b.mu_z == 0.0;
+}
+
+// the fast two-level path keeps its state in the relaxed frame when every
+// medium has a real dipole and invertible half-step relaxation factors
+BlochFrame frame_of(const mbg_solver *s) {
+    BlochFrame F;
+    std::memset(&F, 0, sizeof(F));
+    if (s->g.exact || !(s->bloch || s->g.levels == 0) || s->qm.empty() || (int)s->qm.size() > kMaxQm) return F;
+    for (size_t q = 0; q < s->qm.size(); ++q) {
+        BlochQm b;
+        std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
+        if (!real_dipole(b) || !(b.fxy >= 1e-150) || !(b.kz >= 1e-150) || !std::isfinite(b.fxy) ||
+            !std::isfinite(b.kz) || !std::isfinite(b.cz))
+            return F;
+        F.fxy[q] = b.fxy;
+        F.kz[q] = b.kz;
+        F.cz[q] = b.cz;
+    }
+    F.on = 1;
+    return F;
+}
+
+// the frame the device state is in right now
+BlochFrame state_frame(const mbg_solver *s) {
+    BlochFrame F = frame_of(s);
+    F.on = s->frame_on ? 1 : 0;
+    return F;
+}
+
 BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
     BlochParams P;
     std::memset(&P, 0, sizeof(P));
@@ -223,13 +258,14 @@ BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
     for (int q = 0; q < P.n_qm; ++q) {
         BlochQm &b = P.qm[q];
         std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
-        // _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
-        const bool real = b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 && b.a0_s == 0.0 &&
-                          b.mu_y == 0.0 && b.mu_z == 0.0;
-        P.real_dipole &= real ? 1 : 0;
+        P.real_dipole &= real_dipole(b) ? 1 : 0;
         const double u = b.a0_c * b.a0_c;
-        P.rq[q] = BlochReal{u, 1.0 + u, 4.0 * u, b.az_c * b.az_c, 1.0 - u, b.pol_factor * b.mu_x};
+        P.rq[q] = BlochReal{u,           1.0 + u,         4.0 * u,         b.az_c * b.az_c,     1.0 - u,
+                            b.pol_factor * b.mu_x * b.fxy, b.fxy * b.fxy, b.kz * b.kz, b.kz * b.cz + b.cz};
     }
+    // the fast variant's real-dipole cell function works in the relaxed frame
+    P.frame = state_frame(s);
+    if (!s->g.exact && !P.frame.on) P.real_dipole = 0;
     return P;
 }
 
@@ -282,6 +318,9 @@ bool window_ok(const mbg_grid *g) {
 }  // namespace
 
 extern "C" {
+
+static int sync_frame(mbg_solver *s);
+
 
 const char *mbg_version(void) { return "mbgpu 0.1 (sm_100a)"; }
 
@@ -590,6 +629,8 @@ int mbg_upload_density(mbg_solver *s, const double *words) {
     CK(cudaMemcpyAsync(w, words, sizeof(double) * s->words, cudaMemcpyHostToDevice, s->stream));
     CK(launch_broadcast_state(s->s[s->cur], s->plane, s->win_n, s->words, w, s->rg, s->g.win_lo, s->stream));
     dfree(s->stream, w);
+    s->state_set = false;
+    if (int rc = sync_frame(s)) return rc;
     CK(cudaStreamSynchronize(s->stream));
     return MBG_OK;
 }
@@ -600,6 +641,9 @@ int mbg_upload_state(mbg_solver *s, const double *planes) {
     for (int w = 0; w < s->words; ++w)
         CK(cudaMemcpyAsync(s->s[s->cur] + w * s->plane, planes + w * s->win_n, sizeof(double) * s->win_n,
                            cudaMemcpyHostToDevice, s->stream));
+    s->state_set = false;
+    if (s->have_regions)
+        if (int rc = sync_frame(s)) return rc;
     CK(cudaStreamSynchronize(s->stream));
     return MBG_OK;
 }
@@ -616,6 +660,16 @@ int mbg_download_fields(mbg_solver *s, double *e, double *h) {
 int mbg_download_state(mbg_solver *s, double *planes) {
     if (!s || !planes) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
+    if (s->frame_on) {  // true values out of the relaxed frame
+        double *t = nullptr;
+        const size_t bytes = sizeof(double) * s->words * s->win_n;
+        CK(dalloc(s->stream, &t, bytes));
+        CK(launch_frame(false, s->s[s->cur], s->plane, s->win_n, s->rg, s->g.win_lo, state_frame(s), t, s->stream));
+        CK(cudaMemcpyAsync(planes, t, bytes, cudaMemcpyDeviceToHost, s->stream));
+        dfree(s->stream, t);
+        CK(cudaStreamSynchronize(s->stream));
+        return MBG_OK;
+    }
     for (int w = 0; w < s->words; ++w)
         CK(cudaMemcpyAsync(planes + w * s->win_n, s->s[s->cur] + w * s->plane, sizeof(double) * s->win_n,
                            cudaMemcpyDeviceToHost, s->stream));
@@ -627,9 +681,27 @@ int mbg_sample(mbg_solver *s, int64_t step) {
     if (!s) return MBG_E_ARG;
     if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
     cudaSetDevice(s->g.device);
+    if (int rc = sync_frame(s)) return rc;
     const Launch L = base_launch(s);
-    CK(launch_sample(L, s->g.levels, s->bloch ? 1 : 0, step, s->stream));
+    CK(launch_sample(L, s->g.levels, s->bloch ? 1 : 0, step, state_frame(s), s->stream));
     ++s->launches;
+    return MBG_OK;
+}
+
+// Map the device state into the relaxed frame if the medium calls for it and
+// nothing was uploaded yet (a zero state); afterwards the medium may not
+// change the frame (the stored words would be misread).
+static int sync_frame(mbg_solver *s) {
+    if (!s->have_regions || s->words == 0) return MBG_OK;
+    const BlochFrame F = frame_of(s);
+    if (!s->state_set) {
+        if (F.on)
+            CK(launch_frame(true, s->s[s->cur], s->plane, s->win_n, s->rg, s->g.win_lo, F, nullptr, s->stream));
+        s->frame_on = F.on != 0;
+        s->state_set = true;
+    } else if ((F.on != 0) != s->frame_on) {
+        return fail(s, MBG_E_STATE, "quantum constants changed after the density state was uploaded");
+    }
     return MBG_OK;
 }
 
@@ -649,7 +721,7 @@ static int check_ready(mbg_solver *s) {
         const bool ok = s->bloch ? (!h.dense && !h.rk4) : (s->g.stepper == MBG_STEPPER_RK4 ? h.rk4 : h.dense);
         if (!ok) return fail(s, MBG_E_STATE, "quantum constants do not match the stepper");
     }
-    return MBG_OK;
+    return sync_frame(s);
 }
 
 }  // extern "C"
@@ -848,7 +920,8 @@ int mbg_invariants(mbg_solver *s, double *out) {
     CK(dalloc(s->stream, reinterpret_cast<double **>(&d), sizeof(init)));
     CK(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
     const Launch L = base_launch(s);
-    if (s->words > 0) CK(launch_invariants(L, s->g.levels, s->bloch ? 1 : 0, d, s->stream));
+    if (int rc = sync_frame(s)) return rc;
+    if (s->words > 0) CK(launch_invariants(L, s->g.levels, s->bloch ? 1 : 0, state_frame(s), d, s->stream));
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
     dfree(s->stream, d);

@@ -18,8 +18,30 @@ __global__ void broadcast_state_kernel(double *s, long long plane, long long win
     for (int k = 0; k < words; ++k) s[k * plane + l] = qm ? w[k] : 0.0;
 }
 
+// relaxed-frame state (BlochFrame): map an uploaded true state in (to_frame)
+// or the device state out into `out` (true values) for a download
+__global__ void frame_kernel(bool to_frame, double *s, long long plane, long long win_n, const Regions rg,
+                             long long win_lo, const BlochFrame F, double *out) {
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= win_n) return;
+    const int q = rg.qm[region_of(rg.e_start, rg.n, win_lo + l)];
+    double *x = s + l, *y = s + plane + l, *z = s + 2 * plane + l;
+    if (to_frame) {
+        if (q < 0) return;
+        *x = *x / F.fxy[q];
+        *y = *y / F.fxy[q];
+        *z = (*z - F.cz[q]) / F.kz[q];
+    } else {
+        double a, b, c;
+        frame_true(F, q, *x, *y, *z, a, b, c);
+        out[l] = a;
+        out[win_n + l] = b;
+        out[2 * win_n + l] = c;
+    }
+}
+
 // _sample(step) from the current state (used for row 0, solver_fdtd.py:449)
-__global__ void sample_kernel(const Launch L, int levels, int bloch, long long step) {
+__global__ void sample_kernel(const Launch L, int levels, int bloch, long long step, const BlochFrame F) {
     const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= L.win_n) return;
     const long long c = L.win_lo + l;
@@ -40,7 +62,8 @@ __global__ void sample_kernel(const Launch L, int levels, int bloch, long long s
             const double *s = L.s_in + l;
             const long long P = L.plane;
             if (bloch) {
-                const double x = s[0], y = s[P], z = s[2 * P];
+                double x, y, z;
+                frame_true(F, qm, s[0], s[P], s[2 * P], x, y, z);
                 if (q == MBG_Q_INV) {
                     re = -z;
                 } else {
@@ -152,18 +175,21 @@ __device__ double min_eigenvalue(const double *re, const double *im, int n) {
     return mn;
 }
 
-__global__ void invariants_kernel(const Launch L, int levels, int bloch, unsigned long long *out) {
+__global__ void invariants_kernel(const Launch L, int levels, int bloch, const BlochFrame F,
+                                  unsigned long long *out) {
     const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= L.win_n) return;
     const long long c = L.win_lo + l;
     if (c < L.own_lo || c >= L.own_hi) return;
-    if (L.rg.qm[region_of(L.rg.e_start, L.rg.n, c)] < 0) return;
+    const int qm = L.rg.qm[region_of(L.rg.e_start, L.rg.n, c)];
+    if (qm < 0) return;
     const double *s = L.s_in + l;
     const long long P = L.plane;
     double trace_dev = 0.0, min_eig;
     if (bloch) {
         // eigenvalues (1 +- |v|)/2; trace and Hermiticity exact in this form
-        const double x = s[0], y = s[P], z = s[2 * P];
+        double x, y, z;
+        frame_true(F, qm, s[0], s[P], s[2 * P], x, y, z);
         min_eig = 0.5 * (1.0 - sqrt(x * x + y * y + z * z));
     } else {
         const int n = levels;
@@ -221,15 +247,24 @@ cudaError_t measure_fp64_peak(double *ms, double *flops) {
     return err;
 }
 
-cudaError_t launch_invariants(const Launch &L, int levels, int bloch, unsigned long long *out, cudaStream_t st) {
-    if (L.win_n <= 0) return cudaSuccess;
-    invariants_kernel<<<blocks_for(L.win_n, 128), 128, 0, st>>>(L, levels, bloch, out);
+cudaError_t launch_frame(bool to_frame, double *s, long long plane, long long win_n, const Regions &rg,
+                         long long win_lo, const BlochFrame &F, double *out, cudaStream_t st) {
+    if (win_n <= 0) return cudaSuccess;
+    frame_kernel<<<blocks_for(win_n, 256), 256, 0, st>>>(to_frame, s, plane, win_n, rg, win_lo, F, out);
     return cudaGetLastError();
 }
 
-cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, cudaStream_t st) {
+cudaError_t launch_invariants(const Launch &L, int levels, int bloch, const BlochFrame &F, unsigned long long *out,
+                              cudaStream_t st) {
     if (L.win_n <= 0) return cudaSuccess;
-    sample_kernel<<<blocks_for(L.win_n, 256), 256, 0, st>>>(L, levels, bloch, step);
+    invariants_kernel<<<blocks_for(L.win_n, 128), 128, 0, st>>>(L, levels, bloch, F, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, const BlochFrame &F,
+                          cudaStream_t st) {
+    if (L.win_n <= 0) return cudaSuccess;
+    sample_kernel<<<blocks_for(L.win_n, 256), 256, 0, st>>>(L, levels, bloch, step, F);
     return cudaGetLastError();
 }
 

@@ -115,14 +115,15 @@ __device__ __forceinline__ double rcp_ge1(double d) {
     return fma(r, fma(e, e, e), r);
 }
 
-// fast variant of bloch_cell_real: the same rotation regrouped around the
-// field-independent products g*az and 8/den (tolerance-level, not bitwise).
-// Returns x - x0: the factor pol_factor*mu_x is folded into the E update's
-// coefficient (pol_coef)
-__device__ __forceinline__ double bloch_cell_real_fast(const BlochQm &q, const BlochReal &r, double e, double &x,
-                                                       double &y, double &z) {
-    const double x0 = x, y0 = y, z0 = z;
-    const double x1 = q.fxy * x0, y1 = q.fxy * y0, z1 = fma(q.kz, z0, q.cz);
+// Fast variant of bloch_cell_real on the relaxed-frame state (BlochFrame):
+// the two half relaxations of consecutive steps are one multiply (one FMA for
+// z), the rotation is regrouped around the field-independent products g*az
+// and 8/den (tolerance-level, not bitwise).  Returns X_new - X_old: the factor
+// pol_factor * mu_x * fxy is folded into the E update's coefficient (pol_coef).
+__device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const BlochReal &r, double e, double &x,
+                                                        double &y, double &z) {
+    const double x0 = x;
+    const double x1 = r.f2 * x, y1 = r.f2 * y, z1 = fma(r.kz2, z, r.czz);
     const double ax = q.ax_s * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
     const double num = r.c1 - qq;
@@ -132,15 +133,12 @@ __device__ __forceinline__ double bloch_cell_real_fast(const BlochQm &q, const B
     const double g = num * (4.0 * inv);
     const double gaz = g * az, gax = g * ax;
     const double dotb = (8.0 * inv) * fma(az, z1, ax * x1);
-    const double x2 = fma(dotb, ax, fma(-gaz, y1, k1 * x1));
-    const double y2 = fma(-gax, z1, fma(gaz, x1, k1 * y1));
-    const double z2 = fma(dotb, az, fma(gax, y1, k1 * z1));
-    x = q.fxy * x2;
-    y = q.fxy * y2;
-    z = fma(q.kz, z2, q.cz);
+    x = fma(dotb, ax, fma(-gaz, y1, k1 * x1));
+    y = fma(-gax, z1, fma(gaz, x1, k1 * y1));
+    z = fma(dotb, az, fma(gax, y1, k1 * z1));
     return x - x0;
 }
-#define MBG_BLOCH_REAL bloch_cell_real_fast
+#define MBG_BLOCH_REAL bloch_cell_real_frame
 #define MBG_POL_FOLD 1
 #else
 #define MBG_BLOCH_REAL bloch_cell_real
@@ -302,10 +300,15 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                         case MBG_Q_E: vre = E[i]; break;
                         case MBG_Q_H: vre = H[i]; break;
                         case MBG_Q_D:
-                            if (qi[i] >= 0) bloch_entry(L.rec_i[r], L.rec_j[r], X[i], Y[i], Z[i], vre, vim);
-                            break;
                         default:
-                            if (qi[i] >= 0) vre = -Z[i];
+                            if (qi[i] >= 0) {
+                                double x, y, z;
+                                frame_true(P.frame, qi[i], X[i], Y[i], Z[i], x, y, z);
+                                if (L.rec_q[r] == MBG_Q_D)
+                                    bloch_entry(L.rec_i[r], L.rec_j[r], x, y, z, vre, vim);
+                                else
+                                    vre = -z;
+                            }
                     }
                     L.rec_re[r][idx] = vre;
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
@@ -409,10 +412,15 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                         case MBG_Q_E: vre = E[i]; break;
                         case MBG_Q_H: vre = H[i]; break;
                         case MBG_Q_D:
-                            if (QM) bloch_entry(L.rec_i[r], L.rec_j[r], X[i], Y[i], Z[i], vre, vim);
-                            break;
                         default:
-                            if (QM) vre = -Z[i];
+                            if (QM) {
+                                double x, y, z;
+                                frame_true(P.frame, qmi, X[i], Y[i], Z[i], x, y, z);
+                                if (L.rec_q[r] == MBG_Q_D)
+                                    bloch_entry(L.rec_i[r], L.rec_j[r], x, y, z, vre, vim);
+                                else
+                                    vre = -z;
+                            }
                     }
                     L.rec_re[r][idx] = vre;
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;

@@ -92,7 +92,11 @@ MBG_DECLARE_LAUNCHERS(fast)
 MBG_DECLARE_LAUNCHERS(exact)
 
 // auxiliary kernels (variant independent)
-cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, cudaStream_t st);
+cudaError_t launch_sample(const Launch &L, int levels, int bloch, long long step, const BlochFrame &F,
+                          cudaStream_t st);
+// relaxed-frame state: in place to the frame (to_frame), or out of it into `out`
+cudaError_t launch_frame(bool to_frame, double *s, long long plane, long long win_n, const Regions &rg,
+                         long long win_lo, const BlochFrame &F, double *out, cudaStream_t st);
 cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, int words,
                                    const double *words_dev, const Regions &rg, long long win_lo,
                                    cudaStream_t st);
@@ -101,7 +105,8 @@ cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long pl
 
 // invariant monitor: out[0] max |trace - 1|, out[1] max Hermiticity deviation
 // (0: packed storage), out[2] min eigenvalue, as order-preserving uint64 keys
-cudaError_t launch_invariants(const Launch &L, int levels, int bloch, unsigned long long *out, cudaStream_t st);
+cudaError_t launch_invariants(const Launch &L, int levels, int bloch, const BlochFrame &F, unsigned long long *out,
+                              cudaStream_t st);
 
 // FP64 roofline denominator: best-of-5 DFMA throughput (ms of the best launch, flops per launch)
 cudaError_t measure_fp64_peak(double *ms, double *flops);

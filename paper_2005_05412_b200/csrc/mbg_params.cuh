@@ -82,13 +82,42 @@ struct BlochReal {
     double c4u;   // 4.0 * u
     double az2;   // az_c * az_c
     double c2;    // 1.0 - u          (fast variant)
-    double pfmu;  // pol_factor * mu_x (fast variant)
+    double pfmu;  // pol_factor * mu_x * fxy (fast variant, relaxed-frame state)
+    double f2;    // fxy * fxy
+    double kz2;   // kz * kz
+    double czz;   // kz * cz + cz
 };
+
+// Relaxed-frame state of the fast two-level path: the device holds each
+// Bloch vector after the Cayley rotation and before the second half
+// relaxation, (X, Y, Z) with x = fxy X, y = fxy Y, z = kz Z + cz.  Then one
+// step's two half relaxations fold into one (x1 = fxy^2 X, z1 = kz^2 Z + kz cz
+// + cz), three operations fewer per cell and step.  Every reader of the state
+// (records, sample, invariants, download) maps back with frame_true; uploads
+// map in with frame_in.
+struct BlochFrame {
+    int on;
+    double fxy[kMaxQm], kz[kMaxQm], cz[kMaxQm];
+};
+
+__host__ __device__ inline void frame_true(const BlochFrame &F, int q, double X, double Y, double Z, double &x,
+                                           double &y, double &z) {
+    if (F.on && q >= 0) {
+        x = F.fxy[q] * X;
+        y = F.fxy[q] * Y;
+        z = fma(F.kz[q], Z, F.cz[q]);
+    } else {
+        x = X;
+        y = Y;
+        z = Z;
+    }
+}
 
 struct BlochParams {
     Launch L;
     int n_qm;
-    int real_dipole;  // all materials satisfy the BlochReal pattern
+    int real_dipole;  // all materials satisfy the BlochReal pattern (fast variant: and the frame applies)
+    BlochFrame frame; // fast variant with real_dipole: the state is in the relaxed frame
     BlochQm qm[kMaxQm];
     BlochReal rq[kMaxQm];
 };
