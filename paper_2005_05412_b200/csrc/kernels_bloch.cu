@@ -577,13 +577,32 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
     __shared__ unsigned item_s, next_s;
     __shared__ unsigned long long mask_s[kMaxTileSteps];
     __shared__ unsigned char check_s[kMaxTileSteps];
+    // the current item's chunk and range live in shared memory: the tile code
+    // reads them where it needs them instead of holding them in registers
+    // across the step loop (the per-launch kernels read the same from the
+    // parameter bank)
+    __shared__ Chunk chunk_s;
+    __shared__ WaveItem item_range_s;
     const Launch &L = P.L;
     const long long items = (long long)V.n_chunks * V.tiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long warp_own = W - 2 * L.k;
+    // thread 0: publish item `item` (chunk pointers, step range, cell range)
+    const auto stage = [&](unsigned item) {
+        item_s = item;
+        if (item >= items) return;
+        const int c = (int)(item / V.tiles);
+        const long long t = item - (long long)c * V.tiles;
+        const int buf = (V.cur + c) & 1;
+        chunk_s = Chunk{V.e[buf],     V.h[buf],  V.s[buf], V.e[buf ^ 1], V.h[buf ^ 1],
+                        V.s[buf ^ 1], V.n0 + (long long)c * L.k,
+                        c == V.n_chunks - 1 ? V.last_steps : L.k, mask_s, check_s};
+        item_range_s = V.items[t];
+    };
     if (threadIdx.x == 0) {
-        item_s = atomicAdd(V.ticket, 1u);
-        deps_done(V, item_s, true);
+        const unsigned first = atomicAdd(V.ticket, 1u);
+        deps_done(V, first, true);
+        stage(first);
     }
     __syncthreads();
     for (;;) {
@@ -595,43 +614,41 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
             V.trace[4 * item] = V.trace[4 * item + 1] = global_ns();
             V.trace[4 * item + 3] = sm | ((unsigned long long)blockIdx.x << 32);
         }
-        const int c = (int)(item / V.tiles);
-        const long long t = item - (long long)c * V.tiles;
-        const long long k0 = (long long)c * L.k;
-        const int steps = c == V.n_chunks - 1 ? V.last_steps : L.k;
-        const int buf = (V.cur + c) & 1;
-        const Chunk K{V.e[buf],     V.h[buf],     V.s[buf], V.e[buf ^ 1], V.h[buf ^ 1],
-                      V.s[buf ^ 1], V.n0 + k0,    steps,    mask_s,       check_s};
+        const Chunk &K = chunk_s;
         // with the tile loads in flight: claim the next item, stage the masks
         // (read after the first step's barriers)
         const auto hook = [&]() {
             if (threadIdx.x == 0) next_s = atomicAdd(V.ticket, 1u);
-            if (threadIdx.x < steps) {
+            const long long k0 = K.n0 - V.n0;
+            if (threadIdx.x < K.steps) {
                 mask_s[threadIdx.x] = V.masks[k0 + threadIdx.x];
                 check_s[threadIdx.x] = V.checks[k0 + threadIdx.x];
             }
         };
-        const WaveItem it = V.items[t];
-        if (!it.edge) {
-            interior_tile(P, K, it.lo, it.hi, tile_base(L, it.lo), hook);
+        const long long lo = item_range_s.lo, hi = item_range_s.hi;
+        if (!item_range_s.edge) {
+            interior_tile(P, K, lo, hi, tile_base(L, lo), hook);
         } else {
             hook();
             __syncthreads();
-            const long long n_sub = (it.hi - it.lo + warp_own - 1) / warp_own;
+            const long long n_sub = (hi - lo + warp_own - 1) / warp_own;
             for (long long u = warp; u < n_sub; u += kBlochWarpsPerBlock) {
-                const long long lo = it.lo + u * warp_own;
-                edge_range_call(P, K, lo, lo + warp_own < it.hi ? lo + warp_own : it.hi, lane);
+                const long long sub = lo + u * warp_own;
+                edge_range_call(P, K, sub, sub + warp_own < hi ? sub + warp_own : hi, lane);
             }
         }
-        const unsigned next = next_s;  // thread 0 wrote it before the tile's barriers
+        // item and next come back from shared memory (nothing stays live in
+        // registers across the tile); thread 0 wrote next_s before the tile's barriers
+        const unsigned next = next_s;
         const bool ready = threadIdx.x == 0 && next < items ? deps_done(V, next, false) : true;
         __syncthreads();  // every write of the item precedes the release; item_s may be reused
         if (threadIdx.x == 0) {
-            if (V.trace) V.trace[4 * item + 2] = global_ns();
+            const unsigned done_item = item_s;
+            if (V.trace) V.trace[4 * done_item + 2] = global_ns();
             __threadfence();
-            st_release(V.done + item, 1u);
+            st_release(V.done + done_item, 1u);
             if (!ready) deps_done(V, next, true);
-            item_s = next;
+            stage(next);
         }
         __syncthreads();
     }
