@@ -204,6 +204,9 @@ def workload_config(plan, args, k):
 
 # ------------------------------------------------------------------- mine --
 
+MARK_STEPS = 31  # per-step advance timing marks (mbg_mark slots 2..63)
+
+
 def run_mine(args, world, rank, local):
     import ctypes as C
 
@@ -226,10 +229,14 @@ def run_mine(args, world, rank, local):
     h.call("mbg_tile_steps", C.byref(k))
     k = k.value
 
-    def one_step():
+    def one_step(i=None):
         h.call("mbg_checkpoint_restore")
         h.call("mbg_sample", 0)
+        if i is not None and i < MARK_STEPS:
+            h.call("mbg_mark", 2 + 2 * i)
         h.call("mbg_advance", 1, num_t - 1)
+        if i is not None and i < MARK_STEPS:
+            h.call("mbg_mark", 3 + 2 * i)
 
     for _ in range(args.warmup):
         one_step()
@@ -237,12 +244,20 @@ def run_mine(args, world, rank, local):
     l0 = C.c_int64(0)
     h.call("mbg_launch_count", C.byref(l0))
     with ClockSampler(local) as clocks:
-        h.call("mbg_event_begin")
-        for _ in range(args.steps):
-            one_step()
+        h.call("mbg_mark", 0)
+        for i in range(args.steps):
+            one_step(i)
+        h.call("mbg_mark", 1)
         ms = C.c_float(0)
-        h.call("mbg_event_end", C.byref(ms))
+        h.call("mbg_mark_elapsed", 0, 1, C.byref(ms))
     ms = float(ms.value)
+    # device time of the step launches alone (mbg_advance: the persistent
+    # step kernel and its step-mask pre-kernel), from marks on the same stream
+    adv_ms = []
+    for i in range(min(args.steps, MARK_STEPS)):
+        t = C.c_float(0)
+        h.call("mbg_mark_elapsed", 2 + 2 * i, 3 + 2 * i, C.byref(t))
+        adv_ms.append(float(t.value))
     l1 = C.c_int64(0)
     h.call("mbg_launch_count", C.byref(l1))
     launches = l1.value - l0.value
@@ -254,19 +269,19 @@ def run_mine(args, world, rank, local):
     cell_updates = nx * (num_t - 1) * args.steps
     value = cell_updates / (ms * 1e-3)
 
-    # roofline of the fused step kernel (dominant: it is every launch but the row-0 sample)
+    # roofline of the dominant kernel: one persistent launch per run (two-level
+    # medium, one GPU) working through ceil((Nt-1)/k) fused chunks
     b, f, fq = algorithmic_per_cell(plan)
     peak_fp64 = C.c_double(0)
     native.load().mbg_fp64_peak(local, C.byref(peak_fp64))
     peak_fp64 = peak_fp64.value
     bw, bw_src = measured_hbm_gbs()
-    # the dominant kernel runs once per fused chunk of k steps (its edge-tile
-    # companion overlaps it on a side stream)
-    chunks = args.steps * ((num_t - 1 + k - 1) // k)
-    per_launch_ms = ms / chunks
-    cells_per_launch = cell_updates / chunks  # = nx * k
+    persistent = plan.levels <= 2 and solver.stepper == "splitting" and num_t - 1 > k
+    chunks = (num_t - 1 + k - 1) // k
+    per_launch_ms = sum(adv_ms) / len(adv_ms)
+    cells_per_launch = nx * (num_t - 1)
     flops_launch = f * cells_per_launch
-    bytes_launch = b * nx
+    bytes_launch = b * nx * chunks  # E, H and the state read + written once per fused chunk
     t_hbm = bytes_launch / (bw * 1e9)
     t_fp = flops_launch / (peak_fp64 * 1e12)
     bound = "fp64" if t_fp >= t_hbm else "hbm"
@@ -277,14 +292,16 @@ def run_mine(args, world, rank, local):
     else:
         achieved = bytes_launch / (per_launch_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": bw, "unit": "GB/s", "frac": achieved / bw}
-    traffic = ncu_traffic(f"cfg2_k{k}")
+    traffic = ncu_traffic(f"cfg2_wave_k{k}" if persistent else f"cfg2_k{k}")
     roof.update({
         "traffic": traffic,
-        "kernel": "bloch_interior_kernel (fused H + Bloch + E + records, k steps/launch; edge tiles overlap "
-                  "on a side stream)",
+        "kernel": ("bloch_wave_kernel (one persistent launch per run: ticketed (chunk, tile) items of k fused "
+                   "steps, H + Bloch + E + boundary + sources + records)" if persistent else
+                   "bloch_interior_kernel (fused H + Bloch + E + records, k steps/launch)"),
         "algorithmic_bytes_per_cell_update_k1": b, "algorithmic_flops_per_cell_update": f,
-        "bytes_per_launch": bytes_launch, "flops_per_launch": flops_launch,
-        "launch_ms_avg": per_launch_ms, "hbm_achieved_gbs": bytes_launch / (per_launch_ms * 1e-3) / 1e9,
+        "bytes_per_launch": bytes_launch, "flops_per_launch": flops_launch, "fused_chunks_per_launch": chunks,
+        "launch_ms_avg": per_launch_ms, "launch_share_of_step": sum(adv_ms) / (ms * len(adv_ms) / args.steps),
+        "hbm_achieved_gbs": bytes_launch / (per_launch_ms * 1e-3) / 1e9,
         "hbm_peak_gbs": bw, "hbm_peak_source": bw_src, "fp64_peak_tflops": peak_fp64,
         "fp64_peak_source": "measured in-run (mbg_fp64_peak: DFMA chains on all SMs)",
         "roofline_cell_updates_per_s": min(bw * 1e9 * k / b, peak_fp64 * 1e12 / f),
@@ -310,7 +327,7 @@ def run_mine(args, world, rank, local):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline(plan, args.cpu_steps)
+        cpu = cpu_baseline(plan, 3 * args.cpu_steps)  # ~10 s of host work
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
@@ -318,7 +335,7 @@ def run_mine(args, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(plan, args, k),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches),  # fused step + edge-tile + row-0 sample kernels (library count)
+        "gpu_launches": int(launches),  # persistent step + step-mask + row-0 sample kernels (library count)
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
@@ -352,7 +369,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=("mine", "reference"), default="mine")
     ap.add_argument("--tile-steps", type=int, default=None)
     ap.add_argument("--exact", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=300)
+    ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)
     world, rank, local = dist_env()

@@ -156,6 +156,12 @@ int mbg_fp64_peak(int device, double *tflops);
  * mbg_advance between mark_begin/mark_end (CUDA events on the solver stream) */
 int mbg_event_begin(mbg_solver *s);
 int mbg_event_end(mbg_solver *s, float *ms);
+/* numbered events on the solver stream (slot < MBG_MAX_MARKS) for timing a
+ * part of a timed region without synchronising inside it; mbg_mark_elapsed
+ * waits for mark b and returns the device time from mark a to mark b */
+#define MBG_MAX_MARKS 64
+int mbg_mark(mbg_solver *s, int32_t slot);
+int mbg_mark_elapsed(mbg_solver *s, int32_t a, int32_t b, float *ms);
 /* kernels this handle has launched so far (step, edge, sample and halo kernels) */
 int mbg_launch_count(const mbg_solver *s, int64_t *launches);
 

@@ -70,6 +70,7 @@ struct mbg_solver {
     unsigned long long *bad = nullptr;
     double *ck_e = nullptr, *ck_h = nullptr, *ck_s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t marks[MBG_MAX_MARKS] = {};
     unsigned *wave = nullptr;  // persistent launch: [0] ticket, [1] stall, [2..] done flags
     long long wave_cap = 0;
     WaveItem *wave_items = nullptr;  // work items of one chunk (fixed per solver)
@@ -415,6 +416,8 @@ void mbg_destroy(mbg_solver *s) {
     if (st) cudaStreamSynchronize(st);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
+    for (cudaEvent_t e : s->marks)
+        if (e) cudaEventDestroy(e);
     if (s->side) {
         cudaStreamSynchronize(s->side);
         cudaStreamDestroy(s->side);
@@ -826,7 +829,7 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
             std::fclose(f);
         }
     }
-    s->launches += 1;
+    s->launches += 2;  // step-mask pre-kernel + persistent step kernel
     if (n_chunks & 1) s->cur ^= 1;
     return MBG_OK;
 }
@@ -1022,6 +1025,23 @@ int mbg_event_end(mbg_solver *s, float *ms) {
     CK(cudaEventRecord(s->ev1, s->stream));
     CK(cudaEventSynchronize(s->ev1));
     CK(cudaEventElapsedTime(ms, s->ev0, s->ev1));
+    return MBG_OK;
+}
+
+int mbg_mark(mbg_solver *s, int32_t slot) {
+    if (!s || slot < 0 || slot >= MBG_MAX_MARKS) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    if (!s->marks[slot]) CK(cudaEventCreate(&s->marks[slot]));
+    CK(cudaEventRecord(s->marks[slot], s->stream));
+    return MBG_OK;
+}
+
+int mbg_mark_elapsed(mbg_solver *s, int32_t a, int32_t b, float *ms) {
+    if (!s || !ms || a < 0 || b < 0 || a >= MBG_MAX_MARKS || b >= MBG_MAX_MARKS || !s->marks[a] || !s->marks[b])
+        return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    CK(cudaEventSynchronize(s->marks[b]));
+    CK(cudaEventElapsedTime(ms, s->marks[a], s->marks[b]));
     return MBG_OK;
 }
 

@@ -77,6 +77,8 @@ SIGNATURES = {
     "mbg_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "mbg_event_begin": (C.c_int, [_h]),
     "mbg_event_end": (C.c_int, [_h, C.POINTER(C.c_float)]),
+    "mbg_mark": (C.c_int, [_h, C.c_int32]),
+    "mbg_mark_elapsed": (C.c_int, [_h, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "mbg_launch_count": (C.c_int, [_h, _i64p]),
 }
 

@@ -119,7 +119,7 @@ def launches(path):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("reports", nargs="+", help="path.ncu-rep:key")
+    ap.add_argument("reports", nargs="+", help="path.ncu-rep:key[:cell_steps of the profiled launch]")
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--launches", default=None)
     a = ap.parse_args()
@@ -127,7 +127,10 @@ def main():
     summ = json.loads(summ_path.read_text()) if summ_path.exists() else {}
     md = [f"# ncu summary ({a.tag})\n"]
     for spec in a.reports:
-        rep, key = spec.rsplit(":", 1)
+        parts = spec.split(":")
+        rep, key = parts[0], parts[1]
+        if len(parts) > 2:
+            CELL_STEPS[key.split("_")[0]] = int(float(parts[2]))
         s = summarize(rep, key)
         summ[key] = s
         md.append(f"## {key}\n\n```\n{json.dumps(s, indent=1)}\n```\n")
