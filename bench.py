@@ -321,7 +321,9 @@ def run_mine(args, world, rank, local):
             e2e_times.append(dt_run)
         if it == 0:
             p = sol.plan
-            h2d = 8 * (p.grid.num_x + (p.grid.num_x + 1) + 1 + p.state_words + p.src_values.size)
+            # initial E/H (skipped when identically zero: a device memset), rho0, source samples
+            fields = 0 if p.fields_zero else p.grid.num_x + (p.grid.num_x + 1) + 1
+            h2d = 8 * (fields + p.state_words + p.src_values.size)
             d2h = sum(r.data.size * (16 if r.is_complex else 8) for r in res) + 8 * max(1, (num_t - 1) // (1 << 14))
     e2e_value = cell_updates / sum(e2e_times)
 

@@ -115,7 +115,8 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
 int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *quantity, const int64_t *cell,
                     const int32_t *i, const int32_t *j, const int64_t *every);
 
-/* state: e has (win_hi - win_lo) entries, h has one more (node win_hi) */
+/* state: e has (win_hi - win_lo) entries, h has one more (node win_hi);
+ * e == h == NULL sets both fields to zero on the device (no host copy) */
 int mbg_upload_fields(mbg_solver *s, const double *e, const double *h);
 /* one packed state vector (words per cell) broadcast to every quantum cell */
 int mbg_upload_density(mbg_solver *s, const double *words);

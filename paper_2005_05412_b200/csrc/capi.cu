@@ -611,8 +611,15 @@ int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *c
 }
 
 int mbg_upload_fields(mbg_solver *s, const double *e, const double *h) {
-    if (!s || !e || !h) return MBG_E_ARG;
+    if (!s || (!e) != (!h)) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
+    if (!e) {
+        CK(cudaMemsetAsync(s->e[s->cur], 0, sizeof(double) * s->win_n, s->stream));
+        CK(cudaMemsetAsync(s->h[s->cur], 0, sizeof(double) * (s->win_n + 1), s->stream));
+        CK(cudaMemsetAsync(s->h[1 - s->cur] + s->win_n, 0, sizeof(double), s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+        return MBG_OK;
+    }
     // only the current buffer: every launch writes all of its result cells into
     // the other one, and node win_hi of H (never updated) is zeroed at create
     CK(cudaMemcpyAsync(s->e[s->cur], e, sizeof(double) * s->win_n, cudaMemcpyHostToDevice, s->stream));

@@ -344,11 +344,38 @@ struct NoHook {
     __device__ void operator()() const {}
 };
 
+// record masks / scan flags of the chunk being stepped, staged by the hook
+// (read after the first step's barriers)
+__shared__ unsigned long long s_mask[kMaxTileSteps];
+__shared__ unsigned char s_check[kMaxTileSteps];
+
+// result range [lo, hi) of the CTA tile and its first loaded cell, re-derived
+// where they are used instead of being held in registers across the steps:
+// from blockIdx and the parameter bank (per-launch kernel) ...
+struct LaunchSpan {
+    const Launch &L;
+    __device__ long long lo() const { return L.res_lo + (long long)blockIdx.x * L.tile_own; }
+    __device__ long long hi() const {
+        const long long h = lo() + L.tile_own;
+        return h < L.res_hi ? h : L.res_hi;
+    }
+    __device__ long long base() const { return tile_base(L, lo()); }
+};
+
+// ... or from the item range the persistent kernel staged in shared memory
+struct SharedSpan {
+    const Launch &L;
+    const WaveItem &it;
+    __device__ long long lo() const { return it.lo; }
+    __device__ long long hi() const { return it.hi; }
+    __device__ long long base() const { return tile_base(L, it.lo); }
+};
+
 // hook(): runs once the tile's loads are in flight, before the first step
 // (the persistent kernel stages its step masks and claims its next item there)
-template <bool QM, bool ONE_QM, bool REAL = false, class Hook = NoHook>
-__device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
-                                             long long base, int r_e, int r_h, const Hook &hook = Hook()) {
+template <bool QM, bool ONE_QM, bool REAL, class Span, class Hook>
+__device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &K, const Span &span, int r_e, int r_h,
+                                             const Hook &hook) {
     __shared__ double seam_e[2][kBlochWarpsPerBlock], seam_h[2][kBlochWarpsPerBlock];
     const Launch &L = P.L;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -356,9 +383,9 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     const int qmi = QM ? (ONE_QM ? 0 : L.rg.qm[r_e]) : 0;
     const BlochQm &q = P.qm[qmi];
     const double bgp = pol_coef(bg, P.rq[qmi], REAL);
-    const long long first = base + (long long)warp * W + (long long)lane * C;  // this lane's first cell
-    const long long l0 = first - L.win_lo;
+    const long long lane_off = (long long)warp * W + (long long)lane * C;  // this lane's first cell - base
     double E[C], H[C], X[C], Y[C], Z[C];
+    const long long l0 = span.base() + lane_off - L.win_lo;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
         E[i] = ld(K.e_in + l0 + i);
@@ -393,10 +420,11 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
             // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
             E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bgp * p))) : mad(bdx, hr - H[i], a * E[i]);
         }
-        const unsigned long long mask = K.mask[s];
-        const bool check = K.check[s] != 0;
+        const unsigned long long mask = s_mask[s];
+        const bool check = s_check[s] != 0;
         if (mask || check) {
             const long long n = K.n0 + s;
+            const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
 #pragma unroll
             for (int i = 0; i < C; ++i) {
                 const long long c = first + i;
@@ -428,10 +456,13 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
             }
         }
     }
+    const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
+    const long long o0 = first - L.win_lo;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
         const long long c = first + i;
         if (c < t_lo || c >= t_hi) continue;
+        const long long l0 = o0;
         K.e_out[l0 + i] = E[i];
         K.h_out[l0 + i] = H[i];
         if (QM) {
@@ -450,20 +481,20 @@ constexpr int kEdgeWarps = 4;
 // interior CTA tile: dispatch on the medium (the density step must be the very
 // same formula the edge path uses -- bitwise independence of the tiling -- so
 // the real-dipole choice is global)
-template <class Hook = NoHook>
-__device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
-                                              long long base, const Hook &hook = Hook()) {
+template <class Span, class Hook>
+__device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk &K, const Span &span, const Hook &hook) {
     const Launch &L = P.L;
+    const long long base = span.base();
     const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
     const int qm = L.rg.qm[re];
     if (qm < 0)
-        interior_cta<false, true>(P, K, t_lo, t_hi, base, re, rh, hook);
+        interior_cta<false, true, false>(P, K, span, re, rh, hook);
     else if (P.real_dipole)
-        P.n_qm == 1 ? interior_cta<true, true, true>(P, K, t_lo, t_hi, base, re, rh, hook)
-                    : interior_cta<true, false, true>(P, K, t_lo, t_hi, base, re, rh, hook);
+        P.n_qm == 1 ? interior_cta<true, true, true>(P, K, span, re, rh, hook)
+                    : interior_cta<true, false, true>(P, K, span, re, rh, hook);
     else
-        P.n_qm == 1 ? interior_cta<true, true, false>(P, K, t_lo, t_hi, base, re, rh, hook)
-                    : interior_cta<true, false, false>(P, K, t_lo, t_hi, base, re, rh, hook);
+        P.n_qm == 1 ? interior_cta<true, true, false>(P, K, span, re, rh, hook)
+                    : interior_cta<true, false, false>(P, K, span, re, rh, hook);
 }
 
 // one warp over the result range [t_lo, t_hi) of at most 32*C - 2k cells
@@ -493,12 +524,15 @@ __device__ __noinline__ void edge_range_call(const BlochParams &P, const Chunk &
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
 bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     const Launch &L = P.L;
-    const long long t_lo = L.res_lo + (long long)blockIdx.x * L.tile_own;
-    if (t_lo >= L.res_hi) return;
-    const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
-    const long long base = tile_base(L, t_lo);
-    if (!tile_is_interior(L, base, kBlochCtaTile)) return;
-    interior_tile(P, launch_chunk(L), t_lo, t_hi, base);
+    const LaunchSpan span{L};
+    if (span.lo() >= L.res_hi) return;
+    if (!tile_is_interior(L, span.base(), kBlochCtaTile)) return;
+    interior_tile(P, launch_chunk(L), span, [&]() {
+        if (threadIdx.x < L.k) {
+            s_mask[threadIdx.x] = L.step_mask[threadIdx.x];
+            s_check[threadIdx.x] = L.check[threadIdx.x];
+        }
+    });
 }
 
 // the few remaining cells (domain/window edges, region interfaces, sources),
@@ -575,8 +609,6 @@ __device__ bool deps_done(const BlochWave &V, long long item, bool wait) {
 __global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
 bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ BlochWave V) {
     __shared__ unsigned item_s, next_s;
-    __shared__ unsigned long long mask_s[kMaxTileSteps];
-    __shared__ unsigned char check_s[kMaxTileSteps];
     // the current item's chunk and range live in shared memory: the tile code
     // reads them where it needs them instead of holding them in registers
     // across the step loop (the per-launch kernels read the same from the
@@ -596,7 +628,7 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
         const int buf = (V.cur + c) & 1;
         chunk_s = Chunk{V.e[buf],     V.h[buf],  V.s[buf], V.e[buf ^ 1], V.h[buf ^ 1],
                         V.s[buf ^ 1], V.n0 + (long long)c * L.k,
-                        c == V.n_chunks - 1 ? V.last_steps : L.k, mask_s, check_s};
+                        c == V.n_chunks - 1 ? V.last_steps : L.k, s_mask, s_check};
         item_range_s = V.items[t];
     };
     if (threadIdx.x == 0) {
@@ -621,14 +653,14 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
             if (threadIdx.x == 0) next_s = atomicAdd(V.ticket, 1u);
             const long long k0 = K.n0 - V.n0;
             if (threadIdx.x < K.steps) {
-                mask_s[threadIdx.x] = V.masks[k0 + threadIdx.x];
-                check_s[threadIdx.x] = V.checks[k0 + threadIdx.x];
+                s_mask[threadIdx.x] = V.masks[k0 + threadIdx.x];
+                s_check[threadIdx.x] = V.checks[k0 + threadIdx.x];
             }
         };
-        const long long lo = item_range_s.lo, hi = item_range_s.hi;
         if (!item_range_s.edge) {
-            interior_tile(P, K, lo, hi, tile_base(L, lo), hook);
+            interior_tile(P, K, SharedSpan{L, item_range_s}, hook);
         } else {
+            const long long lo = item_range_s.lo, hi = item_range_s.hi;
             hook();
             __syncthreads();
             const long long n_sub = (hi - lo + warp_own - 1) / warp_own;

@@ -311,6 +311,9 @@ class SolverPlan:
     plans: list
     boundary: tuple  # ((w, c dt/dx, Z) left, (...) right) or None
     materials: list = field(default_factory=list)
+    # the initial fields are identically zero (the scenario's default
+    # ConstantField(0)): the upload is a device memset instead of a copy
+    fields_zero: bool = False
 
     @property
     def state_words(self) -> int:
@@ -413,4 +416,5 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None) -> Solve
         src_cells=np.array(cells, dtype=np.int64),
         src_hard=np.array([1 if s.kind == "hard" else 0 for s in srcs], dtype=np.int32),
         src_values=values, plans=plans, boundary=boundary, materials=mats,
+        fields_zero=not (e_init.any() or h_init.any()),
     )

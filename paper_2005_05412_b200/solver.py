@@ -151,9 +151,12 @@ class GpuFdtdSolver:
 
     def upload_initial_state(self, h, win=None):
         lo, hi = win if win is not None else (0, self.grid.num_x)
-        e = native.f64(self.plan.e_init[lo:hi])
-        hf = native.f64(self.plan.h_init[lo:hi + 1])
-        h.call("mbg_upload_fields", native.ptr(e), native.ptr(hf))
+        if self.plan.fields_zero:  # zero ICs: a device memset, no host copy
+            h.call("mbg_upload_fields", None, None)
+        else:
+            e = native.f64(self.plan.e_init[lo:hi])
+            hf = native.f64(self.plan.h_init[lo:hi + 1])
+            h.call("mbg_upload_fields", native.ptr(e), native.ptr(hf))
         if self.plan.levels:
             w = native.f64(self.plan.rho_init_packed())
             h.call("mbg_upload_density", native.ptr(w))
