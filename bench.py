@@ -107,8 +107,9 @@ def build_workload(mb, gpus):
     mb.clear_material_library()
     if gpus == 1:
         return configs.cfg2(mb)
-    # weak scaling: 2^22 cells and 150 um per GPU, same medium and grid spacing
-    return configs.cfg2(mb, nx=(1 << 22) * gpus, length_scale=gpus)
+    # weak scaling: G copies of the cfg2 device side by side, 2^22 cells per
+    # GPU, so each rank steps exactly cfg2's mix of medium and vacuum cells
+    return configs.cfg2(mb, nx=(1 << 22) * gpus, replicas=gpus)
 
 
 def algorithmic_per_cell(plan):

@@ -96,18 +96,23 @@ def _splitmix(api):
     return fn
 
 
-def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", length_scale=1):
+def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", replicas=1):
     """cfg 1 lengthened to 2^22 cells with T1 = 1 ns, T2 = 1 ps, drawn inversion.
 
-    ``length_scale`` G > 1 builds the weak-scaling variant: a 150 um * G device
-    (same vacuum ends) for nx = 2^22 * G, so dx and dt stay fixed."""
+    ``replicas`` G > 1 builds the weak-scaling variant: G copies of the 150 um
+    device side by side (each vacuum | medium | vacuum) on nx = 2^22 * G
+    cells, so dx and dt stay (almost exactly) fixed and every slab of the
+    G-way partition holds the same mix of medium and vacuum cells as cfg 2."""
     vac = api.ensure_material(api.Material("Vacuum"))
     act = api.ensure_material(api.Material("SIT_2lvl_relax" + tag, qm=sit_medium(api, 1e9, 1e12)))
     dev = api.Device("cfg2")
-    length = 150e-6 * length_scale
-    dev.add_region(api.Region("vacuum left", vac.id, 0.0, 7.5e-6))
-    dev.add_region(api.Region("medium", act.id, 7.5e-6, length - 7.5e-6))
-    dev.add_region(api.Region("vacuum right", vac.id, length - 7.5e-6, length))
+    unit = 150e-6
+    for j in range(replicas):
+        x0 = unit * j
+        sfx = f" {j}" if replicas > 1 else ""
+        dev.add_region(api.Region("vacuum left" + sfx, vac.id, x0, x0 + 7.5e-6))
+        dev.add_region(api.Region("medium" + sfx, act.id, x0 + 7.5e-6, x0 + unit - 7.5e-6))
+        dev.add_region(api.Region("vacuum right" + sfx, vac.id, x0 + unit - 7.5e-6, x0 + unit))
     ic_e = api.RandomField(1e7, seed=7) if stress else None
     sce = api.Scenario("cfg2", nx, _end_time(api, dev, nx, steps), cfg2_rho0(api), ic_e_field=ic_e)
     sce.add_source(sit_source(api))

@@ -744,8 +744,10 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
     Launch L = base_launch(s);
     L.n0 = first;
     L.k = k;
-    L.res_lo = 0;
-    L.res_hi = s->g.num_x;
+    // a window's result range loses k cells per side per chunk; its ghosts
+    // (>= the steps between exchanges) absorb that (see mbg_advance)
+    L.res_lo = s->g.win_lo == 0 ? 0 : s->g.win_lo + k;
+    L.res_hi = s->g.win_hi == s->g.num_x ? s->g.num_x : s->g.win_hi - k;
     L.tile_own = tw - 2 * k;
     if (!s->wave_items) {
         // interior CTA tiles as they are; a non-interior tile split into items
@@ -863,12 +865,12 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     const bool windowed = s->g.win_lo > 0 || s->g.win_hi < s->g.num_x;
     if (windowed) {
         const long long gw = std::min(s->g.win_lo > 0 ? ghost_l : LLONG_MAX, s->g.win_hi < s->g.num_x ? ghost_r : LLONG_MAX);
-        if (n_steps > std::min<long long>(gw, s->k))
-            return fail(s, MBG_E_ARG, "a slab advances at most min(ghost width, k) steps between exchanges");
+        if (n_steps > gw)
+            return fail(s, MBG_E_ARG, "a slab advances at most its ghost width in steps between exchanges");
     }
     cudaSetDevice(s->g.device);
     const int tw = tile_width(s);
-    if (!windowed && (s->bloch || s->g.levels == 0) && !(s->g.flags & MBG_FLAG_PER_LAUNCH) && n_steps > s->k)
+    if ((s->bloch || s->g.levels == 0) && !(s->g.flags & MBG_FLAG_PER_LAUNCH) && n_steps > s->k)
         return advance_wave(s, first, n_steps, tw);
     long long n = first;
     const long long end = first + n_steps;

@@ -3,12 +3,14 @@
 The 1D domain is cut into G contiguous slabs with the reference's own
 partition rule (``np.linspace(0, Nx, G+1)``, solver_fdtd.py:468 -- there it
 splits cells among CPU worker threads).  Each slab is held on its device as a
-window [own_lo - k, own_hi + k) (clipped at the physical ends): k ghost cells
-per side, k = the temporal tile depth.  One fused launch advances k steps; the
-valid region shrinks by one cell per side per step, so after it exactly the
-owned cells are current and the ghosts are refreshed by a point-to-point
-exchange with the two neighbours -- E, H and every density plane of k cells
-per interface and direction.  There is no other collective on the data path:
+window [own_lo - g, own_hi + g) (clipped at the physical ends): g ghost cells
+per side, g = the exchange period P = m * k steps (k = the temporal tile
+depth; m = 32 chunks for the two-level / classical kernels, whose persistent
+launch runs the m chunks back to back, 1 otherwise).  The valid region shrinks
+by one cell per side per step, so after P steps exactly the owned cells are
+current and the ghosts are refreshed by a point-to-point exchange with the two
+neighbours -- E, H and every density plane of g cells per interface and
+direction.  There is no other collective on the data path:
 records are gathered once at the end and the non-finite flag is combined with
 one MIN reduction per poll.
 
@@ -26,6 +28,7 @@ Transports:
 from __future__ import annotations
 
 import ctypes as C
+from contextlib import nullcontext as _nullcontext
 from dataclasses import dataclass
 
 import numpy as np
@@ -236,15 +239,17 @@ def _step_loop(grid, k, advance, exchange, poll, poll_every=1 << 14):
                 raise SolverError(f"non-finite electric field at step {bad}")
 
 
-def run_slabs_local(solver, slabs_count: int):
-    """Run ``solver``'s scenario as ``slabs_count`` slabs on one device (tests)."""
+def run_slabs_local(solver, slabs_count: int, period=None):
+    """Run ``solver``'s scenario as ``slabs_count`` slabs on one device (tests);
+    ``period`` = steps between exchanges (default exchange_period)."""
     if solver._ran:
         raise SolverError("run() may only be called once per solver instance")
     solver._ran = True
     import torch
 
     k = tile_steps_of(solver)
-    slabs = partition(solver.grid.num_x, slabs_count, k)
+    period = period or exchange_period(solver, k, slabs_count)
+    slabs = partition(solver.grid.num_x, slabs_count, period)
     # one shared stream: every pack, unpack and launch runs in issue order
     stream = torch.cuda.Stream(device=f"cuda:{solver.gpu}")
     states = [SlabState(solver, s, stream=stream.cuda_stream) for s in slabs]
@@ -261,13 +266,25 @@ def run_slabs_local(solver, slabs_count: int):
             bads = [b for b in (st.poll() for st in states) if b >= 0]
             return min(bads) if bads else -1
 
-        _step_loop(solver.grid, k, advance, tr.exchange, poll)
+        _step_loop(solver.grid, period, advance, tr.exchange, poll)
         recs = assemble(solver.plan, slabs, [st.records() for st in states])
     finally:
         for st in states:
             st.close()
     solver.results = [p.to_result(solver.grid, d, solver._result_cls) for p, d in zip(solver.plan.plans, recs)]
     return solver.results
+
+
+CHUNKS_PER_EXCHANGE = 32
+
+
+def exchange_period(solver, k: int, world: int) -> int:
+    """Steps between halo exchanges (= ghost width): m fused chunks of k steps,
+    at most the thinnest slab.  The two-level / classical kernels run the m
+    chunks as one persistent launch."""
+    dense = solver.plan.levels > 2 or (solver.plan.levels == 2 and solver.stepper == "rk4")
+    period = k if dense else CHUNKS_PER_EXCHANGE * k
+    return max(1, min(period, solver.grid.num_x // max(1, world)))
 
 
 def tile_steps_of(solver) -> int:
@@ -283,7 +300,7 @@ def tile_steps_of(solver) -> int:
         h.close()
 
 
-def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None):
+def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None):
     """This process's slab of a ``world``-way run (torch.distributed initialised).
     Returns the assembled records on rank 0 and None elsewhere.
 
@@ -294,24 +311,29 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
 
     if k is None:
         k = tile_steps_of(solver)
-    slabs = partition(solver.grid.num_x, world, k)
+    period = period or exchange_period(solver, k, world)
+    slabs = partition(solver.grid.num_x, world, period)
+    # the native launches, the pack/unpack kernels and torch's NCCL ops must
+    # be ordered on one stream: a dedicated torch stream, made current, that
+    # the native handle adopts (the legacy default stream cannot be adopted)
+    stream = torch.cuda.Stream(device) if state_factory is None else None
     if state_factory is None:
-        stream = torch.cuda.current_stream(device).cuda_stream
-        st = SlabState(solver, slabs[rank], stream=stream)
+        st = SlabState(solver, slabs[rank], stream=stream.cuda_stream)
     else:
         st = state_factory(solver, slabs[rank])
     try:
-        tr = TorchTransport(st, device)
-        st.sample(0)
+        with torch.cuda.stream(stream) if stream is not None else _nullcontext():
+            tr = TorchTransport(st, device)
+            st.sample(0)
 
-        def poll():
-            b = st.poll()
-            t = torch.tensor([b if b >= 0 else 2**62], dtype=torch.int64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)
-            v = int(t.item())
-            return -1 if v == 2**62 else v
+            def poll():
+                b = st.poll()
+                t = torch.tensor([b if b >= 0 else 2**62], dtype=torch.int64, device=device)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                v = int(t.item())
+                return -1 if v == 2**62 else v
 
-        _step_loop(solver.grid, k, st.advance, tr.exchange, poll)
+            _step_loop(solver.grid, period, st.advance, tr.exchange, poll)
         mine = st.records()
     finally:
         st.close()
@@ -338,9 +360,13 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
         dist.init_process_group("nccl", device_id=device)
     solver = GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
     k = tile_steps_of(solver)
-    slabs = partition(solver.grid.num_x, world, k)
-    stream = torch.cuda.current_stream(device).cuda_stream
-    st = SlabState(solver, slabs[rank], stream=stream)
+    period = exchange_period(solver, k, world)
+    slabs = partition(solver.grid.num_x, world, period)
+    # one stream for the native launches, the halo pack/unpack and NCCL (see run_slab_rank)
+    stream = torch.cuda.Stream(device)
+    st = SlabState(solver, slabs[rank], stream=stream.cuda_stream)
+    ctx = torch.cuda.stream(stream)
+    ctx.__enter__()
     tr = TorchTransport(st, device)
     st.h.call("mbg_checkpoint_save")
     grid = solver.grid
@@ -350,7 +376,7 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
         st.sample(0)
         n = 1
         while n < grid.num_t:
-            cnt = min(k, grid.num_t - n)
+            cnt = min(period, grid.num_t - n)
             st.advance(n, cnt)
             tr.exchange()
             n += cnt
@@ -363,10 +389,10 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
     st.h.call("mbg_launch_count", C.byref(l0))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(torch.cuda.current_stream(device))
+    t0.record(stream)
     for _ in range(args.steps):
         one_run()
-    t1.record(torch.cuda.current_stream(device))
+    t1.record(stream)
     torch.cuda.synchronize(device)
     ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=device)
     dist.barrier()
@@ -375,6 +401,7 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
     st.h.call("mbg_launch_count", C.byref(l1))
     bad = st.poll()
     st.close()
+    ctx.__exit__(None, None, None)
     if bad >= 0:
         raise SolverError(f"non-finite electric field at step {bad}")
     ms = float(ms.item())
@@ -387,8 +414,10 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"cfg2 weak-scaled: {world} slabs x 2^22 cells, 20000 steps",
-                       "num_x": grid.num_x, "tile_steps": k, "parallelism": f"slab{world}",
-                       "exchange": "NCCL batched isend/irecv of k ghost cells per interface every k steps"},
+                       "num_x": grid.num_x, "tile_steps": k, "exchange_period": period,
+                       "parallelism": f"slab{world}",
+                       "exchange": f"NCCL batched isend/irecv of {period} ghost cells per interface every "
+                                   f"{period} steps (one persistent launch of {period // k} chunks between)"},
             # this rank's kernels (step, edge, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),
         }

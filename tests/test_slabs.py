@@ -49,7 +49,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, k, out_path):
+def _worker(rank, world, port, case, k, period, out_path):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     import torch.distributed as dist
@@ -68,16 +68,17 @@ def _worker(rank, world, port, case, k, out_path):
         mbw.clear_material_library()
         dev, sce = build(mbw)
         solver = mbw.GpuFdtdSolver(dev, sce, stepper=stepper)
-        recs = sl.run_slab_rank(solver, world, rank, "cpu", state_factory=NumpySlab, k=k)
+        recs = sl.run_slab_rank(solver, world, rank, "cpu", state_factory=NumpySlab, k=k, period=period)
         if rank == 0:
             np.savez(out_path, *recs)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k,case", [(2, 7, "sit_hard_whole"), (3, 16, "multi_material"),
-                                          (2, 5, "vacuum_sources")])
-def test_gloo_ranks_match_oracle_bitwise(world, k, case):
+@pytest.mark.parametrize("world,k,period,case", [(2, 7, None, "sit_hard_whole"), (3, 16, 16, "multi_material"),
+                                                 (2, 5, None, "vacuum_sources"), (2, 3, 7, "sit_hard_whole")])
+def test_gloo_ranks_match_oracle_bitwise(world, k, period, case):
+    """period: steps between exchanges (ghost width); None = m chunks of k."""
     import oracle as orc
 
     dev, sce, stepper = build_case(case)
@@ -86,7 +87,7 @@ def test_gloo_ranks_match_oracle_bitwise(world, k, case):
     assert bad == 0
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "recs.npz")
-        mp.spawn(_worker, args=(world, _free_port(), case, k, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), case, k, period, out), nprocs=world, join=True)
         got = np.load(out)
         for r, (p, want) in enumerate(zip(plan.plans, ref)):
             have = got[f"arr_{r}"]
@@ -95,16 +96,20 @@ def test_gloo_ranks_match_oracle_bitwise(world, k, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,count", [("sit_hard_whole", 2), ("sit_hard_whole", 5), ("multi_material", 3),
-                                        ("rand3_split", 2), ("rand6_split", 3), ("rand4_rk4", 2),
-                                        ("cfg4_r14", 4)])
-def test_native_slabs_on_one_gpu_match_single_domain(case, count):
+@pytest.mark.parametrize("case,count,period", [("sit_hard_whole", 2, None), ("sit_hard_whole", 5, None),
+                                               ("multi_material", 3, None), ("multi_material", 2, 64),
+                                               ("cfg2_r16", 3, None), ("vacuum_sources", 2, 100),
+                                               ("rand3_split", 2, None), ("rand6_split", 3, None),
+                                               ("rand4_rk4", 2, None), ("cfg4_r14", 4, None)])
+def test_native_slabs_on_one_gpu_match_single_domain(case, count, period):
+    """Windowed solvers (persistent multi-chunk launches between exchanges for
+    the two-level / classical kernels) bit-identical to the single domain."""
     dev, sce, stepper = build_case(case)
     ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     mb.clear_material_library()
     dev, sce, stepper = build_case(case)
     solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
-    got = slabs.run_slabs_local(solver, count)
+    got = slabs.run_slabs_local(solver, count, period)
     for a, b in zip(ref, got):
         assert a.name == b.name and a.data.shape == b.data.shape
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name

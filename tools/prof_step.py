@@ -24,6 +24,7 @@ ap.add_argument("--exact", action="store_true")
 ap.add_argument("--stepper", default="splitting")
 ap.add_argument("--nx", type=int, default=0)
 ap.add_argument("--per-launch", action="store_true", help="one launch per k steps (no persistent kernel)")
+ap.add_argument("--advance-steps", type=int, default=0, help="steps per mbg_advance call (0: all at once)")
 ap.add_argument("--no-warm", action="store_true", help="single pass (for ncu)")
 a = ap.parse_args()
 kw = {"nx": a.nx} if a.nx else {}
@@ -40,12 +41,23 @@ k = C.c_int32(0)
 h.call("mbg_tile_steps", C.byref(k))
 steps = a.steps or 4 * k.value
 h.call("mbg_sample", 0)
+
+
+def advance():
+    per = a.advance_steps or steps
+    n = 1
+    while n < steps + 1:
+        cnt = min(per, steps + 1 - n)
+        h.call("mbg_advance", n, cnt)
+        n += cnt
+
+
 if not a.no_warm:  # ramp clocks / load modules outside the timed region
     h.call("mbg_checkpoint_save")
-    h.call("mbg_advance", 1, steps)
+    advance()
     h.call("mbg_checkpoint_restore")
 h.call("mbg_event_begin")
-h.call("mbg_advance", 1, steps)
+advance()
 ms = C.c_float(0)
 h.call("mbg_event_end", C.byref(ms))
 print(f"{a.config}/{a.stepper}: nx={sol.grid.num_x} k={k.value} steps={steps} device {ms.value:.3f} ms "
