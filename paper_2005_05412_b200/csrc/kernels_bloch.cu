@@ -54,6 +54,14 @@ __device__ __forceinline__ Chunk launch_chunk(const Launch &L) {
 // field / state loads bypass L1 (streamed once per chunk; in the persistent
 // kernel another CTA of the same launch produced them)
 __device__ __forceinline__ double ld(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ void ld2(const double *p, double &a, double &b) {
+    const double2 v = __ldcg(reinterpret_cast<const double2 *>(p));
+    a = v.x;
+    b = v.y;
+}
+__device__ __forceinline__ void st2(double *p, double a, double b) {
+    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
 
 // _kernels.py:200-232, same expression order (each mad(a, b, c) is the
 // reference's "c + a*b" term)
@@ -386,14 +394,27 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     const long long lane_off = (long long)warp * W + (long long)lane * C;  // this lane's first cell - base
     double E[C], H[C], X[C], Y[C], Z[C];
     const long long l0 = span.base() + lane_off - L.win_lo;
+    if ((l0 & 1) == 0) {  // 16-byte aligned pairs (the usual case: even tile bases, padded planes)
 #pragma unroll
-    for (int i = 0; i < C; ++i) {
-        E[i] = ld(K.e_in + l0 + i);
-        H[i] = ld(K.h_in + l0 + i);
-        if (QM) {
-            X[i] = ld(K.s_in + l0 + i);
-            Y[i] = ld(K.s_in + L.plane + l0 + i);
-            Z[i] = ld(K.s_in + 2 * L.plane + l0 + i);
+        for (int i = 0; i < C; i += 2) {
+            ld2(K.e_in + l0 + i, E[i], E[i + 1]);
+            ld2(K.h_in + l0 + i, H[i], H[i + 1]);
+            if (QM) {
+                ld2(K.s_in + l0 + i, X[i], X[i + 1]);
+                ld2(K.s_in + L.plane + l0 + i, Y[i], Y[i + 1]);
+                ld2(K.s_in + 2 * L.plane + l0 + i, Z[i], Z[i + 1]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            E[i] = ld(K.e_in + l0 + i);
+            H[i] = ld(K.h_in + l0 + i);
+            if (QM) {
+                X[i] = ld(K.s_in + l0 + i);
+                Y[i] = ld(K.s_in + L.plane + l0 + i);
+                Z[i] = ld(K.s_in + 2 * L.plane + l0 + i);
+            }
         }
     }
     hook();
@@ -458,17 +479,29 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     }
     const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
     const long long o0 = first - L.win_lo;
+    if (first >= t_lo && first + C <= t_hi && (o0 & 1) == 0) {  // the whole lane, 16-byte pairs
+#pragma unroll
+        for (int i = 0; i < C; i += 2) {
+            st2(K.e_out + o0 + i, E[i], E[i + 1]);
+            st2(K.h_out + o0 + i, H[i], H[i + 1]);
+            if (QM) {
+                st2(K.s_out + o0 + i, X[i], X[i + 1]);
+                st2(K.s_out + L.plane + o0 + i, Y[i], Y[i + 1]);
+                st2(K.s_out + 2 * L.plane + o0 + i, Z[i], Z[i + 1]);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < C; ++i) {
         const long long c = first + i;
         if (c < t_lo || c >= t_hi) continue;
-        const long long l0 = o0;
-        K.e_out[l0 + i] = E[i];
-        K.h_out[l0 + i] = H[i];
+        K.e_out[o0 + i] = E[i];
+        K.h_out[o0 + i] = H[i];
         if (QM) {
-            K.s_out[l0 + i] = X[i];
-            K.s_out[L.plane + l0 + i] = Y[i];
-            K.s_out[2 * L.plane + l0 + i] = Z[i];
+            K.s_out[o0 + i] = X[i];
+            K.s_out[L.plane + o0 + i] = Y[i];
+            K.s_out[2 * L.plane + o0 + i] = Z[i];
         }
     }
 }
