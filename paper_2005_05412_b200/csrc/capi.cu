@@ -94,7 +94,7 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
     } while (0)
 
 int default_tile_steps(int levels, int stepper) {
-    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 80;
+    if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 64;
     if (levels <= 3) return 16;
     return 4;
 }
