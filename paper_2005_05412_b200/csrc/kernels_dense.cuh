@@ -77,17 +77,15 @@ __device__ __forceinline__ void herm(V &s, int i, int j, double &re, double &im)
 }
 
 // 1/d for a normal positive d (|pivot|^2 of (I + iA)/2 is >= 1/4): the fast
-// variant uses the hardware seed + two Newton steps, no special-case branch
+// variant refines the hardware seed (error 2^-22) once, cubically, no special-case branch
 __device__ __forceinline__ double recip_pos(double d) {
 #if defined(MBG_EXACT) && MBG_EXACT
     return 1.0 / d;
 #else
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-    double e = fma(-d, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-d, r, 1.0);
-    return fma(r, e, r);
+    const double e = fma(-d, r, 1.0);  // one cubically convergent step r + r(e + e^2)
+    return fma(r, fma(e, e, e), r);
 #endif
 }
 
