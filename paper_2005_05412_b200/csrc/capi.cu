@@ -261,8 +261,19 @@ BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
         std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
         P.real_dipole &= real_dipole(b) ? 1 : 0;
         const double u = b.a0_c * b.a0_c;
-        P.rq[q] = BlochReal{u,           1.0 + u,         4.0 * u,         b.az_c * b.az_c,     1.0 - u,
-                            b.pol_factor * b.mu_x * b.fxy, b.fxy * b.fxy, b.kz * b.kz, b.kz * b.cz + b.cz};
+        P.rq[q] = BlochReal{u,
+                            1.0 + u,
+                            4.0 * u,
+                            b.az_c * b.az_c,
+                            1.0 - u,
+                            b.pol_factor * b.mu_x * b.fxy,
+                            b.fxy * b.fxy,
+                            b.kz * b.kz,
+                            b.kz * b.cz + b.cz,
+                            0.5 * (1.0 + u),
+                            0.5 * (1.0 - u),
+                            2.0 * b.az_c,
+                            2.0 * b.ax_s};
     }
     // the fast variant's real-dipole cell function works in the relaxed frame
     P.frame = state_frame(s);

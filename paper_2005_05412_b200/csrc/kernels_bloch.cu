@@ -113,7 +113,7 @@ __device__ __forceinline__ double bloch_cell_real(const BlochQm &q, const BlochR
 }
 
 #if !(defined(MBG_EXACT) && MBG_EXACT)
-// 1/d for d >= 1 (the Cayley denominator (1+q-u)^2 + 4u is never below 1):
+// 1/d for d >= 1/4 (a quarter of the Cayley denominator (1+q-u)^2 + 4u >= 1):
 // hardware seed refined by one cubically convergent step r + r(e + e^2),
 // e = 1 - d r (seed error 2^-22 -> below double rounding), no special cases
 __device__ __forceinline__ double rcp_ge1(double d) {
@@ -132,18 +132,20 @@ __device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const 
                                                         double &y, double &z) {
     const double x0 = x;
     const double x1 = r.f2 * x, y1 = r.f2 * y, z1 = fma(r.kz2, z, r.czz);
-    const double ax = q.ax_s * e, az = q.az_c;
+    // the rotation with the factors 4 and 8 absorbed: q = 4/den = 1/((t1/2)^2 + u),
+    // nh = num/2, k1 = (nh^2 - qq) q, g = 2 nh q, dotb = 2 q (a . v1)
+    const double ax = q.ax_s * e, ax2 = r.axs2 * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
-    const double num = r.c1 - qq;
-    const double t1 = qq + r.c2;
-    const double inv = rcp_ge1(fma(t1, t1, r.c4u));
-    const double k1 = fma(num, num, -4.0 * qq) * inv;
-    const double g = num * (4.0 * inv);
-    const double gaz = g * az, gax = g * ax;
-    const double dotb = (8.0 * inv) * fma(az, z1, ax * x1);
-    x = fma(dotb, ax, fma(-gaz, y1, k1 * x1));
+    const double nh = fma(-0.5, qq, r.c1h);
+    const double th = fma(0.5, qq, r.c2h);
+    const double iq = rcp_ge1(fma(th, th, r.u));
+    const double k1 = fma(nh, nh, -qq) * iq;
+    const double ph = nh * iq;
+    const double gaz = ph * r.az2x, gax = ph * ax2;
+    const double dh = iq * fma(az, z1, ax * x1);
+    x = fma(dh, ax2, fma(-gaz, y1, k1 * x1));
     y = fma(-gax, z1, fma(gaz, x1, k1 * y1));
-    z = fma(dotb, az, fma(gax, y1, k1 * z1));
+    z = fma(dh, r.az2x, fma(gax, y1, k1 * z1));
     return x - x0;
 }
 #define MBG_BLOCH_REAL bloch_cell_real_frame

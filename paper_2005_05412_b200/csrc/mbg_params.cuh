@@ -86,6 +86,10 @@ struct BlochReal {
     double f2;    // fxy * fxy
     double kz2;   // kz * kz
     double czz;   // kz * cz + cz
+    double c1h;   // (1 + u) / 2
+    double c2h;   // (1 - u) / 2
+    double az2x;  // 2 az_c
+    double axs2;  // 2 ax_s
 };
 
 // Relaxed-frame state of the fast two-level path: the device holds each
