@@ -162,6 +162,16 @@ __device__ __forceinline__ double pol_coef(double bg, const BlochReal &r, bool r
     return (MBG_POL_FOLD && real) ? bg * r.pfmu : bg;
 }
 
+// E^n = a E - b'G p + b'/dx (H[m+1] - H[m]) (solver_fdtd.py:59-66).  The fast
+// variant fuses the polarisation term into E when a == 1 (lossless medium;
+// 1*E is exact, so only the rounding of the fused term changes); every path
+// uses this one function, so interior and edge cells stay bitwise equal.
+template <bool A1>
+__device__ __forceinline__ double e_update(double a, double bdx, double bgp, double e, double dh, double p) {
+    if (MBG_POL_FOLD && A1) return mad(bdx, dh, fma(-bgp, p, e));
+    return mad(bdx, dh, mad(a, e, -(bgp * p)));
+}
+
 // density entry (i, j) of a Bloch vector (_kernels.py:530-536)
 __device__ __forceinline__ void bloch_entry(int i, int j, double x, double y, double z, double &re, double &im) {
     if (i == j) {
@@ -262,9 +272,13 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
             const double hr = (lane == 31) ? u[i < C - 1 ? i + 1 : i] : u[i];
             double en = E[i];
             if ((emask >> i) & 1u)
-                en = UNI ? mad(ubdx, hr - Hn[i], mad(ua, E[i], -(ubgp * p[i])))
-                         : mad(cbdx[i], hr - Hn[i],
-                               mad(ca[i], E[i], -(pol_coef(cbg[i], P.rq[qi[i] < 0 ? 0 : qi[i]], P.real_dipole) * p[i])));
+            {
+                const double a = UNI ? ua : ca[i], bdx = UNI ? ubdx : cbdx[i];
+                const double bgp =
+                    UNI ? ubgp : pol_coef(cbg[i], P.rq[qi[i] < 0 ? 0 : qi[i]], P.real_dipole);
+                en = a == 1.0 ? e_update<true>(a, bdx, bgp, E[i], hr - Hn[i], p[i])
+                              : e_update<false>(a, bdx, bgp, E[i], hr - Hn[i], p[i]);
+            }
             if (left_edge && i == 0 && lane == 0) {
                 // solver_fdtd.py:372-374
                 const double e_at = mad(L.l_c, e_right0, L.l_omc * E[0]);
@@ -383,7 +397,7 @@ struct SharedSpan {
 
 // hook(): runs once the tile's loads are in flight, before the first step
 // (the persistent kernel stages its step masks and claims its next item there)
-template <bool QM, bool ONE_QM, bool REAL, class Span, class Hook>
+template <bool QM, bool ONE_QM, bool REAL, bool A1, class Span, class Hook>
 __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &K, const Span &span, int r_e, int r_h,
                                              const Hook &hook) {
     __shared__ double seam_e[2][kBlochWarpsPerBlock], seam_h[2][kBlochWarpsPerBlock];
@@ -441,7 +455,8 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                              : bloch_cell(q, E[i], X[i], Y[i], Z[i]);
             const double hr = i == C - 1 ? hr_last : H[i + 1];
             // p = 0 in classical cells: a E - bg*0 == a E exactly, so the term is dropped
-            E[i] = QM ? mad(bdx, hr - H[i], mad(a, E[i], -(bgp * p))) : mad(bdx, hr - H[i], a * E[i]);
+            E[i] = QM ? e_update<A1>(a, bdx, bgp, E[i], hr - H[i], p)
+                      : mad(bdx, hr - H[i], (MBG_POL_FOLD && A1) ? E[i] : a * E[i]);
         }
         const unsigned long long mask = s_mask[s];
         const bool check = s_check[s] != 0;
@@ -522,14 +537,18 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk 
     const long long base = span.base();
     const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
     const int qm = L.rg.qm[re];
+    const bool a1 = L.rg.a[re] == 1.0;  // lossless region (the fast variant fuses the p term)
     if (qm < 0)
-        interior_cta<false, true, false>(P, K, span, re, rh, hook);
+        a1 ? interior_cta<false, true, false, true>(P, K, span, re, rh, hook)
+           : interior_cta<false, true, false, false>(P, K, span, re, rh, hook);
+    else if (P.real_dipole && P.n_qm == 1)
+        a1 ? interior_cta<true, true, true, true>(P, K, span, re, rh, hook)
+           : interior_cta<true, true, true, false>(P, K, span, re, rh, hook);
     else if (P.real_dipole)
-        P.n_qm == 1 ? interior_cta<true, true, true>(P, K, span, re, rh, hook)
-                    : interior_cta<true, false, true>(P, K, span, re, rh, hook);
+        interior_cta<true, false, true, false>(P, K, span, re, rh, hook);
     else
-        P.n_qm == 1 ? interior_cta<true, true, false>(P, K, span, re, rh, hook)
-                    : interior_cta<true, false, false>(P, K, span, re, rh, hook);
+        P.n_qm == 1 ? interior_cta<true, true, false, false>(P, K, span, re, rh, hook)
+                    : interior_cta<true, false, false, false>(P, K, span, re, rh, hook);
 }
 
 // one warp over the result range [t_lo, t_hi) of at most 32*C - 2k cells
