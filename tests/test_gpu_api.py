@@ -264,3 +264,85 @@ def test_phase_velocity_error_below_one_percent():
     assert abs((2 * math.pi / period) / k - mb.C0) / mb.C0 <= 0.01
     omega_num = (2.0 / dt) * math.asin(0.5 * math.sin(k * dx / 2.0))
     assert abs(2 * math.pi / period - omega_num) / omega_num < 2e-3
+
+
+# ---------------------------------------------------------------- C ABI details
+
+def _cfg2_small(nx=1 << 14, steps=600, stress=True):
+    from paper_2005_05412_b200 import configs
+
+    mb.clear_material_library()
+    return configs.cfg2(mb, nx=nx, steps=steps, stress=stress, cells=(16, nx // 2, nx - 17))
+
+
+def test_event_marks_time_the_advance():
+    import ctypes as C
+
+    dev, sce = _cfg2_small(stress=False)
+    s = mb.GpuFdtdSolver(dev, sce)
+    h = s.open_handle()
+    s.upload_initial_state(h)
+    h.call("mbg_mark", 0)
+    h.call("mbg_sample", 0)
+    h.call("mbg_mark", 1)
+    h.call("mbg_advance", 1, s.grid.num_t - 1)
+    h.call("mbg_mark", 2)
+    part, total = C.c_float(0), C.c_float(0)
+    h.call("mbg_mark_elapsed", 1, 2, C.byref(part))
+    h.call("mbg_mark_elapsed", 0, 2, C.byref(total))
+    assert 0.0 < part.value <= total.value
+    with pytest.raises(mb.NativeError):
+        h.call("mbg_mark_elapsed", 0, 7, C.byref(part))  # slot never recorded
+    h.close()
+
+
+def test_zero_field_upload_is_a_memset():
+    """mbg_upload_fields(NULL, NULL) == uploading explicit zero arrays; a half
+    NULL pair is an argument error."""
+    from paper_2005_05412_b200 import native
+
+    dev, sce = _cfg2_small(stress=False)
+    a = mb.GpuFdtdSolver(dev, sce)
+    assert a.plan.fields_zero
+    ra = a.run()
+    b = mb.GpuFdtdSolver(dev, sce)
+    h = b.open_handle()
+    e, hf = np.zeros(b.grid.num_x), np.zeros(b.grid.num_x + 1)
+    h.call("mbg_upload_fields", native.ptr(e), native.ptr(hf))
+    h.call("mbg_upload_density", native.ptr(native.f64(b.plan.rho_init_packed())))
+    with pytest.raises(mb.NativeError):
+        h.call("mbg_upload_fields", native.ptr(e), None)
+    b._ran = True
+    b._run_on(h)
+    rb = b.download_results(h)
+    h.close()
+    for x, y in zip(ra, rb):
+        assert np.array_equal(x.data, y.data), x.name
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_state_round_trip_through_the_relaxed_frame(exact):
+    """The fast two-level path keeps (X, Y, Z) = pre-relaxation vectors on the
+    device; uploads map in, downloads map out: a round trip returns the state
+    to rounding (bitwise in the exact variant, which keeps the reference's form)."""
+    from paper_2005_05412_b200 import native
+
+    dev, sce = _cfg2_small()
+    s = mb.GpuFdtdSolver(dev, sce, exact=exact)
+    h = s.open_handle()
+    s.upload_initial_state(h)
+    nx, w = s.grid.num_x, s.plan.state_words
+    rng = np.random.default_rng(3)
+    planes = np.zeros((w, nx))
+    cells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in s.plan.groups])
+    v = rng.normal(size=(3, cells.size))
+    v *= 0.9 / np.linalg.norm(v, axis=0)
+    planes[:, cells] = v
+    h.call("mbg_upload_state", native.ptr(native.f64(planes)))
+    back = np.zeros_like(planes)
+    h.call("mbg_download_state", native.ptr(back))
+    h.close()
+    if exact:
+        assert np.array_equal(back, planes)
+    else:
+        assert np.max(np.abs(back - planes)) <= 1e-15
