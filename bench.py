@@ -217,7 +217,8 @@ def run_mine(args, world, rank, local):
     dev, sce = build_workload(mb, args.gpus)
     if world > 1:
         from paper_2005_05412_b200 import slabs
-        return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT)
+        return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT, clock_sampler=ClockSampler,
+                                rebuild=lambda: build_workload(mb, args.gpus))
 
     solver = mb.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
     plan = solver.plan

@@ -344,10 +344,17 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     return assemble(solver.plan, slabs, gathered)
 
 
-def bench_rank(args, dev, sce, world, rank, local, metric, unit):
+def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=None, rebuild=None):
     """bench.py --gpus N under torchrun: weak-scaled cfg2, one slab per GPU,
-    device time of K full runs, max over ranks."""
+    device time of K full runs, max over ranks.
+
+    ``clock_sampler(gpu)``: context manager sampling clocks during the timed
+    region (bench.py's ClockSampler); ``rebuild()``: fresh (device, scenario)
+    for the end-to-end runs through run_slab_rank (the public multi-GPU call:
+    window upload, exchanges, record download and gather), wall-clocked with
+    barriers, max over ranks."""
     import json
+    import time
 
     import torch
     import torch.distributed as dist
@@ -389,11 +396,13 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
     st.h.call("mbg_launch_count", C.byref(l0))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
-        one_run()
-    t1.record(stream)
-    torch.cuda.synchronize(device)
+    sampler = clock_sampler(local) if clock_sampler is not None else _nullcontext()
+    with sampler:
+        t0.record(stream)
+        for _ in range(args.steps):
+            one_run()
+        t1.record(stream)
+        torch.cuda.synchronize(device)
     ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=device)
     dist.barrier()
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -405,22 +414,53 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit):
     if bad >= 0:
         raise SolverError(f"non-finite electric field at step {bad}")
     ms = float(ms.item())
+    cells = grid.num_x * (grid.num_t - 1) * args.steps
+
+    e2e = None
+    if rebuild is not None:
+        walls = []
+        for it in range(args.warmup + args.steps):
+            d2, s2 = rebuild()
+            sol = GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+            torch.cuda.synchronize(device)
+            dist.barrier()
+            w0 = time.perf_counter()
+            run_slab_rank(sol, world, rank, device)
+            torch.cuda.synchronize(device)
+            w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=device)
+            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            if it >= args.warmup:
+                walls.append(float(w.item()))
+        plan = solver.plan
+        mine = slabs[rank]
+        fields = 0 if plan.fields_zero else 2 * (mine.win_hi - mine.win_lo) + 1
+        h2d = 8 * (fields + plan.state_words + plan.src_values.size)
+        e2e = {"value": cells / sum(walls), "unit": unit, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(sum(p.rows * (mine.own_hi - mine.own_lo if p.cell is None else 1) *
+                                             (16 if p.is_complex else 8) for p in plan.plans
+                                             if p.cell is None or mine.own_lo <= p.cell < mine.own_hi)),
+               "note": "rank 0's bytes; wall clock around run_slab_rank (window upload, exchanges, record "
+                       "download + gather), max over ranks"}
     if rank == 0:
-        cells = grid.num_x * (grid.num_t - 1) * args.steps
         launches = l1.value - l0.value
         line = {
             "metric": metric, "value": cells / (ms * 1e-3), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"cfg2 weak-scaled: {world} slabs x 2^22 cells, 20000 steps",
+            "config": {"workload": f"cfg2 weak-scaled: {world} copies of the cfg2 device, {world} slabs x 2^22 "
+                                   f"cells, 20000 steps",
                        "num_x": grid.num_x, "tile_steps": k, "exchange_period": period,
                        "parallelism": f"slab{world}",
                        "exchange": f"NCCL batched isend/irecv of {period} ghost cells per interface every "
-                                   f"{period} steps (one persistent launch of {period // k} chunks between)"},
-            # this rank's kernels (step, edge, sample, halo pack/unpack; library count)
+                                   f"{period} steps (one persistent launch of {period // k} chunks between)",
+                       "l2": "inputs larger than L2 (~335 MB of state per GPU vs 126 MB L2)"},
+            "e2e": e2e,
+            # this rank's kernels (step, step-mask, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),
         }
+        if clock_sampler is not None:
+            line["clocks"] = sampler.summary()
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

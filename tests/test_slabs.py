@@ -160,6 +160,8 @@ def test_bench_rank_prints_a_line(capsys, monkeypatch):
     for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(_free_port())), ("RANK", "0"),
                      ("WORLD_SIZE", "1")):
         monkeypatch.setenv(key, val)
-    slabs.bench_rank(args, dev, sce, 1, 0, 0, "m", "cell-updates/s")
+    slabs.bench_rank(args, dev, sce, 1, 0, 0, "m", "cell-updates/s",
+                     rebuild=lambda: configs.cfg2(mb, nx=1 << 16, steps=512))
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
