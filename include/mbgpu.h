@@ -127,7 +127,12 @@ int mbg_download_state(mbg_solver *s, double *planes);
 
 /* run */
 int mbg_sample(mbg_solver *s, int64_t step);
-int mbg_advance(mbg_solver *s, int64_t first_step, int64_t n_steps); /* async */
+/* steps first_step .. first_step + n_steps - 1, asynchronous on the solver
+ * stream.  Two-level / classical media: one persistent wavefront launch for
+ * the whole range (unless MBG_FLAG_PER_LAUNCH); N >= 3 and RK4: one launch per
+ * k steps.  A windowed solver (slab) advances at most its ghost width. */
+int mbg_advance(mbg_solver *s, int64_t first_step, int64_t n_steps);
+/* waits for the stream; reports a persistent launch that gave up waiting */
 int mbg_synchronize(mbg_solver *s);
 int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step); /* syncs; -1 when all finite */
 /* invariant monitor of the current state (_kernels.py:394-401, solver_fdtd.py:428-440):
