@@ -107,12 +107,16 @@ def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", replica
     act = api.ensure_material(api.Material("SIT_2lvl_relax" + tag, qm=sit_medium(api, 1e9, 1e12)))
     dev = api.Device("cfg2")
     unit = 150e-6
+    x0 = 0.0
     for j in range(replicas):
-        x0 = unit * j
+        # each copy starts exactly where the previous one ended (the device
+        # refuses gaps/overlaps, and unit * j need not equal that end in fp64)
         sfx = f" {j}" if replicas > 1 else ""
-        dev.add_region(api.Region("vacuum left" + sfx, vac.id, x0, x0 + 7.5e-6))
-        dev.add_region(api.Region("medium" + sfx, act.id, x0 + 7.5e-6, x0 + unit - 7.5e-6))
-        dev.add_region(api.Region("vacuum right" + sfx, vac.id, x0 + unit - 7.5e-6, x0 + unit))
+        x1, x2, x3 = x0 + 7.5e-6, x0 + unit - 7.5e-6, x0 + unit
+        dev.add_region(api.Region("vacuum left" + sfx, vac.id, x0, x1))
+        dev.add_region(api.Region("medium" + sfx, act.id, x1, x2))
+        dev.add_region(api.Region("vacuum right" + sfx, vac.id, x2, x3))
+        x0 = x3
     ic_e = api.RandomField(1e7, seed=7) if stress else None
     sce = api.Scenario("cfg2", nx, _end_time(api, dev, nx, steps), cfg2_rho0(api), ic_e_field=ic_e)
     sce.add_source(sit_source(api))

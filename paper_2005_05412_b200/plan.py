@@ -377,14 +377,13 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None) -> Solve
         qm_index=qm_index,
     )
 
+    # maximal runs of cells in one region (solver_fdtd.py:276-285), vectorised
+    cuts = (np.flatnonzero(cell_region[1:] != cell_region[:-1]) + 1).tolist()
     groups = []
-    start = 0
-    for m in range(1, nx + 1):
-        if m == nx or cell_region[m] != cell_region[m - 1]:
-            r = int(cell_region[start])
-            if qm_index[r] >= 0:
-                groups.append((start, m, int(qm_index[r])))
-            start = m
+    for start, stop in zip([0] + cuts, cuts + [nx]):
+        r = int(cell_region[start])
+        if qm_index[r] >= 0:
+            groups.append((start, stop, int(qm_index[r])))
 
     srcs = list(scenario.sources)
     cells = [0 if nx == 1 else int(math.floor(s.position / dx + 0.5)) for s in srcs]

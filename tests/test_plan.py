@@ -112,6 +112,30 @@ def test_region_table_reproduces_per_cell_maps(case):
     assert cells["coef_ch"][0] == 0.0 and cells["coef_ch"][nx] == 0.0
 
 
+@pytest.mark.parametrize("replicas", [1, 2, 3, 8])
+def test_weak_scaling_device_builds_for_every_gpu_count(replicas):
+    """bench.py --gpus G: G copies of the cfg2 device side by side (G = 8 once
+    failed: replica starts unit * j did not equal the previous end in fp64)."""
+    mb.clear_material_library()
+    from paper_2005_05412_b200 import configs
+
+    nx = 4096 * replicas
+    dev, sce = configs.cfg2(mb, nx=nx, steps=10, replicas=replicas, cells=(16, nx // 2))
+    plan = mb.GpuFdtdSolver(dev, sce).plan
+    assert len(dev.regions) == 3 * replicas and len(plan.groups) == replicas
+    # the reference's per-cell group runs (solver_fdtd.py:276-285)
+    ends = np.array([r.x_end for r in dev.regions])
+    cell_region = np.minimum(np.searchsorted(ends, np.arange(nx) * plan.grid.dx, side="right"), len(ends) - 1)
+    runs = []
+    start = 0
+    for m in range(1, nx + 1):
+        if m == nx or cell_region[m] != cell_region[m - 1]:
+            if cell_region[start] % 3 == 1:
+                runs.append((start, m))
+            start = m
+    assert [(a, b) for a, b, _ in plan.groups] == runs
+
+
 @pytest.mark.parametrize("n,stepper", [(2, "splitting"), (2, "rk4"), (3, "splitting"), (6, "splitting")])
 def test_density_packing_round_trip(n, stepper):
     rng = np.random.default_rng(n)
