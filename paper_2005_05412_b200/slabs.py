@@ -198,23 +198,45 @@ class TorchTransport:
             return None if spec is None else torch.empty(w * spec[1], dtype=torch.float64, device=device)
 
         self.send_l, self.recv_l, self.send_r, self.recv_r = buf(sl), buf(rl), buf(sr), buf(rr)
+        # gloo moves host memory only: device buffers are staged through pinned
+        # host copies (CPU tests, and several ranks sharing one GPU); NCCL
+        # sends the device buffers directly
+        self.stage = (torch.device(device).type == "cuda" and dist.get_backend() == "gloo")
+        if self.stage:
+            def host(b):
+                return None if b is None else torch.empty(b.numel(), dtype=b.dtype, pin_memory=True)
+
+            self.h_send_l, self.h_recv_l = host(self.send_l), host(self.recv_l)
+            self.h_send_r, self.h_recv_r = host(self.send_r), host(self.recv_r)
 
     def exchange(self):
         sl, rl, sr, rr = self.plan
         st, dist = self.state, self.dist
         rank = st.slab.rank
         ops = []
+        if self.stage:
+            send_l, recv_l, send_r, recv_r = self.h_send_l, self.h_recv_l, self.h_send_r, self.h_recv_r
+        else:
+            send_l, recv_l, send_r, recv_r = self.send_l, self.recv_l, self.send_r, self.recv_r
         if sl is not None:
             st.pack_into(sl[0], sl[1], self.send_l)
-            ops.append(dist.P2POp(dist.isend, self.send_l, rank - 1))
-            ops.append(dist.P2POp(dist.irecv, self.recv_l, rank - 1))
+            ops.append(dist.P2POp(dist.isend, send_l, rank - 1))
+            ops.append(dist.P2POp(dist.irecv, recv_l, rank - 1))
         if sr is not None:
             st.pack_into(sr[0], sr[1], self.send_r)
-            ops.append(dist.P2POp(dist.isend, self.send_r, rank + 1))
-            ops.append(dist.P2POp(dist.irecv, self.recv_r, rank + 1))
+            ops.append(dist.P2POp(dist.isend, send_r, rank + 1))
+            ops.append(dist.P2POp(dist.irecv, recv_r, rank + 1))
+        if self.stage:
+            for d, h in ((self.send_l, send_l), (self.send_r, send_r)):
+                if d is not None:
+                    h.copy_(d)  # synchronous: the pack kernel has run
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if self.stage:
+            for d, h in ((self.recv_l, recv_l), (self.recv_r, recv_r)):
+                if d is not None:
+                    d.copy_(h)
         if rl is not None:
             st.unpack_from(rl[0], rl[1], self.recv_l)
         if rr is not None:
@@ -300,6 +322,38 @@ def tile_steps_of(solver) -> int:
         h.close()
 
 
+def _reduce_scalar(value, op, device, dtype=None):
+    """All-reduce one number: on the device under NCCL, on the host under gloo."""
+    import torch
+    import torch.distributed as dist
+
+    dtype = torch.float64 if dtype is None else dtype
+    where = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=dtype, device=where)
+    dist.all_reduce(t, op=op)
+    return t.item()
+
+
+def slab_backend(local: int):
+    """(backend, gpu) of a bench rank: NCCL on GPU ``local`` -- one process per
+    GPU, the production shape.  ``MBG_SLAB_BACKEND=gloo MBG_SLAB_GPU=g`` puts
+    every rank on GPU g with host-staged gloo exchanges instead: the whole
+    multi-rank driver (partition, halo exchange, scan-flag reduction, record
+    gather, timing) on a one-GPU box.  No kernel waits on another rank, since
+    the ranks meet only on the host.  NCCL ranks sharing a GPU are refused."""
+    import os
+
+    backend = os.environ.get("MBG_SLAB_BACKEND", "nccl")
+    if backend not in ("nccl", "gloo"):
+        raise ValueError(f"MBG_SLAB_BACKEND must be nccl or gloo, not {backend!r}")
+    shared = os.environ.get("MBG_SLAB_GPU")
+    if shared is not None:
+        if backend != "gloo":
+            raise ValueError("MBG_SLAB_GPU (several ranks on one GPU) needs MBG_SLAB_BACKEND=gloo")
+        local = int(shared)
+    return backend, local
+
+
 def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None):
     """This process's slab of a ``world``-way run (torch.distributed initialised).
     Returns the assembled records on rank 0 and None elsewhere.
@@ -328,9 +382,7 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
 
             def poll():
                 b = st.poll()
-                t = torch.tensor([b if b >= 0 else 2**62], dtype=torch.int64, device=device)
-                dist.all_reduce(t, op=dist.ReduceOp.MIN)
-                v = int(t.item())
+                v = int(_reduce_scalar(b if b >= 0 else 2**62, dist.ReduceOp.MIN, device, torch.int64))
                 return -1 if v == 2**62 else v
 
             _step_loop(solver.grid, period, st.advance, tr.exchange, poll)
@@ -354,6 +406,7 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
     window upload, exchanges, record download and gather), wall-clocked with
     barriers, max over ranks."""
     import json
+    import os
     import time
 
     import torch
@@ -361,10 +414,11 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
 
     from .solver import GpuFdtdSolver
 
+    backend, local = slab_backend(local)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=device)
+        dist.init_process_group(backend, device_id=device if backend == "nccl" else None)
     solver = GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
     k = tile_steps_of(solver)
     period = exchange_period(solver, k, world)
@@ -403,9 +457,8 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
             one_run()
         t1.record(stream)
         torch.cuda.synchronize(device)
-    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=device)
     dist.barrier()
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = _reduce_scalar(t0.elapsed_time(t1), dist.ReduceOp.MAX, device)
     l1 = C.c_int64(0)
     st.h.call("mbg_launch_count", C.byref(l1))
     bad = st.poll()
@@ -413,7 +466,7 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
     ctx.__exit__(None, None, None)
     if bad >= 0:
         raise SolverError(f"non-finite electric field at step {bad}")
-    ms = float(ms.item())
+    ms = float(ms)
     cells = grid.num_x * (grid.num_t - 1) * args.steps
 
     e2e = None
@@ -427,10 +480,9 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
             w0 = time.perf_counter()
             run_slab_rank(sol, world, rank, device)
             torch.cuda.synchronize(device)
-            w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=device)
-            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            w = _reduce_scalar(time.perf_counter() - w0, dist.ReduceOp.MAX, device)
             if it >= args.warmup:
-                walls.append(float(w.item()))
+                walls.append(w)
         plan = solver.plan
         mine = slabs[rank]
         fields = 0 if plan.fields_zero else 2 * (mine.win_hi - mine.win_lo) + 1
@@ -459,6 +511,10 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
             # this rank's kernels (step, step-mask, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),
         }
+        if backend != "nccl" or local != int(os.environ.get("LOCAL_RANK", local)):
+            line["config"]["shared_gpu"] = (f"all {world} ranks on GPU {local}, {backend} exchanges staged "
+                                            f"through the host: a functional run of the multi-rank path, "
+                                            f"not a scaling measurement")
         if clock_sampler is not None:
             line["clocks"] = sampler.summary()
         print(json.dumps(line), flush=True)

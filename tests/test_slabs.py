@@ -165,3 +165,71 @@ def test_bench_rank_prints_a_line(capsys, monkeypatch):
     line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+
+
+def _gpu_worker(rank, world, port, case, period, out_path):
+    """One rank of a gloo run whose slabs all live on cuda:0 (native kernels,
+    host-staged exchanges: the ranks only meet on the host)."""
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_05412_b200 as mbw
+    from paper_2005_05412_b200 import slabs as sl
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cases import CASES
+
+        build, stepper = CASES[case]
+        mbw.clear_material_library()
+        dev, sce = build(mbw)
+        torch.cuda.set_device(0)
+        solver = mbw.GpuFdtdSolver(dev, sce, stepper=stepper, gpu=0)
+        recs = sl.run_slab_rank(solver, world, rank, torch.device("cuda", 0), period=period)
+        if rank == 0:
+            np.savez(out_path, *[r.data for r in recs])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,case,period", [(2, "multi_material", None), (3, "cfg2_r16", None),
+                                               (2, "rand3_split", None), (2, "vacuum_sources", 100)])
+def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period):
+    """run_slab_rank across processes with the native slab kernels: the
+    TorchTransport exchange plan, pack/unpack on the adopted stream, scan-flag
+    reduction and record gather, bit-identical to the single-domain run."""
+    dev, sce, stepper = build_case(case)
+    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "recs.npz")
+        mp.spawn(_gpu_worker, args=(world, _free_port(), case, period, out), nprocs=world, join=True)
+        got = np.load(out)
+        for r, a in enumerate(ref):
+            have = got[f"arr_{r}"]
+            assert have.shape == a.data.shape, a.name
+            assert np.array_equal(have, a.data), (a.name, np.max(np.abs(have - a.data)))
+
+
+@pytest.mark.gpu
+def test_bench_under_torchrun_two_ranks_on_one_gpu():
+    """bench.py --gpus 2 exactly as the driver launches it (torchrun), both
+    ranks on cuda:0 with gloo (MBG_SLAB_GPU): one JSON line from rank 0."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, MBG_SLAB_BACKEND="gloo", MBG_SLAB_GPU="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "1"]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-4000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["num_x"] == 2 << 22 and "shared_gpu" in line["config"]
