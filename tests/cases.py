@@ -254,6 +254,88 @@ def kernel_case(dim, seed, stepper="splitting", nx=64):
     return build, stepper
 
 
+def qcl5(api):
+    """The reference's built-in tzenov2016 QCL comb setup (setups.py:212-277:
+    five levels with tunnelling couplings, one laser dipole, a dense
+    scattering matrix, split dephasing, losses 1100/m, overlap factor 0.9,
+    mirrors R = 0.8, random initial field) at its default 4096 cells, run
+    for 20 of its 200 ps.  make_golden.py checks this builder against
+    builtin_setup("tzenov2016") record for record."""
+    e0 = api.E0
+    h_off = np.zeros(10, dtype=complex)
+    h_off[1] = 1.2329e-3 * e0
+    h_off[2] = -1.3447e-3 * e0
+    mu_off = np.zeros(10, dtype=complex)
+    mu_off[5] = -e0 * 4e-9
+    rates = np.array([[0.0, 0.4947e12, 0.0974e12, 0.8116e12, 1.0410e12],
+                      [0.8245e12, 0.0, 0.1358e12, 0.6621e12, 1.1240e12],
+                      [0.0229e12, 0.0469e12, 0.0, 0.0794e12, 0.0357e12],
+                      [0.0047e12, 0.0029e12, 0.1252e12, 0.0, 0.2810e12],
+                      [0.0049e12, 0.0049e12, 0.1101e12, 0.4949e12, 0.0]])
+    deph = np.full(10, 1.0 / 1.0e-12)
+    deph[0] = 0.0
+    deph[1] = deph[2] = 1.0 / 0.6e-12
+    qm = api.QmDescription(5.6e21, api.QmOperator(np.array([0.10103, 0.09677, 0.09720, 0.08129, 0.07633]) * e0,
+                                                  h_off),
+                           api.QmOperator(np.zeros(5), mu_off), api.LindbladRelaxation(rates, deph))
+    act = api.ensure_material(api.Material("AR_Tzenov", rel_permittivity=12.96, overlap_factor=0.9, losses=1100.0,
+                                           qm=qm))
+    dev = api.Device("tzenov2016", bc_left=api.BoundaryReflectivity(0.8), bc_right=api.BoundaryReflectivity(0.8))
+    dev.add_region(api.Region("Active region", act.id, 0.0, 0.5e-3))
+    sce = api.Scenario("basic", 4096, 20e-12, api.QmOperator([0.0, 0.0, 1.0, 0.0, 0.0]),
+                       ic_e_field=api.RandomField(amplitude=3e4, seed=None))
+    sce.add_record(api.Record("e0", quantity="e", position=0.0))
+    sce.add_record(api.Record("e", quantity="e", interval=1e-12))
+    sce.add_record(api.Record("h", quantity="h", interval=1e-12))
+    return dev, sce
+
+
+def ladder6(api):
+    """The reference's built-in marskar2011 six-level anharmonic ladder
+    (setups.py:149-209) at its default 8192 cells, run for 1.2 of its 2000 ps
+    (the hard Gaussian pulse peaks at 600 fs); two probes added after the
+    setup's own records."""
+    levels = 6
+    w0 = 2.0 * math.pi * 1e13
+    energies = np.zeros(levels)
+    for n in range(1, levels):
+        energies[n] = energies[n - 1] + api.HBAR * w0 * (1.0 - 0.1 * (n - 3))
+    n_off = levels * (levels - 1) // 2
+    dipoles = np.zeros(n_off, dtype=complex)
+    rates = np.zeros((levels, levels))
+    k = 0
+    for j in range(1, levels):
+        for i in range(j):
+            if j == i + 1:
+                dipoles[k] = -api.E0 * 1e-10 * math.sqrt(i + 1.0)
+                rates[i, j] = 1e10
+            k += 1
+    qm = api.QmDescription(1e24, api.QmOperator(energies), api.QmOperator(np.zeros(levels), dipoles),
+                           api.LindbladRelaxation(rates, np.zeros(n_off)))
+    vac = api.ensure_material(api.Material("Vacuum"))
+    act = api.ensure_material(api.Material("AR_Marskar_6lvl", qm=qm))
+    dev = api.Device("Marskar_6lvl")
+    dev.add_region(api.Region("Vacuum left", vac.id, 0.0, 7.5e-6))
+    dev.add_region(api.Region("Active region", act.id, 7.5e-6, 142.5e-6))
+    dev.add_region(api.Region("Vacuum right", vac.id, 142.5e-6, 150e-6))
+    rho = np.zeros(levels)
+    rho[0] = 1.0
+    sce = api.Scenario("Basic", 8192, 1.2e-12, api.QmOperator(rho))
+    sce.add_record(api.Record("e", quantity="e", interval=1e-12))
+    sce.add_record(api.Record("d11", quantity="d", i=1, j=1, interval=1e-12, position=75e-6))
+    sce.add_source(api.GaussianPulse("gaussian", position=0.0, kind="hard", amplitude=1e9, carrier_freq=1e13,
+                                     peak_time=600e-15, width=200e-15))
+    sce.add_record(api.Record("e@20um", quantity="e", interval=10e-15, position=20e-6))
+    sce.add_record(api.Record("d12@20um", quantity="d", i=1, j=2, interval=10e-15, position=20e-6))
+    return dev, sce
+
+
+# the reference's built-in setups that the cases above do not already cover
+# (ziolkowski1995 ~ cfg1, song2005 = song_point): name -> (builtin args, case)
+BUILTIN_TWINS = {"qcl5": (("tzenov2016", None, 20e-12), 3), "ladder6": (("marskar2011-6lvl", None, 1.2e-12), 2)}
+
+CASES["qcl5"] = (qcl5, "splitting")
+CASES["ladder6"] = (ladder6, "splitting")
 CASES["bragg_stack"] = (bragg_stack, "splitting")
 CASES["song_point"] = (song_point, "splitting")
 CASES["song_point_rk4"] = (song_point, "rk4")

@@ -20,7 +20,7 @@ import paper_2005_05412_b200 as mb
 
 BITWISE = {"cfg1_full", "cfg2_r16", "cfg2_full", "cfg2_stress_full", "sit_hard_whole", "multi_material", "bragg_stack",
            "vacuum_sources", "rand2_split", "kernel2_split", "rand2_rk4", "kernel2_rk4"}
-LONG = {"cfg3_r16", "cfg3_r16_stress", "cfg4_r14", "cfg2_full", "cfg2_stress_full"}
+LONG = {"cfg3_r16", "cfg3_r16_stress", "cfg4_r14", "cfg2_full", "cfg2_stress_full", "ladder6"}
 NAMES = sorted(n for n in CASES if n not in LONG or os.environ.get("MBG_SLOW"))
 
 
