@@ -125,27 +125,34 @@ __device__ __forceinline__ double rcp_ge1(double d) {
 
 // Fast variant of bloch_cell_real on the relaxed-frame state (BlochFrame):
 // the two half relaxations of consecutive steps are one multiply (one FMA for
-// z), the rotation is regrouped around the field-independent products g*az
-// and 8/den (tolerance-level, not bitwise).  Returns X_new - X_old: the factor
+// z), the rotation is evaluated in Rodrigues form (below; tolerance-level,
+// not bitwise).  Returns X_new - X_old: the factor
 // pol_factor * mu_x * fxy is folded into the E update's coefficient (pol_coef).
 __device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const BlochReal &r, double e, double &x,
                                                         double &y, double &z) {
     const double x0 = x;
     const double x1 = r.f2 * x, y1 = r.f2 * y, z1 = fma(r.kz2, z, r.czz);
-    // the rotation with the factors 4 and 8 absorbed: q = 4/den = 1/((t1/2)^2 + u),
-    // nh = num/2, k1 = (nh^2 - qq) q, g = 2 nh q, dotb = 2 q (a . v1)
+    // The Cayley rotation in Rodrigues form around a = (ax, 0, az):
+    //   v2 = v1 + P (a x v1) + Q (a x (a x v1)),  P = 2 nh / D, Q = 2 / D,
+    //   nh = (1 + u - |a|^2) / 2,  D = nh^2 + |a|^2  (= ((1 - u + |a|^2)/2)^2 + u = W/4),
+    // the same rotation as the reference's k1 v1 + g (a x v1) + (8/W)(a.v1) a:
+    // cos = (nh^2 - |a|^2)/D, sin = 2 nh |a|/D.  With ay = 0 the y component
+    // of a x (a x v1) is -|a|^2 y1, and the x and z components share one factor:
+    //   x2 = x1 - 2az (ph y1 + iD cy),  z2 = z1 + 2ax (ph y1 + iD cy),
+    //   y2 = k1 y1 + 2 ph cy,  cy = az x1 - ax z1,  ph = nh/D, iD = 1/D, k1 = cos.
+    // 24 FP64 operations (30 in the g / dot-product grouping), tolerance-level
+    // against the reference (not bitwise).
     const double ax = q.ax_s * e, ax2 = r.axs2 * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
     const double nh = fma(-0.5, qq, r.c1h);
-    const double th = fma(0.5, qq, r.c2h);
-    const double iq = rcp_ge1(fma(th, th, r.u));
-    const double k1 = fma(nh, nh, -qq) * iq;
-    const double ph = nh * iq;
-    const double gaz = ph * r.az2x, gax = ph * ax2;
-    const double dh = iq * fma(az, z1, ax * x1);
-    x = fma(dh, ax2, fma(-gaz, y1, k1 * x1));
-    y = fma(-gax, z1, fma(gaz, x1, k1 * y1));
-    z = fma(dh, r.az2x, fma(gax, y1, k1 * z1));
+    const double iD = rcp_ge1(fma(nh, nh, qq));
+    const double k1 = fma(nh, nh, -qq) * iD;
+    const double ph = nh * iD;
+    const double cy = fma(az, x1, -(ax * z1));
+    const double in = fma(ph, y1, iD * cy);
+    x = fma(-r.az2x, in, x1);
+    y = fma(ph + ph, cy, k1 * y1);
+    z = fma(ax2, in, z1);
     return x - x0;
 }
 #define MBG_BLOCH_REAL bloch_cell_real_frame
