@@ -348,6 +348,8 @@ def run_mine(args, world, rank, local):
             d2h = sum(r.data.size * (16 if r.is_complex else 8) for r in res) + 8 * max(1, (num_t - 1) // (1 << 14))
     e2e_value = cell_updates / sum(e2e_times)
 
+    n_level = None if args.no_n_level else n_level_samples(local)
+
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_baseline(plan, 3 * args.cpu_steps)  # ~10 s of host work
@@ -362,9 +364,52 @@ def run_mine(args, world, rank, local):
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
+        # BASELINE configs[2], [3] (N = 3, N = 6) on one GPU, bounded samples beside the headline
+        "n_level": n_level,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def n_level_samples(local, chunks=16):
+    """BASELINE configs[2] / [3] on one GPU (N = 3 on 2^23 cells, N = 6 on 2^24
+    cells): device time of `chunks` fused launches from the initial state
+    (bounded samples of the 50000- / 100000-step runs; reported beside the
+    headline, not the headline), with the roofline of SURVEY 8(d)."""
+    import ctypes as C
+
+    import paper_2005_05412_b200 as mb
+    from paper_2005_05412_b200 import configs, native
+
+    peak = C.c_double(0)
+    native.load().mbg_fp64_peak(local, C.byref(peak))
+    out = {}
+    for name, n in (("cfg3", 3), ("cfg4", 6)):
+        mb.clear_material_library()
+        dev, sce = getattr(configs, name)(mb)
+        sol = mb.GpuFdtdSolver(dev, sce, gpu=local)
+        h = sol.open_handle()
+        sol.upload_initial_state(h)
+        k = C.c_int32(0)
+        h.call("mbg_tile_steps", C.byref(k))
+        steps = chunks * k.value
+        h.call("mbg_sample", 0)
+        h.call("mbg_checkpoint_save")
+        h.call("mbg_advance", 1, 2 * k.value)  # warm-up (clocks, modules)
+        h.call("mbg_checkpoint_restore")
+        h.call("mbg_event_begin")
+        h.call("mbg_advance", 1, steps)
+        ms = C.c_float(0)
+        h.call("mbg_event_end", C.byref(ms))
+        h.close()
+        rate = sol.grid.num_x * steps / (ms.value * 1e-3)
+        b, f, fq = algorithmic_per_cell(sol.plan)
+        out[name] = {"levels": n, "num_x": sol.grid.num_x, "tile_steps": k.value, "sampled_steps": steps,
+                     "of_steps": sol.grid.num_t - 1, "value": rate, "unit": UNIT,
+                     "algorithmic_flops_per_cell_update": f, "achieved_tflops": rate * f / 1e12,
+                     "fp64_peak_tflops": peak.value, "frac": rate * f / 1e12 / peak.value,
+                     "launches": chunks}
+    return out
 
 
 def cpu_baseline(plan, steps):
@@ -394,6 +439,7 @@ def main(argv=None):
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-n-level", action="store_true", help="skip the N = 3 / N = 6 samples")
     args = ap.parse_args(argv)
     world, rank, local = dist_env()
     if args.gpus != world:
