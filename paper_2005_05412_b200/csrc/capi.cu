@@ -95,6 +95,7 @@ int fail(mbg_solver *s, int code, const std::string &msg) {
 
 int default_tile_steps(int levels, int stepper) {
     if (levels <= 2 && stepper == MBG_STEPPER_SPLITTING) return 64;
+    if (levels == 3 && stepper == MBG_STEPPER_SPLITTING) return 12;  // cfg3 sweep: k = 8..16 within 2 %, 12 best
     if (levels <= 3) return 16;
     return 4;
 }
