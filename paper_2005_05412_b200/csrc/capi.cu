@@ -525,7 +525,7 @@ static bool pol_ok(int n, int npol, const int32_t *pi, const int32_t *pj, int nd
 int mbg_set_qm_dense(mbg_solver *s, int32_t q, const double *pop, const double *coh, const double *bc,
                      const double *bf, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
                      int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
-    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support 2 quantum materials");
+    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support at most MBG_MAX_QM quantum materials");
     const int n = s->g.levels;
     if (s->bloch || s->g.stepper != MBG_STEPPER_SPLITTING || n < 3)
         return fail(s, MBG_E_STATE, "solver is not an N>=3 splitting solver");
@@ -544,7 +544,7 @@ int mbg_set_qm_dense(mbg_solver *s, int32_t q, const double *pop, const double *
 int mbg_set_qm_rk4(mbg_solver *s, int32_t q, const double *h0, const double *mu, const double *popm,
                    const double *deph, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
                    int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
-    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support 2 quantum materials");
+    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support at most MBG_MAX_QM quantum materials");
     const int n = s->g.levels;
     if (s->g.stepper != MBG_STEPPER_RK4 || n < 2) return fail(s, MBG_E_STATE, "solver is not an RK4 solver");
     if (!pol_ok(n, npol, pi, pj, ndpol, pdi)) return fail(s, MBG_E_ARG, "bad dipole index list");

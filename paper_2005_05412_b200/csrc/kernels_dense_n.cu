@@ -12,6 +12,7 @@ namespace dense {
 
 template <int N, bool RK4, class Q>
 static cudaError_t launch_n(const void *params, long long tiles, cudaStream_t st) {
+    static_assert(sizeof(DenseParams<N, Q>) <= 32764, "kernel parameter block over the 32 KB launch limit");
     const auto &P = *static_cast<const DenseParams<N, Q> *>(params);
     constexpr size_t smem = Layout<N, RK4>::smem_bytes();
     static bool configured[64] = {};

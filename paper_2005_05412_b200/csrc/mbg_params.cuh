@@ -15,7 +15,7 @@ namespace mbg {
 
 constexpr int kMaxRegions = MBG_MAX_REGIONS;
 constexpr int kMaxQm = MBG_MAX_QM;
-constexpr int kMaxDenseQm = 2;
+constexpr int kMaxDenseQm = kMaxQm;  // param block: DenseParams<8, *> with 4 media stays under the 32 KB launch limit
 constexpr int kMaxSources = MBG_MAX_SOURCES;
 constexpr int kMaxRecords = MBG_MAX_RECORDS;
 constexpr int kMaxTileSteps = MBG_MAX_TILE_STEPS;

@@ -72,6 +72,8 @@ class GpuFdtdSolver:
             raise ValueError(f"the GPU solver supports at most {native.MAX_RECORDS} records")
         if len(self.plan.src_cells) > native.MAX_SOURCES:
             raise ValueError(f"the GPU solver supports at most {native.MAX_SOURCES} sources")
+        if len(self.plan.qm) > native.MAX_QM:
+            raise ValueError(f"the GPU solver supports at most {native.MAX_QM} distinct quantum materials")
         if len(self.plan.regions.e_start) > native.MAX_REGIONS:
             raise ValueError(f"the GPU solver supports at most {native.MAX_REGIONS} device regions")
 

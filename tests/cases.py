@@ -330,6 +330,36 @@ def ladder6(api):
     return dev, sce
 
 
+def four_media(api):
+    """Four distinct three-level media (random draws) separated by dielectric
+    spacers, partial mirrors, soft source: every constant-set slot of the
+    N-level kernels in use."""
+    rng = np.random.default_rng(44)
+    vac = api.ensure_material(api.Material("Vacuum"))
+    spacer = api.ensure_material(api.Material("Spacer", rel_permittivity=2.0, losses=200.0))
+    dev = api.Device("four", bc_left=api.BoundaryReflectivity(0.5), bc_right=api.BoundaryReflectivity(0.9))
+    dev.add_region(api.Region("lead", vac.id, 0.0, 3e-6))
+    x = 3e-6
+    for m in range(4):
+        desc = random_medium(api, rng, 3, rate_scale=10 ** (10 + m / 2), density=(m + 1) * 3e23)
+        mat = api.ensure_material(api.Material(f"Med3_{m}", rel_permittivity=1.0 + 0.5 * m, overlap_factor=1.0 - 0.1 * m,
+                                               qm=desc))
+        dev.add_region(api.Region(f"m{m}", mat.id, x, x + 4e-6))
+        dev.add_region(api.Region(f"s{m}", spacer.id, x + 4e-6, x + 5e-6))
+        x += 5e-6
+    sce = api.Scenario("s", 2400, 60e-15, api.QmOperator([0.8, 0.15, 0.05]), ic_e_field=api.RandomField(1e4, seed=9))
+    sce.add_source(api.SechPulse("sech", 1e-6, "soft", 2e9, 1.5e14, 6.0, 2e14))
+    sce.add_record(api.Record("e", quantity="e", interval=5e-15))
+    for m in range(4):
+        xm = 3e-6 + 5e-6 * m + 2e-6
+        sce.add_record(api.Record(f"d13@{m}", quantity="d", i=1, j=3, position=xm, interval=0.5e-15))
+        sce.add_record(api.Record(f"d22@{m}", quantity="d", i=2, j=2, position=xm, interval=0.5e-15))
+    return dev, sce
+
+
+CASES["four_media"] = (four_media, "splitting")
+CASES["four_media_rk4"] = (four_media, "rk4")
+
 # the reference's built-in setups that the cases above do not already cover
 # (ziolkowski1995 ~ cfg1, song2005 = song_point): name -> (builtin args, case)
 BUILTIN_TWINS = {"qcl5": (("tzenov2016", None, 20e-12), 3), "ladder6": (("marskar2011-6lvl", None, 1.2e-12), 2)}
