@@ -298,14 +298,19 @@ def run_slabs_local(solver, slabs_count: int, period=None):
 
 
 CHUNKS_PER_EXCHANGE = 32
+# N-level / RK4 slabs: launches of k steps between exchanges (cfg5 per-rank
+# rate flat from 4 to 32 launches per exchange, tools/slab_step.py, profiles/)
+LAUNCHES_PER_EXCHANGE = 4
 
 
 def exchange_period(solver, k: int, world: int) -> int:
     """Steps between halo exchanges (= ghost width): m fused chunks of k steps,
     at most the thinnest slab.  The two-level / classical kernels run the m
-    chunks as one persistent launch."""
+    chunks as one persistent launch; the N-level / RK4 kernels as m launches,
+    each computing the window minus k cells per side (the valid region shrinks
+    k cells per launch into the ghosts, as in the persistent kernel)."""
     dense = solver.plan.levels > 2 or (solver.plan.levels == 2 and solver.stepper == "rk4")
-    period = k if dense else CHUNKS_PER_EXCHANGE * k
+    period = (LAUNCHES_PER_EXCHANGE if dense else CHUNKS_PER_EXCHANGE) * k
     return max(1, min(period, solver.grid.num_x // max(1, world)))
 
 

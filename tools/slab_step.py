@@ -1,9 +1,14 @@
 """Per-rank cost of the slab path on one GPU (what one rank of `bench.py
 --gpus G` does, minus the NCCL transfer): the middle slab of a G-way
-weak-scaled cfg2, advanced period steps at a time with both halos packed and
+weak-scaled run, advanced period steps at a time with both halos packed and
 unpacked (into a scratch buffer, self-looped) after every period.
 
-    python tools/slab_step.py [--world 3] [--period P] [--steps 20000]
+    python tools/slab_step.py [--config cfg2|cfg5] [--world 3] [--period P] [--tile-steps K] [--steps S]
+
+cfg2: G copies of the two-level cfg2 device (2^22 cells per rank).  cfg5:
+BASELINE configs[4], the six-level cfg4 medium on 2^22 cells per rank; the
+exchange period P (= ghost width) may exceed the tile depth k (P/k fused
+launches between exchanges).
 """
 import argparse
 import ctypes as C
@@ -19,12 +24,17 @@ import paper_2005_05412_b200 as mb  # noqa: E402
 from paper_2005_05412_b200 import configs, slabs  # noqa: E402
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2", choices=("cfg2", "cfg5"))
+ap.add_argument("--tile-steps", type=int, default=None)
 ap.add_argument("--world", type=int, default=3)
 ap.add_argument("--period", type=int, default=0)
 ap.add_argument("--steps", type=int, default=20000)
 a = ap.parse_args()
-dev, sce = configs.cfg2(mb, nx=(1 << 22) * a.world, steps=a.steps, replicas=a.world)
-solver = mb.GpuFdtdSolver(dev, sce)
+if a.config == "cfg2":
+    dev, sce = configs.cfg2(mb, nx=(1 << 22) * a.world, steps=a.steps, replicas=a.world)
+else:
+    dev, sce = configs.cfg5(mb, gpus=a.world, steps=a.steps)
+solver = mb.GpuFdtdSolver(dev, sce, tile_steps=a.tile_steps)
 k = slabs.tile_steps_of(solver)
 period = a.period or slabs.exchange_period(solver, k, a.world)
 part = slabs.partition(solver.grid.num_x, a.world, period)
