@@ -249,13 +249,16 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
 // Same derivative for N >= 4 with H = h0 - E mu formed row by row on the fly
 // (a full H would hold 2N^2 doubles in registers).  The empty asm on the
 // field value keeps the compiler from caching H rows across (i, j) pairs.
-template <int N, class VS0, class VD>
-__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VS0 &src0, VD &dst) {
+// The source is the stage state A + c K (c = 0: A alone), formed while it is
+// read into registers, so no stage buffer is kept in shared memory; dst may
+// be K itself (every source word is read before the first write).
+template <int N, class VA, class VK, class VD>
+__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA &a0, VK &k0, double c, VD &dst) {
     constexpr double kInvHbar = 1.0 / 1.054571817e-34;
     // one pass over the shared-memory state into registers: every entry is used 2N times
     RegVec<N * N> src;
 #pragma unroll
-    for (int w = 0; w < N * N; ++w) src[w] = src0[w];
+    for (int w = 0; w < N * N; ++w) src[w] = c == 0.0 ? a0[w] : mad(c, k0[w], a0[w]);  // c is a literal per call
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double ei = e;
@@ -297,15 +300,9 @@ __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VS0
     }
 }
 
-template <int N, class VS, class VD>
-__device__ __forceinline__ void rhs(const Rk4Qm<N> &q, double e, const double *hr, const double *hi, VS &src,
-                                    VD &dst) {
-    if constexpr (N >= 4)
-        master_rhs_rows<N>(q, e, src, dst);
-    else
-        master_rhs<N>(q, hr, hi, src, dst);
-}
-
+// Classical RK4 on the packed state.  Registers (N <= 3): explicit stage
+// state S.  Shared memory (N >= 4): S is never stored -- each derivative reads
+// A + c K on the fly (the same mad(c, K, A) values), three buffers instead of four.
 template <int N, class VA, class VB>
 __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, VB &S, VB &K, VB &Acc) {
     constexpr int NW = N * N;
@@ -319,26 +316,38 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
         }
     }
     const double dt = q.dt;
-    // k1
-    rhs<N>(q, e, hr, hi, A, K);
+    if constexpr (N >= 4) {
+        master_rhs_rows<N>(q, e, A, K, 0.0, K);  // k1
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        Acc[w] = K[w];
-        S[w] = mad(0.5 * dt, K[w], A[w]);
-    }
-    rhs<N>(q, e, hr, hi, S, K);  // k2
+        for (int w = 0; w < NW; ++w) Acc[w] = K[w];
+        master_rhs_rows<N>(q, e, A, K, 0.5 * dt, K);  // k2
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        Acc[w] = mad(2.0, K[w], Acc[w]);
-        S[w] = mad(0.5 * dt, K[w], A[w]);
-    }
-    rhs<N>(q, e, hr, hi, S, K);  // k3
+        for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
+        master_rhs_rows<N>(q, e, A, K, 0.5 * dt, K);  // k3
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        Acc[w] = mad(2.0, K[w], Acc[w]);
-        S[w] = mad(dt, K[w], A[w]);
+        for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
+        master_rhs_rows<N>(q, e, A, K, dt, K);  // k4
+    } else {
+        master_rhs<N>(q, hr, hi, A, K);  // k1
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            Acc[w] = K[w];
+            S[w] = mad(0.5 * dt, K[w], A[w]);
+        }
+        master_rhs<N>(q, hr, hi, S, K);  // k2
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            Acc[w] = mad(2.0, K[w], Acc[w]);
+            S[w] = mad(0.5 * dt, K[w], A[w]);
+        }
+        master_rhs<N>(q, hr, hi, S, K);  // k3
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            Acc[w] = mad(2.0, K[w], Acc[w]);
+            S[w] = mad(dt, K[w], A[w]);
+        }
+        master_rhs<N>(q, hr, hi, S, K);  // k4
     }
-    rhs<N>(q, e, hr, hi, S, K);  // k4
     const double sixth = dt / 6.0;
     double acc_p = 0.0;
 #pragma unroll
@@ -370,7 +379,7 @@ struct Layout {
     static constexpr bool kRegState = RK4 ? (N <= 3) : (N <= 4);
     static constexpr bool kRegG = N <= 6;
     // smem words per thread: A/B (or A/S/K/Acc for RK4) when not in registers, G when not in regs
-    static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 4 * NW : 2 * NW);
+    static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 3 * NW : 2 * NW);
     static constexpr int kGWords = (RK4 || kRegG) ? 0 : 2 * NW;
     static constexpr int kFieldWords = 6;  // Es[2], Hs[2], Ho[2]
     static constexpr int TW = tile_width<N, RK4>();
@@ -386,8 +395,8 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
             RegVec<NW> S, K, Acc;
             return rk4_cell<N>(q, e, A, S, K, Acc);
         } else {
-            SmemVec<TW> As{col}, S{col + NW * TW}, K{col + 2 * NW * TW}, Acc{col + 3 * NW * TW};
-            return rk4_cell<N>(q, e, As, S, K, Acc);
+            SmemVec<TW> As{col}, K{col + NW * TW}, Acc{col + 2 * NW * TW};
+            return rk4_cell<N>(q, e, As, K, K, Acc);  // S unused (stage states formed on the fly)
         }
     } else {
         if constexpr (Lay::kRegState) {

@@ -38,7 +38,11 @@ constexpr int kBlochCtaTile = kBlochWarpsPerBlock * kBlochTile;
 // dense kernels: one thread per cell, one CTA per tile
 // dense kernels: one thread per cell, one CTA per tile; small N use wide tiles
 // (less redundant halo) at 128 registers, large N narrow tiles (state in smem)
-__host__ __device__ constexpr int dense_tile_width(int n, bool rk4) { return n <= 3 ? 256 : (n <= 6 ? 128 : 64); }
+// (six-level RK4: 96-cell tiles, so two CTAs of three shared-memory state
+// buffers fit an SM)
+__host__ __device__ constexpr int dense_tile_width(int n, bool rk4) {
+    return n <= 3 ? 256 : (rk4 && n == 6 ? 96 : (n <= 6 ? 128 : 64));
+}
 __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <= 3 ? 2 : 1; }
 
 // One persistent launch of the two-level kernel over many fused chunks
