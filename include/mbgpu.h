@@ -141,6 +141,16 @@ int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step); /* syncs; -1 when all 
 int mbg_invariants(mbg_solver *s, double *out);
 int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols);
 int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im);
+/* Streamed records (the reference keeps every row in host memory,
+ * solver_fdtd.py:164-172, 398-424; here only a window of rows lives in HBM):
+ * mbg_set_record_rows gives record r a device window of `cap` rows starting
+ * at row 0 (after mbg_set_records); steps may only write rows inside the
+ * window (mbg_advance / mbg_sample refuse otherwise); completed rows are
+ * copied out with mbg_download_record_rows into the caller's host rows
+ * [row_lo, row_hi) and the window is moved on with mbg_set_record_row0. */
+int mbg_set_record_rows(mbg_solver *s, int32_t r, int64_t cap);
+int mbg_download_record_rows(mbg_solver *s, int32_t r, int64_t row_lo, int64_t row_hi, double *re, double *im);
+int mbg_set_record_row0(mbg_solver *s, int32_t r, int64_t row0);
 
 /* multi-device slabs: pack/unpack `count` cells starting at global cell
  * `cell0` of E, H and every state plane into/out of a device buffer of

@@ -38,6 +38,7 @@ struct QmHost {
 struct Rec {
     int q = 0, i = 0, j = 0;
     long long cell = -1, every = 1, rows = 0, cols = 0, col0 = 0;
+    long long row0 = 0, cap = 0;  // device rows [row0, row0 + cap) (cap < rows: streamed)
     double *re = nullptr, *im = nullptr;
 };
 
@@ -146,6 +147,7 @@ Launch base_launch(const mbg_solver *s) {
         L.rec_every[r] = R.every;
         L.rec_cols[r] = R.cols;
         L.rec_col0[r] = R.col0;
+        L.rec_row0[r] = R.row0;
         L.rec_re[r] = R.re;
         L.rec_im[r] = R.im;
     }
@@ -611,6 +613,8 @@ int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *q, const int64_t *c
         R.rows = (s->g.num_t - 1) / R.every + 1;
         R.cols = R.cell >= 0 ? 1 : s->g.own_hi - s->g.own_lo;
         R.col0 = R.cell >= 0 ? R.cell : s->g.own_lo;
+        R.row0 = 0;
+        R.cap = R.rows;
         const size_t bytes = sizeof(double) * (size_t)R.rows * R.cols;
         CK(dalloc(s->stream, &R.re, bytes));
         CK(cudaMemsetAsync(R.re, 0, bytes, s->stream));
@@ -699,9 +703,20 @@ int mbg_download_state(mbg_solver *s, double *planes) {
     return MBG_OK;
 }
 
+// every record row that steps [first, last] write lies in its device window
+static bool rows_resident(const mbg_solver *s, long long first, long long last) {
+    for (const Rec &R : s->recs) {
+        if (R.cap >= R.rows || last < first) continue;
+        const long long lo = (first + R.every - 1) / R.every, hi = last / R.every;  // rows written
+        if (lo <= hi && (lo < R.row0 || hi >= R.row0 + R.cap)) return false;
+    }
+    return true;
+}
+
 int mbg_sample(mbg_solver *s, int64_t step) {
     if (!s) return MBG_E_ARG;
     if (!s->have_regions) return fail(s, MBG_E_STATE, "regions not set");
+    if (!rows_resident(s, step, step)) return fail(s, MBG_E_ARG, "record row of this step is not device-resident");
     cudaSetDevice(s->g.device);
     if (int rc = sync_frame(s)) return rc;
     const Launch L = base_launch(s);
@@ -873,6 +888,8 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     if (int rc = check_ready(s)) return rc;
     if (first < 1 || n_steps < 0 || first + n_steps > s->g.num_t)
         return fail(s, MBG_E_ARG, "step range outside 1 .. num_t-1");
+    if (!rows_resident(s, first, first + n_steps - 1))
+        return fail(s, MBG_E_ARG, "record rows of this step range are not device-resident (streamed records)");
     const long long ghost_l = s->g.own_lo - s->g.win_lo, ghost_r = s->g.win_hi - s->g.own_hi;
     const bool windowed = s->g.win_lo > 0 || s->g.win_hi < s->g.num_x;
     if (windowed) {
@@ -963,10 +980,58 @@ int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *col
     return MBG_OK;
 }
 
+int mbg_set_record_rows(mbg_solver *s, int32_t r, int64_t cap) {
+    if (!s || r < 0 || r >= (int)s->recs.size()) return MBG_E_ARG;
+    Rec &R = s->recs[r];
+    if (cap < 1 || cap > R.rows) return fail(s, MBG_E_ARG, "record row capacity outside [1, rows]");
+    cudaSetDevice(s->g.device);
+    dfree(s->stream, R.re);
+    dfree(s->stream, R.im);
+    R.re = R.im = nullptr;
+    R.row0 = 0;
+    R.cap = cap;
+    const size_t bytes = sizeof(double) * (size_t)cap * R.cols;
+    CK(dalloc(s->stream, &R.re, bytes));
+    CK(cudaMemsetAsync(R.re, 0, bytes, s->stream));
+    if (R.q == MBG_Q_D && R.i != R.j) {
+        CK(dalloc(s->stream, &R.im, bytes));
+        CK(cudaMemsetAsync(R.im, 0, bytes, s->stream));
+    }
+    return MBG_OK;
+}
+
+int mbg_download_record_rows(mbg_solver *s, int32_t r, int64_t row_lo, int64_t row_hi, double *re, double *im) {
+    if (!s || r < 0 || r >= (int)s->recs.size() || (!re && row_hi > row_lo)) return MBG_E_ARG;
+    const Rec &R = s->recs[r];
+    if (row_lo < R.row0 || row_hi < row_lo || row_hi > R.row0 + R.cap || row_hi > R.rows)
+        return fail(s, MBG_E_ARG, "record rows outside the device-resident window");
+    if (row_hi == row_lo) return MBG_OK;
+    cudaSetDevice(s->g.device);
+    const size_t off = (size_t)(row_lo - R.row0) * R.cols;
+    const size_t bytes = sizeof(double) * (size_t)(row_hi - row_lo) * R.cols;
+    CK(cudaMemcpyAsync(re, R.re + off, bytes, cudaMemcpyDeviceToHost, s->stream));
+    if (R.im && im) CK(cudaMemcpyAsync(im, R.im + off, bytes, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return MBG_OK;
+}
+
+int mbg_set_record_row0(mbg_solver *s, int32_t r, int64_t row0) {
+    if (!s || r < 0 || r >= (int)s->recs.size()) return MBG_E_ARG;
+    Rec &R = s->recs[r];
+    if (row0 < 0 || row0 > R.rows) return fail(s, MBG_E_ARG, "record window start outside [0, rows]");
+    cudaSetDevice(s->g.device);
+    R.row0 = row0;
+    const size_t bytes = sizeof(double) * (size_t)R.cap * R.cols;
+    CK(cudaMemsetAsync(R.re, 0, bytes, s->stream));
+    if (R.im) CK(cudaMemsetAsync(R.im, 0, bytes, s->stream));
+    return MBG_OK;
+}
+
 int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im) {
     if (!s || r < 0 || r >= (int)s->recs.size() || !re) return MBG_E_ARG;
     cudaSetDevice(s->g.device);
     const Rec &R = s->recs[r];
+    if (R.cap < R.rows) return fail(s, MBG_E_STATE, "streamed record: use mbg_download_record_rows");
     const size_t bytes = sizeof(double) * (size_t)R.rows * R.cols;
     CK(cudaMemcpyAsync(re, R.re, bytes, cudaMemcpyDeviceToHost, s->stream));
     if (R.im && im) CK(cudaMemcpyAsync(im, R.im, bytes, cudaMemcpyDeviceToHost, s->stream));

@@ -51,7 +51,7 @@ __global__ void sample_kernel(const Launch L, int levels, int bloch, long long s
         if (step % L.rec_every[r]) continue;
         const long long cell = L.rec_cell[r];
         if (cell >= 0 && cell != c) continue;
-        const long long idx = (step / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+        const long long idx = (step / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
         double re = 0.0, im = 0.0;
         const int q = L.rec_q[r];
         if (q == MBG_Q_E) {

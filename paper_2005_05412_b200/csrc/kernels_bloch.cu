@@ -325,7 +325,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                     const long long cell = L.rec_cell[r];
                     if (cell >= 0 && cell != c) continue;
                     const long long col = cell >= 0 ? 0 : c - L.rec_col0[r];
-                    const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + col;
+                    const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + col;
                     double vre = 0.0, vim = 0.0;
                     switch (L.rec_q[r]) {
                         case MBG_Q_E: vre = E[i]; break;
@@ -479,7 +479,7 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                     if (!((mask >> r) & 1ull)) continue;
                     const long long cell = L.rec_cell[r];
                     if (cell >= 0 && cell != c) continue;
-                    const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+                    const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
                     double vre = 0.0, vim = 0.0;
                     switch (L.rec_q[r]) {
                         case MBG_Q_E: vre = E[i]; break;

@@ -495,7 +495,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
                 if (!((mask >> r) & 1ull)) continue;
                 const long long cell = L.rec_cell[r];
                 if (cell >= 0 && cell != c) continue;
-                const long long idx = (n / L.rec_every[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+                const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
                 double vre = 0.0, vim = 0.0;
                 const int qq = L.rec_q[r];
                 if (qq == MBG_Q_E) {

@@ -60,6 +60,7 @@ struct Launch {
     long long rec_every[kMaxRecords];
     long long rec_cols[kMaxRecords];
     long long rec_col0[kMaxRecords];  // global cell of column 0
+    long long rec_row0[kMaxRecords];  // first row resident on the device (streamed records; 0 otherwise)
     double *rec_re[kMaxRecords];
     double *rec_im[kMaxRecords];
     unsigned long long step_mask[kMaxTileSteps];  // bit r: record r samples at fused step s

@@ -69,6 +69,9 @@ SIGNATURES = {
     "mbg_invariants": (C.c_int, [_h, _dp]),
     "mbg_record_shape": (C.c_int, [_h, C.c_int32, _i64p, _i64p]),
     "mbg_download_record": (C.c_int, [_h, C.c_int32, _dp, _dp]),
+    "mbg_set_record_rows": (C.c_int, [_h, C.c_int32, C.c_int64]),
+    "mbg_download_record_rows": (C.c_int, [_h, C.c_int32, C.c_int64, C.c_int64, _dp, _dp]),
+    "mbg_set_record_row0": (C.c_int, [_h, C.c_int32, C.c_int64]),
     "mbg_halo_words": (C.c_int, [_h, _i32p]),
     "mbg_pack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
     "mbg_unpack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),

@@ -28,6 +28,10 @@ from .plan import build_plan, resolve_threads
 from .setup_model import Result, register_solver
 
 SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
+# records larger than this stream through a device window of rows ...
+RECORD_HBM_BYTES = 4 << 30
+# ... sized so one segment's rows take about this much device memory
+RECORD_SEGMENT_BYTES = 512 << 20
 
 
 def _result_class(scenario):
@@ -45,11 +49,17 @@ class GpuFdtdSolver:
       ``exact``      -- disable FMA contraction (bit-exact two-level path),
       ``gpu``        -- CUDA device ordinal,
       ``persistent`` -- two-level / classical runs: one persistent wavefront
-                        launch per advance (False: one launch per k steps).
+                        launch per advance (False: one launch per k steps),
+      ``record_segment`` -- stream the records: keep only the rows of this
+                        many time steps in HBM and copy completed rows into
+                        the host result arrays after every segment (None:
+                        automatic -- streamed when the records would take
+                        more than RECORD_HBM_BYTES of device memory; 0: never).
     """
 
     def __init__(self, device, scenario, stepper="splitting", threads=None, seed=None,
-                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=True):
+                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=True,
+                 record_segment=None):
         self.plan = build_plan(device, scenario, stepper, seed)
         self.device = device
         self.scenario = scenario
@@ -63,6 +73,8 @@ class GpuFdtdSolver:
         self.exact = bool(exact)
         self.gpu = int(gpu)
         self.persistent = bool(persistent)
+        self.record_segment = record_segment
+        self._host_rows = None
         self.results = None
         self.launches = 0
         self.kernel_ms = None
@@ -166,12 +178,64 @@ class GpuFdtdSolver:
     def download_results(self, h):
         out = []
         for r, p in enumerate(self.plan.plans):
-            re = np.zeros((p.rows, p.cols))
-            im = np.zeros((p.rows, p.cols)) if p.is_complex else None
-            h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
+            if self._host_rows is not None:  # streamed: the rows are already on the host
+                re, im = self._host_rows[r]
+            else:
+                re = np.zeros((p.rows, p.cols))
+                im = np.zeros((p.rows, p.cols)) if p.is_complex else None
+                h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
             data = re if im is None else re + 1j * im
             out.append(p.to_result(self.grid, data, self._result_cls))
         return out
+
+    # -- streamed records ---------------------------------------------------------
+
+    def _segment_steps(self) -> int:
+        """Steps per streamed record segment (0: records stay whole in HBM)."""
+        seg = self._segment_unaligned()
+        monitor = self._monitor_cadence()
+        if seg and monitor is not None:  # segments end on invariant-monitor steps
+            seg = max(1, seg // monitor) * monitor
+        return seg
+
+    def _segment_unaligned(self) -> int:
+        if self.record_segment is not None:
+            return max(0, int(self.record_segment))
+        plans = self.plan.plans
+        total = sum(p.rows * p.cols * (16 if p.is_complex else 8) for p in plans)
+        if total <= RECORD_HBM_BYTES:
+            return 0
+        # rows of S steps for every record within RECORD_SEGMENT_BYTES
+        per_step = sum(p.cols * (16 if p.is_complex else 8) / p.every for p in plans)
+        return max(1024, int(RECORD_SEGMENT_BYTES / per_step) // 1024 * 1024)
+
+    def _open_streams(self, h, segment):
+        """Device windows of floor(S/every) + 1 rows; full host arrays (the
+        reference keeps every row in host memory, solver_fdtd.py:164-172)."""
+        self._host_rows = []
+        self._row0 = []
+        for r, p in enumerate(self.plan.plans):
+            cap = min(p.rows, segment // p.every + 1)
+            if cap < p.rows:
+                h.call("mbg_set_record_rows", r, cap)
+            re = np.zeros((p.rows, p.cols))
+            im = np.zeros((p.rows, p.cols)) if p.is_complex else None
+            self._host_rows.append((re, im))
+            self._row0.append(0)
+
+    def _drain_streams(self, h, last_step):
+        """Copy every row completed up to ``last_step`` to the host and move
+        each record's device window past it."""
+        for r, p in enumerate(self.plan.plans):
+            done = min(p.rows, last_step // p.every + 1)
+            lo = self._row0[r]
+            if done <= lo:
+                continue
+            re, im = self._host_rows[r]
+            h.call("mbg_download_record_rows", r, lo, done, native.ptr(re[lo:done]),
+                   native.ptr(im[lo:done]) if im is not None else None)
+            h.call("mbg_set_record_row0", r, done)
+            self._row0[r] = done
 
     # -- run ------------------------------------------------------------------
 
@@ -194,11 +258,16 @@ class GpuFdtdSolver:
         device-side non-finite flag between chunks (a chunk is a multiple of the
         1024-step scan cadence, so the first failing scan is the one reported)."""
         num_t = self.grid.num_t
+        segment = self._segment_steps()
+        if segment:
+            self._open_streams(h, segment)
         h.call("mbg_sample", 0)
         monitor = self._monitor_cadence()
         if monitor is not None:
             self._update_invariants(h)
         chunk = poll_every if monitor is None else max(1, monitor)
+        if segment:
+            chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
         n = 1
         h.call("mbg_event_begin")
         while n < num_t:
@@ -209,6 +278,8 @@ class GpuFdtdSolver:
             h.call("mbg_poll_nonfinite", C.byref(bad))
             if bad.value >= 0:
                 raise SolverError(f"non-finite electric field at step {bad.value}")
+            if segment:
+                self._drain_streams(h, n - 1)
             if monitor is not None and (n - 1) % monitor == 0:
                 self._update_invariants(h)
         ms = C.c_float(0)

@@ -346,3 +346,56 @@ def test_state_round_trip_through_the_relaxed_frame(exact):
         assert np.array_equal(back, planes)
     else:
         assert np.max(np.abs(back - planes)) <= 1e-15
+
+
+@pytest.mark.parametrize("case", ["sit_hard_whole", "multi_material", "rand3_split", "four_media_rk4", "cfg2_r16"])
+@pytest.mark.parametrize("segment", [1, 37, 1000])
+def test_streamed_records_equal_resident_records(case, segment):
+    """Records streamed through a device window of rows (copied to the host
+    after every segment of `segment` steps) equal the HBM-resident records bit
+    for bit, for point and whole-domain, real and complex records."""
+    dev, sce, stepper = build_case(case)
+    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case(case)
+    got = mb.GpuFdtdSolver(dev, sce, stepper=stepper, record_segment=segment).run()
+    for a, b in zip(ref, got):
+        assert a.name == b.name and a.data.shape == b.data.shape
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), (case, segment, a.name)
+
+
+def test_records_stream_automatically_past_the_device_budget(monkeypatch):
+    from paper_2005_05412_b200 import solver as S
+
+    dev, sce, stepper = build_case("sit_hard_whole")
+    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    monkeypatch.setattr(S, "RECORD_HBM_BYTES", 1 << 10)
+    monkeypatch.setattr(S, "RECORD_SEGMENT_BYTES", 1 << 16)
+    mb.clear_material_library()
+    dev, sce, stepper = build_case("sit_hard_whole")
+    sol = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    assert sol._segment_steps() >= 1024
+    got = sol.run()
+    assert sol._host_rows is not None
+    for a, b in zip(ref, got):
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
+
+
+def test_advance_refuses_rows_outside_the_device_window():
+    from paper_2005_05412_b200 import native
+
+    dev, sce, stepper = build_case("sit_hard_whole")
+    sol = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    h = sol.open_handle()
+    try:
+        sol.upload_initial_state(h)
+        every = sol.plan.plans[0].every
+        h.call("mbg_set_record_rows", 0, 2)  # rows 0 and 1 resident
+        h.call("mbg_sample", 0)
+        h.call("mbg_advance", 1, every)  # writes row 1: fine
+        with pytest.raises(native.NativeError):
+            h.call("mbg_advance", every + 1, every)  # would write row 2
+        with pytest.raises(native.NativeError):
+            h.call("mbg_download_record", 0, native.ptr(np.zeros(10)), None)
+    finally:
+        h.close()
