@@ -138,20 +138,19 @@ __device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const 
     // the same rotation as the reference's k1 v1 + g (a x v1) + (8/W)(a.v1) a:
     // cos = (nh^2 - |a|^2)/D, sin = 2 nh |a|/D.  With ay = 0 the y component
     // of a x (a x v1) is -|a|^2 y1, and the x and z components share one factor:
-    //   x2 = x1 - 2az (ph y1 + iD cy),  z2 = z1 + 2ax (ph y1 + iD cy),
-    //   y2 = k1 y1 + 2 ph cy,  cy = az x1 - ax z1,  ph = nh/D, iD = 1/D, k1 = cos.
-    // 24 FP64 operations (30 in the g / dot-product grouping), tolerance-level
+    //   x2 = x1 - 2az s,  z2 = z1 + 2ax s,  s = (nh y1 + cy) / D,
+    //   y2 = ((nh^2 - |a|^2) y1 + 2 nh cy) / D,  cy = az x1 - ax z1.
+    // 23 FP64 operations (30 in the g / dot-product grouping), tolerance-level
     // against the reference (not bitwise).
     const double ax = q.ax_s * e, ax2 = r.axs2 * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
     const double nh = fma(-0.5, qq, r.c1h);
     const double iD = rcp_ge1(fma(nh, nh, qq));
-    const double k1 = fma(nh, nh, -qq) * iD;
-    const double ph = nh * iD;
+    const double nm = fma(nh, nh, -qq);  // D cos
     const double cy = fma(az, x1, -(ax * z1));
-    const double in = fma(ph, y1, iD * cy);
+    const double in = iD * fma(nh, y1, cy);
     x = fma(-r.az2x, in, x1);
-    y = fma(ph + ph, cy, k1 * y1);
+    y = iD * fma(nm, y1, (nh + nh) * cy);
     z = fma(ax2, in, z1);
     return x - x0;
 }
