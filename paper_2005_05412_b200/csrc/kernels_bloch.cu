@@ -362,18 +362,6 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
     }
 }
 
-// Interior tiles (the overwhelming majority): every slot is a regular cell of
-// the window (1 <= c <= Nx-2), one E region and one H region, no source and no
-// boundary cell.  A CTA of 4 warps owns kBlochCtaTile consecutive cells;
-// inside a warp the layout is blocked (lane l holds C consecutive cells), so
-// the stencil needs one shuffle of E up and one of H down per lane and step,
-// and the two cells at each warp seam go through double-buffered shared
-// slots (two barriers per step).  For a single quantum material the stepper
-// constants are constant-bank operands.
-struct NoHook {
-    __device__ void operator()() const {}
-};
-
 // record masks / scan flags of the chunk being stepped, staged by the hook
 // (read after the first step's barriers)
 __shared__ unsigned long long s_mask[kMaxTileSteps];
@@ -401,6 +389,14 @@ struct SharedSpan {
     __device__ long long base() const { return tile_base(L, it.lo); }
 };
 
+// Interior tiles (the overwhelming majority): every slot is a regular cell of
+// the window (1 <= c <= Nx-2), one E region and one H region, no source and no
+// boundary cell.  A CTA of kBlochWarpsPerBlock warps owns kBlochCtaTile
+// consecutive cells; inside a warp the layout is blocked (lane l holds C
+// consecutive cells), so the stencil needs one shuffle of E up and one of H
+// down per lane and step, and the two cells at each warp seam go through
+// double-buffered shared slots (two barriers per step).  For a single quantum
+// material the stepper constants are constant-bank operands.
 // hook(): runs once the tile's loads are in flight, before the first step
 // (the persistent kernel stages its step masks and claims its next item there)
 template <bool QM, bool ONE_QM, bool REAL, bool A1, class Span, class Hook>
