@@ -419,6 +419,13 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
 // region, no source/boundary (no per-cell predicates, scalar coefficients);
 // ONE_QM: the stepper constants are compile-time offsets into the parameter
 // block (constant-bank operands of the FP64 instructions).
+// Register economy around the density step when the state lives in shared
+// memory (N >= 5, at the 255-register limit): the cell's E and new H are
+// re-read from the shared exchange slots after the step, the E-update
+// coefficients are read after it and the cell / window indices re-derived
+// from the tile base where used, so little but the step's own values is live
+// across it (cfg4 4.32e9 -> 4.64e9).  Register-state kernels (N <= 4) and
+// RK4 keep them in registers, which measured faster there.
 template <int N, bool RK4, class Q, bool INTERIOR, bool ONE_QM>
 __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *sm, long long t_lo, long long t_hi,
                                            long long base) {
@@ -428,30 +435,40 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     double *col = sm + 6 * W + threadIdx.x;  // per-thread state column
     const Launch &L = P.L;
     const long long nx = L.num_x;
+    constexpr bool kLean = !Lay::kRegState && !RK4;  // splitting N >= 5 (RK4 measured 1.5 % slower lean)
     const int j = threadIdx.x;
-    const long long c = base + j;
-    const long long l = c - L.win_lo;
-    const bool in_e = INTERIOR || (l >= 0 && l < L.win_n && c < nx);
-    double E = in_e ? L.e_in[l] : 0.0;
-    double H = (INTERIOR || (l >= 0 && l <= L.win_n)) ? L.h_in[l] : 0.0;
-    const int re = region_of(L.rg.e_start, L.rg.n, INTERIOR ? base : c);
-    const int rh = region_of(L.rg.h_start, L.rg.n, INTERIOR ? base : c);
-    const double ca = L.rg.a[re], cbg = L.rg.bg[re], cbdx = L.rg.bdx[re], cch = L.rg.ch[rh];
+    const long long c0 = base + j, l0 = c0 - L.win_lo;
+    const auto cell = [&]() { return kLean ? base + j : c0; };
+    const auto loc = [&]() { return kLean ? base + j - L.win_lo : l0; };
+    const bool in_e = INTERIOR || (l0 >= 0 && l0 < L.win_n && c0 < nx);
+    double E = in_e ? L.e_in[l0] : 0.0;
+    double H = (INTERIOR || (l0 >= 0 && l0 <= L.win_n)) ? L.h_in[l0] : 0.0;
+    const int re = region_of(L.rg.e_start, L.rg.n, INTERIOR ? base : c0);
+    const int rh = region_of(L.rg.h_start, L.rg.n, INTERIOR ? base : c0);
     const int qi = in_e ? L.rg.qm[re] : -1;
+    // E-update coefficients: held from here (register state) or read per step (lean)
+    const double ca0 = kLean ? 0.0 : L.rg.a[re], cbg0 = kLean ? 0.0 : L.rg.bg[re];
+    const double cbdx0 = kLean ? 0.0 : L.rg.bdx[re], cch0 = kLean ? 0.0 : L.rg.ch[rh];
     const Q &q = P.qm[ONE_QM ? 0 : (qi < 0 ? 0 : qi)];
     RegVec<NW> rA;
     if (qi >= 0) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const double v = L.s_in[w * L.plane + l];
+            const double v = L.s_in[w * L.plane + l0];
             if constexpr (Lay::kRegState) rA[w] = v; else col[w * W] = v;
         }
     }
-    const bool upd_h = INTERIOR || (c >= 1 && c <= nx - 1);
-    const bool upd_e = INTERIOR || (nx > 1 && c >= 0 && c < nx);
-    const bool left_edge = !INTERIOR && L.has_boundary && base == 0 && j == 0;
-    const bool right_edge = !INTERIOR && L.has_boundary && c == nx - 1;
-    const bool own = c >= t_lo && c < t_hi && c >= L.own_lo && c < L.own_hi;
+    const bool own0 = c0 >= t_lo && c0 < t_hi && c0 >= L.own_lo && c0 < L.own_hi;
+    const auto own = [&]() {
+        if constexpr (kLean) {
+            const long long c = cell();
+            return c >= t_lo && c < t_hi && c >= L.own_lo && c < L.own_hi;
+        } else {
+            return own0;
+        }
+    };
+    const auto upd_h = [&]() { return INTERIOR || (cell() >= 1 && cell() <= nx - 1); };
+    const auto upd_e = [&]() { return INTERIOR || (nx > 1 && cell() >= 0 && cell() < nx); };
 
     for (int s = 0; s < L.k; ++s) {
         const long long n = L.n0 + s;
@@ -460,22 +477,28 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
         if (!INTERIOR) Ho[b + j] = H;
         __syncthreads();
         const double el = j > 0 ? Es[b + j - 1] : 0.0;
-        const double hn = upd_h ? mad(cch, E - el, H) : H;
-        Hs[b + j] = hn;
+        const double hn0 = upd_h() ? mad(kLean ? L.rg.ch[rh] : cch0, E - el, H) : H;
+        Hs[b + j] = hn0;
         double p = 0.0;
         if (qi >= 0) p = cell_step<N, RK4>(q, E, col, rA);
         __syncthreads();
+        // lean: E and H of this cell back from the exchange slots (not live across the step)
+        if constexpr (kLean) E = Es[b + j];
+        const double hn = kLean ? Hs[b + j] : hn0;
         const double hr = j < W - 1 ? Hs[b + j + 1] : 0.0;
-        double en = upd_e ? mad(cbdx, hr - hn, mad(ca, E, -(cbg * p))) : E;
+        const double ca = kLean ? L.rg.a[re] : ca0, cbg = kLean ? L.rg.bg[re] : cbg0;
+        const double cbdx = kLean ? L.rg.bdx[re] : cbdx0;
+        double en = upd_e() ? mad(cbdx, hr - hn, mad(ca, E, -(cbg * p))) : E;
         if (!INTERIOR) {
-            if (left_edge) {
+            const long long c = cell();
+            if (L.has_boundary && base == 0 && j == 0) {
                 const double e_at = mad(L.l_c, Es[b + 1], L.l_omc * E);
                 const double h_at = 0.5 * (Ho[b + 1] + hr);
                 en = L.l_hw * mad(L.l_z, h_at, e_at);
             }
-            if (right_edge) {
+            if (L.has_boundary && c == nx - 1) {
                 const double e_at = mad(L.r_c, el, L.r_omc * E);
-                const double h_at = 0.5 * (H + hn);
+                const double h_at = 0.5 * (Ho[b + j] + hn);
                 en = L.r_hw * mad(-L.r_z, h_at, e_at);
             }
             for (int qq = 0; qq < L.n_src; ++qq) {
@@ -489,13 +512,14 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
         H = hn;
         const unsigned long long mask = L.step_mask[s];
         const bool check = L.check[s] != 0;
-        if ((mask || check) && own) {
+        if ((mask || check) && own()) {
+            const long long c = cell();
             if (check && !isfinite(E)) atomicMin(L.bad_step, (unsigned long long)n);
             for (int r = 0; r < L.n_rec; ++r) {
                 if (!((mask >> r) & 1ull)) continue;
-                const long long cell = L.rec_cell[r];
-                if (cell >= 0 && cell != c) continue;
-                const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + (cell >= 0 ? 0 : c - L.rec_col0[r]);
+                const long long rc = L.rec_cell[r];
+                if (rc >= 0 && rc != c) continue;
+                const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + (rc >= 0 ? 0 : c - L.rec_col0[r]);
                 double vre = 0.0, vim = 0.0;
                 const int qq = L.rec_q[r];
                 if (qq == MBG_Q_E) {
@@ -538,7 +562,9 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
             }
         }
     }
+    const long long c = cell();
     if (c >= t_lo && c < t_hi) {
+        const long long l = loc();
         L.e_out[l] = E;
         L.h_out[l] = H;
         if (qi >= 0) {
