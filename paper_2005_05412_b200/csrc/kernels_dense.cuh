@@ -91,8 +91,8 @@ __device__ __forceinline__ double recip_pos(double d) {
 
 // ---------------------------------------------------------------------------
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
-template <int N, class VA, class VB, class MG>
-__device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G) {
+template <int N, class VA, class VB, class MG, class VR>
+__device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G, VR &raw) {
     // relaxation half step -> B
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -148,7 +148,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
 #pragma unroll
     for (int i = 0; i < N; ++i) G.r(i, i) -= 1.0;
     // rho' = U r1 U^H, one row at a time; second relaxation half step fused
-    double acc_p = 0.0, raw[N];
+    double acc_p = 0.0;  // raw[i]: row i's diagonal before the second half relaxation
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         double tr[N], ti[N];
@@ -381,9 +381,13 @@ struct Layout {
     // smem words per thread: A/B (or A/S/K/Acc for RK4) when not in registers, G when not in regs
     static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 3 * NW : 2 * NW);
     static constexpr int kGWords = (RK4 || kRegG) ? 0 : 2 * NW;
+    // shared-memory splitting: the congruence's raw diagonal in shared memory too
+    static constexpr int kRawWords = (RK4 || kRegState) ? 0 : N;
     static constexpr int kFieldWords = 6;  // Es[2], Hs[2], Ho[2]
     static constexpr int TW = tile_width<N, RK4>();
-    static constexpr size_t smem_bytes() { return sizeof(double) * TW * (kFieldWords + kStateWords + kGWords); }
+    static constexpr size_t smem_bytes() {
+        return sizeof(double) * TW * (kFieldWords + kStateWords + kGWords + kRawWords);
+    }
 };
 
 template <int N, bool RK4, class Q>
@@ -402,15 +406,16 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
         if constexpr (Lay::kRegState) {
             RegVec<NW> B;
             RegMat<N> G;
-            return split_cell<N>(q, e, A, B, G);
+            RegVec<N> raw;
+            return split_cell<N>(q, e, A, B, G, raw);
         } else if constexpr (Lay::kRegG) {
-            SmemVec<TW> As{col}, B{col + NW * TW};
+            SmemVec<TW> As{col}, B{col + NW * TW}, raw{col + 2 * NW * TW};
             RegMat<N> G;
-            return split_cell<N>(q, e, As, B, G);
+            return split_cell<N>(q, e, As, B, G, raw);
         } else {
-            SmemVec<TW> As{col}, B{col + NW * TW};
+            SmemVec<TW> As{col}, B{col + NW * TW}, raw{col + 4 * NW * TW};
             SmemMat<N, TW> G{{col + 2 * NW * TW}, {col + 3 * NW * TW}};
-            return split_cell<N>(q, e, As, B, G);
+            return split_cell<N>(q, e, As, B, G, raw);
         }
     }
 }
