@@ -175,6 +175,24 @@ void fill_split(DenseQm<N> &d, const QmHost &h) {
     d.pol.pol_factor = h.pol_factor;
 }
 
+// B = I + i a (H0 - E mu) with a real A = a (H0 - E mu): Re(b_const) = I and
+// Re(b_field) = 0 exactly (real H0 and dipole; _kernels.py:437-439)
+template <int N>
+bool real_hamiltonian(const QmHost &h) {
+    for (int i = 0; i < N * N; ++i)
+        if (h.bc[2 * i] != (i % (N + 1) == 0 ? 1.0 : 0.0) || h.bf[2 * i] != 0.0) return false;
+    return true;
+}
+
+// MBG_REAL_A=0: always the complex inversion (A/B timing)
+inline bool disable_real_a() {
+    static const bool off = [] {
+        const char *v = std::getenv("MBG_REAL_A");
+        return v && v[0] == '0';
+    }();
+    return off;
+}
+
 template <int N>
 void fill_rk4(Rk4Qm<N> &d, const QmHost &h, double dt) {
     for (int i = 0; i < N * N; ++i) {
@@ -211,7 +229,11 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
         auto *P = new DenseParams<N, DenseQm<N>>();
         P->L = L;
         P->n_qm = (int)s->qm.size();
-        for (int q = 0; q < P->n_qm; ++q) fill_split<N>(P->qm[q], s->qm[q]);
+        P->real_a = P->n_qm > 0 && !disable_real_a();
+        for (int q = 0; q < P->n_qm; ++q) {
+            fill_split<N>(P->qm[q], s->qm[q]);
+            P->real_a &= real_hamiltonian<N>(s->qm[q]) ? 1 : 0;
+        }
         cudaError_t e = s->g.exact ? exact::launch_dense_split(N, P, tiles, s->stream)
                                    : fast::launch_dense_split(N, P, tiles, s->stream);
         delete P;

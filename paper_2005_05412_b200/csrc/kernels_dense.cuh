@@ -91,7 +91,7 @@ __device__ __forceinline__ double recip_pos(double d) {
 
 // ---------------------------------------------------------------------------
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
-template <int N, class VA, class VB, class MG, class VR>
+template <int N, bool RA, class VA, class VB, class MG, class VR>
 __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G, VR &raw) {
     // relaxation half step -> B
 #pragma unroll
@@ -108,6 +108,67 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             B[wre(N, i, j)] = A[wre(N, i, j)] * q.coh[i * N + j];
             B[wim(N, i, j)] = A[wim(N, i, j)] * q.coh[i * N + j];
         }
+    if constexpr (RA) {
+        // Real Hamiltonian and dipole (fast variant): A real symmetric, so
+        // 2 (I + iA)^-1 = 2 (I - iA)(I + A^2)^-1 = 2P - 2iAP with P = (I + A^2)^-1
+        // real, obtained by a real in-place Gauss-Jordan of (I + A^2)/2 (SPD,
+        // ~I/2, no pivoting): a quarter of the complex inversion's work.
+        // G.m <- Ah = A/2 (the host's halved constants), G.r <- (I + A^2)/2
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = i; j < N; ++j) {
+                G.m(i, j) = mad(e, q.bf_im[i * N + j], q.bc_im[i * N + j]);
+                if (j != i) G.m(j, i) = G.m(i, j);
+            }
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = i; j < N; ++j) {
+                double acc = G.m(i, 0) * G.m(0, j);
+#pragma unroll
+                for (int k = 1; k < N; ++k) acc = mad(G.m(i, k), G.m(k, j), acc);
+                G.r(i, j) = mad(2.0, acc, i == j ? 0.5 : 0.0);  // (I + A^2)/2 = I/2 + 2 Ah^2
+                if (j != i) G.r(j, i) = G.r(i, j);
+            }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const double ip = recip_pos(G.r(k, k));
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+                if (j != k) G.r(k, j) *= ip;
+            G.r(k, k) = ip;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                if (i == k) continue;
+                const double f = G.r(i, k);
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (j != k) G.r(i, j) = mad(-f, G.r(k, j), G.r(i, j));
+                G.r(i, k) = -f * ip;
+            }
+        }
+        // G.r = 2P; imaginary part -2AP = -2 Ah (2P), row by row in place: row
+        // i of the product reads only row i of Ah (its lower part, j < i, still
+        // holds Ah; the upper part is overwritten once the row is done)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double t[N];
+#pragma unroll
+            for (int j = i; j < N; ++j) {
+                double acc = G.m(i, 0) * G.r(0, j);
+#pragma unroll
+                for (int k = 1; k < N; ++k) acc = mad(G.m(i, k), G.r(k, j), acc);
+                t[j] = -2.0 * acc;
+            }
+#pragma unroll
+            for (int j = i; j < N; ++j) G.m(i, j) = t[j];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = 0; j < i; ++j) G.m(i, j) = G.m(j, i);
+    } else {
     // G = (B/2)^-1 = 2 (I + iA)^-1: the host halves bc and bf (exact), so the
     // Gauss-Jordan inverse (in place, no pivoting) is already 2(I + iA)^-1
 #pragma unroll
@@ -143,6 +204,7 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             G.r(i, k) = mad(-fr, ir, fi * ii);
             G.m(i, k) = mad(-fr, ii, -(fi * ir));
         }
+    }
     }
     // U = 2(I + iA)^-1 - I = G - I
 #pragma unroll
@@ -390,7 +452,7 @@ struct Layout {
     }
 };
 
-template <int N, bool RK4, class Q>
+template <int N, bool RK4, bool RA, class Q>
 __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, RegVec<N * N> &A) {
     using Lay = Layout<N, RK4>;
     constexpr int NW = N * N, TW = Lay::TW;
@@ -407,15 +469,15 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
             RegVec<NW> B;
             RegMat<N> G;
             RegVec<N> raw;
-            return split_cell<N>(q, e, A, B, G, raw);
+            return split_cell<N, RA>(q, e, A, B, G, raw);
         } else if constexpr (Lay::kRegG) {
             SmemVec<TW> As{col}, B{col + NW * TW}, raw{col + 2 * NW * TW};
             RegMat<N> G;
-            return split_cell<N>(q, e, As, B, G, raw);
+            return split_cell<N, RA>(q, e, As, B, G, raw);
         } else {
             SmemVec<TW> As{col}, B{col + NW * TW}, raw{col + 4 * NW * TW};
             SmemMat<N, TW> G{{col + 2 * NW * TW}, {col + 3 * NW * TW}};
-            return split_cell<N>(q, e, As, B, G, raw);
+            return split_cell<N, RA>(q, e, As, B, G, raw);
         }
     }
 }
@@ -431,7 +493,7 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
 // from the tile base where used, so little but the step's own values is live
 // across it (cfg4 4.32e9 -> 4.64e9).  Register-state kernels (N <= 4) and
 // RK4 keep them in registers, which measured faster there.
-template <int N, bool RK4, class Q, bool INTERIOR, bool ONE_QM>
+template <int N, bool RK4, class Q, bool INTERIOR, bool ONE_QM, bool RA>
 __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *sm, long long t_lo, long long t_hi,
                                            long long base) {
     using Lay = Layout<N, RK4>;
@@ -485,7 +547,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
         const double hn0 = upd_h() ? mad(kLean ? L.rg.ch[rh] : cch0, E - el, H) : H;
         Hs[b + j] = hn0;
         double p = 0.0;
-        if (qi >= 0) p = cell_step<N, RK4>(q, E, col, rA);
+        if (qi >= 0) p = cell_step<N, RK4, RA>(q, E, col, rA);
         __syncthreads();
         // lean: E and H of this cell back from the exchange slots (not live across the step)
         if constexpr (kLean) E = Es[b + j];
@@ -582,6 +644,20 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     }
 }
 
+template <int N, bool RK4, class Q, bool RA>
+__device__ __forceinline__ void dense_dispatch(const DenseParams<N, Q> &P, double *sm, long long t_lo, long long t_hi,
+                                               long long base) {
+    using Lay = Layout<N, RK4>;
+    if (tile_is_interior(P.L, base, Lay::TW)) {
+        if (P.n_qm == 1)
+            dense_tile<N, RK4, Q, true, true, RA>(P, sm, t_lo, t_hi, base);
+        else
+            dense_tile<N, RK4, Q, true, false, RA>(P, sm, t_lo, t_hi, base);
+    } else {
+        dense_tile<N, RK4, Q, false, false, RA>(P, sm, t_lo, t_hi, base);
+    }
+}
+
 template <int N, bool RK4, class Q>
 __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
     using Lay = Layout<N, RK4>;
@@ -591,14 +667,15 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) 
     if (t_lo >= L.res_hi) return;  // uniform per block
     const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
     const long long base = tile_base(L, t_lo);
-    if (tile_is_interior(L, base, Lay::TW)) {
-        if (P.n_qm == 1)
-            dense_tile<N, RK4, Q, true, true>(P, sm, t_lo, t_hi, base);
-        else
-            dense_tile<N, RK4, Q, true, false>(P, sm, t_lo, t_hi, base);
-    } else {
-        dense_tile<N, RK4, Q, false, false>(P, sm, t_lo, t_hi, base);
-    }
+#if defined(MBG_EXACT) && MBG_EXACT
+    constexpr bool kRa = false;  // the exact variant keeps the reference's complex inversion
+#else
+    constexpr bool kRa = !RK4;
+#endif
+    if (kRa && P.real_a)
+        dense_dispatch<N, RK4, Q, kRa>(P, sm, t_lo, t_hi, base);
+    else
+        dense_dispatch<N, RK4, Q, false>(P, sm, t_lo, t_hi, base);
 }
 
 }  // namespace dense

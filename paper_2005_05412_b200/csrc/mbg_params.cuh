@@ -159,6 +159,7 @@ template <int N, class Q>
 struct DenseParams {
     Launch L;
     int n_qm;
+    int real_a;  // every medium has a real Hamiltonian and dipole (fast variant: real inversion)
     Q qm[kMaxDenseQm];
 };
 
