@@ -184,6 +184,14 @@ bool real_hamiltonian(const QmHost &h) {
     return true;
 }
 
+// RK4 constants: H0 and the dipole real (_kernels.py:554-557)
+template <int N>
+bool real_operators(const QmHost &h) {
+    for (int i = 0; i < N * N; ++i)
+        if (h.h0[2 * i + 1] != 0.0 || h.mu[2 * i + 1] != 0.0) return false;
+    return true;
+}
+
 // MBG_REAL_A=0: always the complex inversion (A/B timing)
 inline bool disable_real_a() {
     static const bool off = [] {
@@ -219,7 +227,11 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
         auto *P = new DenseParams<N, Rk4Qm<N>>();
         P->L = L;
         P->n_qm = (int)s->qm.size();
-        for (int q = 0; q < P->n_qm; ++q) fill_rk4<N>(P->qm[q], s->qm[q], s->g.dt);
+        P->real_a = P->n_qm > 0 && !disable_real_a();
+        for (int q = 0; q < P->n_qm; ++q) {
+            fill_rk4<N>(P->qm[q], s->qm[q], s->g.dt);
+            P->real_a &= real_operators<N>(s->qm[q]) ? 1 : 0;
+        }
         cudaError_t e = s->g.exact ? exact::launch_dense_rk4(N, P, tiles, s->stream)
                                    : fast::launch_dense_rk4(N, P, tiles, s->stream);
         delete P;

@@ -274,7 +274,9 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
 // ---------------------------------------------------------------------------
 // RK4: f(src) = -i/hbar [H, src] + D(src) on packed Hermitian states.
 // Only the upper triangle + diagonal of the (Hermitian) derivative is formed.
-template <int N, class VS, class VD>
+// RH (fast variant, real H0 and dipole): H real, the commutator in half the
+// operations.
+template <int N, bool RH, class VS, class VD>
 __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, const double *hi, VS &src, VD &dst) {
     constexpr double kInvHbar = 1.0 / 1.054571817e-34;
 #pragma unroll
@@ -288,10 +290,15 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
                 double sr, si, tr, ti;
                 herm<N>(src, k, j, sr, si);
                 herm<N>(src, i, k, tr, ti);
-                const double ar = hr[i * N + k], ai = hi[i * N + k];
-                const double br = hr[k * N + j], bi = hi[k * N + j];
-                cr += mad(ar, sr, -(ai * si)) - mad(tr, br, -(ti * bi));
-                ci += mad(ar, si, ai * sr) - mad(tr, bi, ti * br);
+                const double ar = hr[i * N + k], br = hr[k * N + j];
+                if constexpr (RH) {
+                    cr += mad(ar, sr, -(tr * br));
+                    ci += mad(ar, si, -(ti * br));
+                } else {
+                    const double ai = hi[i * N + k], bi = hi[k * N + j];
+                    cr += mad(ar, sr, -(ai * si)) - mad(tr, br, -(ti * bi));
+                    ci += mad(ar, si, ai * sr) - mad(tr, bi, ti * br);
+                }
             }
             // -i/hbar * (cr + i ci) = (ci/hbar, -cr/hbar)
             double dr = ci * kInvHbar, di = -cr * kInvHbar;
@@ -314,7 +321,7 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
 // The source is the stage state A + c K (c = 0: A alone), formed while it is
 // read into registers, so no stage buffer is kept in shared memory; dst may
 // be K itself (every source word is read before the first write).
-template <int N, class VA, class VK, class VD>
+template <int N, bool RH, class VA, class VK, class VD>
 __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA &a0, VK &k0, double c, VD &dst) {
     constexpr double kInvHbar = 1.0 / 1.054571817e-34;
     // one pass over the shared-memory state into registers: every entry is used 2N times
@@ -329,7 +336,7 @@ __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA 
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             ar[k] = mad(-ei, q.mu_re[i * N + k], q.h0_re[i * N + k]);
-            ai[k] = mad(-ei, q.mu_im[i * N + k], q.h0_im[i * N + k]);
+            ai[k] = RH ? 0.0 : mad(-ei, q.mu_im[i * N + k], q.h0_im[i * N + k]);
         }
 #pragma unroll
         for (int j = i; j < N; ++j) {
@@ -343,9 +350,14 @@ __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA 
                 herm<N>(src, i, k, tr, ti);
                 // H_kj = conj(H_jk) (H is exactly Hermitian)
                 const double br = mad(-ej, q.mu_re[j * N + k], q.h0_re[j * N + k]);
-                const double bi = -mad(-ej, q.mu_im[j * N + k], q.h0_im[j * N + k]);
-                cr += mad(ar[k], sr, -(ai[k] * si)) - mad(tr, br, -(ti * bi));
-                ci += mad(ar[k], si, ai[k] * sr) - mad(tr, bi, ti * br);
+                if constexpr (RH) {
+                    cr += mad(ar[k], sr, -(tr * br));
+                    ci += mad(ar[k], si, -(ti * br));
+                } else {
+                    const double bi = -mad(-ej, q.mu_im[j * N + k], q.h0_im[j * N + k]);
+                    cr += mad(ar[k], sr, -(ai[k] * si)) - mad(tr, br, -(ti * bi));
+                    ci += mad(ar[k], si, ai[k] * sr) - mad(tr, bi, ti * br);
+                }
             }
             double dr = ci * kInvHbar, di = -cr * kInvHbar;
             if (i == j) {
@@ -365,7 +377,7 @@ __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA 
 // Classical RK4 on the packed state.  Registers (N <= 3): explicit stage
 // state S.  Shared memory (N >= 4): S is never stored -- each derivative reads
 // A + c K on the fly (the same mad(c, K, A) values), three buffers instead of four.
-template <int N, class VA, class VB>
+template <int N, bool RH, class VA, class VB>
 __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, VB &S, VB &K, VB &Acc) {
     constexpr int NW = N * N;
     constexpr int NH = N >= 4 ? 1 : N * N;
@@ -379,36 +391,36 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
     }
     const double dt = q.dt;
     if constexpr (N >= 4) {
-        master_rhs_rows<N>(q, e, A, K, 0.0, K);  // k1
+        master_rhs_rows<N, RH>(q, e, A, K, 0.0, K);  // k1
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = K[w];
-        master_rhs_rows<N>(q, e, A, K, 0.5 * dt, K);  // k2
+        master_rhs_rows<N, RH>(q, e, A, K, 0.5 * dt, K);  // k2
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
-        master_rhs_rows<N>(q, e, A, K, 0.5 * dt, K);  // k3
+        master_rhs_rows<N, RH>(q, e, A, K, 0.5 * dt, K);  // k3
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
-        master_rhs_rows<N>(q, e, A, K, dt, K);  // k4
+        master_rhs_rows<N, RH>(q, e, A, K, dt, K);  // k4
     } else {
-        master_rhs<N>(q, hr, hi, A, K);  // k1
+        master_rhs<N, RH>(q, hr, hi, A, K);  // k1
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             Acc[w] = K[w];
             S[w] = mad(0.5 * dt, K[w], A[w]);
         }
-        master_rhs<N>(q, hr, hi, S, K);  // k2
+        master_rhs<N, RH>(q, hr, hi, S, K);  // k2
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             Acc[w] = mad(2.0, K[w], Acc[w]);
             S[w] = mad(0.5 * dt, K[w], A[w]);
         }
-        master_rhs<N>(q, hr, hi, S, K);  // k3
+        master_rhs<N, RH>(q, hr, hi, S, K);  // k3
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
             Acc[w] = mad(2.0, K[w], Acc[w]);
             S[w] = mad(dt, K[w], A[w]);
         }
-        master_rhs<N>(q, hr, hi, S, K);  // k4
+        master_rhs<N, RH>(q, hr, hi, S, K);  // k4
     }
     const double sixth = dt / 6.0;
     double acc_p = 0.0;
@@ -459,10 +471,10 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
     if constexpr (RK4) {
         if constexpr (Lay::kRegState) {
             RegVec<NW> S, K, Acc;
-            return rk4_cell<N>(q, e, A, S, K, Acc);
+            return rk4_cell<N, RA>(q, e, A, S, K, Acc);
         } else {
             SmemVec<TW> As{col}, K{col + NW * TW}, Acc{col + 2 * NW * TW};
-            return rk4_cell<N>(q, e, As, K, K, Acc);  // S unused (stage states formed on the fly)
+            return rk4_cell<N, RA>(q, e, As, K, K, Acc);  // S unused (stage states formed on the fly)
         }
     } else {
         if constexpr (Lay::kRegState) {
@@ -670,7 +682,7 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) 
 #if defined(MBG_EXACT) && MBG_EXACT
     constexpr bool kRa = false;  // the exact variant keeps the reference's complex inversion
 #else
-    constexpr bool kRa = !RK4;
+    constexpr bool kRa = true;
 #endif
     if (kRa && P.real_a)
         dense_dispatch<N, RK4, Q, kRa>(P, sm, t_lo, t_hi, base);

@@ -357,6 +357,8 @@ def four_media(api):
     return dev, sce
 
 
+# cfg3's real three-level medium under RK4 (the real-operator derivative path)
+CASES["cfg3_rk4_r12"] = (lambda api: configs.cfg3(api, nx=1 << 12, steps=4000, cells=(300, 1100, 2500)), "rk4")
 CASES["four_media"] = (four_media, "splitting")
 CASES["four_media_rk4"] = (four_media, "rk4")
 
