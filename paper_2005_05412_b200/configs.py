@@ -160,14 +160,18 @@ def cfg3(api, nx=1 << 23, steps=50000, cells=None, stress=False, tag=""):
     return dev, sce
 
 
-def qcl6_medium(api, seed=4):
-    """Seeded six-level QCL-like medium (draw order of SURVEY 8(d) cfg 4)."""
+def qcl6_medium(api, seed=4, real=False):
+    """Seeded six-level QCL-like medium (draw order of SURVEY 8(d) cfg 4).
+    ``real``: drop the imaginary parts of the drawn couplings (same draws; a
+    real-Hamiltonian twin of the medium for timing the real-operator path)."""
     hbar, _ = _api_constants(api)
     rng = np.random.default_rng(seed)
     unit = 2.0 * math.pi * hbar
     spacing = rng.uniform(1e12, 4e12, 5) * unit
     energies = np.concatenate([[0.0], np.cumsum(spacing)])
     off_h = (rng.standard_normal(15) + 1j * rng.standard_normal(15)) * unit * 1e11
+    if real:
+        off_h = off_h.real.astype(complex)
     mu_nn = rng.uniform(1e-28, 5e-28, 5)
     rates = 10.0 ** rng.uniform(10, 12, (6, 6))
     np.fill_diagonal(rates, 0.0)
@@ -181,9 +185,10 @@ def qcl6_medium(api, seed=4):
         api.LindbladRelaxation(rates, np.full(15, 1e12)))
 
 
-def cfg4(api, nx=1 << 24, steps=100000, cells=None, length=2e-3, tag=""):
+def cfg4(api, nx=1 << 24, steps=100000, cells=None, length=2e-3, tag="", real=False):
     """Six-level QCL-like cavity, eps_r 12.96, R = 0.3, noise-seeded field."""
-    act = api.ensure_material(api.Material("QCL6" + tag, rel_permittivity=12.96, qm=qcl6_medium(api)))
+    act = api.ensure_material(api.Material("QCL6" + tag + ("r" if real else ""), rel_permittivity=12.96,
+                                           qm=qcl6_medium(api, real=real)))
     dev = api.Device("cfg4", bc_left=api.BoundaryReflectivity(0.3), bc_right=api.BoundaryReflectivity(0.3))
     dev.add_region(api.Region("cavity", act.id, 0.0, length))
     rho0 = np.zeros(6)

@@ -680,9 +680,12 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) 
     const long long t_hi = t_lo + L.tile_own < L.res_hi ? t_lo + L.tile_own : L.res_hi;
     const long long base = tile_base(L, t_lo);
 #if defined(MBG_EXACT) && MBG_EXACT
-    constexpr bool kRa = false;  // the exact variant keeps the reference's complex inversion
+    constexpr bool kRa = false;  // the exact variant keeps the reference's complex arithmetic
 #else
-    constexpr bool kRa = true;
+    // real operators: RK4 always; splitting for the register-state kernels
+    // (N <= 4: cfg3 6.28e10 -> 7.07e10) -- at six levels the extra phase of
+    // the real inversion costs more in spills than it saves (4.80e9 -> 4.30e9)
+    constexpr bool kRa = RK4 || Layout<N, RK4>::kRegState;
 #endif
     if (kRa && P.real_a)
         dense_dispatch<N, RK4, Q, kRa>(P, sm, t_lo, t_hi, base);

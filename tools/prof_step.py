@@ -26,8 +26,11 @@ ap.add_argument("--nx", type=int, default=0)
 ap.add_argument("--per-launch", action="store_true", help="one launch per k steps (no persistent kernel)")
 ap.add_argument("--advance-steps", type=int, default=0, help="steps per mbg_advance call (0: all at once)")
 ap.add_argument("--no-warm", action="store_true", help="single pass (for ncu)")
+ap.add_argument("--real", action="store_true", help="cfg4: the real-Hamiltonian twin of the medium")
 a = ap.parse_args()
 kw = {"nx": a.nx} if a.nx else {}
+if a.real:
+    kw["real"] = True
 total = max(400, a.steps)
 if a.config == "cfg5":
     dev, sce = configs.cfg5(mb, steps=total)
