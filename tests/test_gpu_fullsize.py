@@ -1,0 +1,62 @@
+"""Parity at BASELINE's full grid sizes: cfg3 (three levels, 2^23 cells) and
+cfg4 (six levels, 2^24 cells) advanced a few fused launches on the GPU and by
+the CPU oracle (OpenMP, all host cores) from the same initial state; the whole
+fields E, H and every cell's density matrix are compared (the golden records
+cover these media on reduced grids only: the full-grid oracle
+runs take hours to days).  cfg2 at full size is a golden case.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+from conftest import ROOT
+
+import paper_2005_05412_b200 as mb
+from paper_2005_05412_b200 import configs, native
+from paper_2005_05412_b200.plan import unpack_density
+
+sys.path.insert(0, str(ROOT / "oracle"))
+import oracle as orc  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.mark.parametrize("name,steps,kw", [("cfg3", 36, {}), ("cfg4", 12, {}), ("cfg4", 12, {"real": True})])
+def test_full_grid_prefix_matches_the_oracle(name, steps, kw):
+    import psutil
+
+    need = 48 << 30 if name == "cfg4" else 8 << 30  # oracle state (19 GB for 2^24 six-level cells) + plan
+    if psutil.virtual_memory().available < need:
+        pytest.skip(f"host memory below {need >> 30} GB for the full-grid oracle")
+    mb.clear_material_library()
+    dev, sce = getattr(configs, name)(mb, **kw)
+    sol = mb.GpuFdtdSolver(dev, sce)
+    plan = sol.plan
+    nx = sol.grid.num_x
+    h = sol.open_handle()
+    try:
+        sol.upload_initial_state(h)
+        h.call("mbg_sample", 0)
+        h.call("mbg_advance", 1, steps)
+        e = np.zeros(nx)
+        hf = np.zeros(nx + 1)
+        h.call("mbg_download_fields", native.ptr(e), native.ptr(hf))
+        words = np.zeros((plan.state_words, nx))
+        h.call("mbg_download_state", native.ptr(words))
+    finally:
+        h.close()
+
+    run = orc.OracleRun(plan, threads=os.cpu_count() or 1, step_limit=steps)
+    assert run.run() == 0
+    e_ref, h_ref = run.e, run.h
+    assert np.max(np.abs(e - e_ref)) <= TOL * np.max(np.abs(e_ref))
+    assert np.max(np.abs(hf - h_ref)) <= TOL * np.max(np.abs(h_ref))
+    cells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in plan.groups])
+    rho = unpack_density(words[:, cells], plan.levels, plan.stepper)
+    rho_ref = run.density()
+    assert rho.shape == rho_ref.shape
+    # density matrices are O(1): absolute error, and no cell may drift
+    assert np.max(np.abs(rho - rho_ref)) <= 1e-12
