@@ -399,3 +399,19 @@ def test_advance_refuses_rows_outside_the_device_window():
             h.call("mbg_download_record", 0, native.ptr(np.zeros(10)), None)
     finally:
         h.close()
+
+
+def test_streamed_records_with_the_invariant_monitor():
+    """Segments end on monitor steps: same records and the same invariant
+    report as the resident run."""
+    dev, sce, stepper = build_case("rand3_split")
+    a = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    ra = a.run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case("rand3_split")
+    b = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True, record_segment=37)
+    rb = b.run()
+    assert b._host_rows is not None
+    for x, y in zip(ra, rb):
+        assert np.array_equal(x.data, y.data), x.name
+    assert a.invariant_report == b.invariant_report
