@@ -152,6 +152,19 @@ int mbg_set_record_rows(mbg_solver *s, int32_t r, int64_t cap);
 int mbg_download_record_rows(mbg_solver *s, int32_t r, int64_t row_lo, int64_t row_hi, double *re, double *im);
 int mbg_set_record_row0(mbg_solver *s, int32_t r, int64_t row0);
 
+/* Batched single-point systems (many Nx = 1 master-equation runs
+ * of solver_fdtd.py:89-96, 347-349 per launch).  The handle is a num_x = 1
+ * solver whose media (mbg_set_qm_*) the B systems index by medium[b]; at one
+ * grid point the field is source-driven only, so e_seq [num_t][B] holds every
+ * system's E at every step (computed by the caller from its sources), state
+ * [words][B] the initial packed states (overwritten with the final ones).
+ * Density records (MBG_Q_D with 0-based i, j; MBG_Q_INV for two-level media)
+ * of rows (num_t - 1)/every + 1 are written to re[r] / im[r] as [B][rows];
+ * row 0 (the initial state) is left to the caller.  Blocking. */
+int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const double *e_seq, double *state,
+                     int32_t n_rec, const int32_t *quantity, const int32_t *i, const int32_t *j,
+                     const int64_t *every, double *const *re, double *const *im);
+
 /* multi-device slabs: pack/unpack `count` cells starting at global cell
  * `cell0` of E, H and every state plane into/out of a device buffer of
  * (2 + words) * count doubles (ordered on the solver's stream) */

@@ -254,6 +254,39 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
     return cudaErrorInvalidValue;
 }
 
+// batched single points: the N-level parameter block (same constants and
+// real-operator choice as the step kernels)
+template <int N>
+cudaError_t batch_dense_n(const mbg_solver *s, int B, const BatchRecs &R, const double *e_seq, double *state,
+                          const int *medium) {
+    const bool rk4 = s->g.stepper == MBG_STEPPER_RK4;
+    auto go = [&](auto *P, auto fill, auto real) {
+        P->B = B;
+        P->num_t = s->g.num_t;
+        P->e_seq = e_seq;
+        P->state = state;
+        P->medium = medium;
+        P->R = R;
+        P->n_qm = (int)s->qm.size();
+        P->real_a = P->n_qm > 0 && !disable_real_a();
+        for (int q = 0; q < P->n_qm; ++q) {
+            fill(P->qm[q], s->qm[q]);
+            P->real_a &= real(s->qm[q]) ? 1 : 0;
+        }
+        cudaError_t e = s->g.exact ? exact::launch_batch_dense(N, rk4, P, B, s->stream)
+                                   : fast::launch_batch_dense(N, rk4, P, B, s->stream);
+        delete P;
+        return e;
+    };
+    if (rk4)
+        return go(new BatchParams<N, Rk4Qm<N>>(), [&](Rk4Qm<N> &d, const QmHost &h) { fill_rk4<N>(d, h, s->g.dt); },
+                  [](const QmHost &h) { return real_operators<N>(h); });
+    if constexpr (N >= 3)
+        return go(new BatchParams<N, DenseQm<N>>(), [](DenseQm<N> &d, const QmHost &h) { fill_split<N>(d, h); },
+                  [](const QmHost &h) { return real_hamiltonian<N>(h); });
+    return cudaErrorInvalidValue;
+}
+
 // _kernels.py:481-494 components that vanish for a real dipole / diagonal H0
 bool real_dipole(const BlochQm &b) {
     return b.ax_c == 0.0 && b.ay_c == 0.0 && b.ay_s == 0.0 && b.az_s == 0.0 && b.a0_s == 0.0 && b.mu_y == 0.0 &&
@@ -287,6 +320,23 @@ BlochFrame state_frame(const mbg_solver *s) {
     return F;
 }
 
+BlochReal bloch_real(const BlochQm &b) {
+    const double u = b.a0_c * b.a0_c;
+    return BlochReal{u,
+                     1.0 + u,
+                     4.0 * u,
+                     b.az_c * b.az_c,
+                     1.0 - u,
+                     b.pol_factor * b.mu_x * b.fxy,
+                     b.fxy * b.fxy,
+                     b.kz * b.kz,
+                     b.kz * b.cz + b.cz,
+                     0.5 * (1.0 + u),
+                     0.5 * (1.0 - u),
+                     2.0 * b.az_c,
+                     2.0 * b.ax_s};
+}
+
 BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
     BlochParams P;
     std::memset(&P, 0, sizeof(P));
@@ -297,20 +347,7 @@ BlochParams bloch_params(const mbg_solver *s, const Launch &L) {
         BlochQm &b = P.qm[q];
         std::memcpy(&b, s->qm[q].bloch, sizeof(BlochQm));
         P.real_dipole &= real_dipole(b) ? 1 : 0;
-        const double u = b.a0_c * b.a0_c;
-        P.rq[q] = BlochReal{u,
-                            1.0 + u,
-                            4.0 * u,
-                            b.az_c * b.az_c,
-                            1.0 - u,
-                            b.pol_factor * b.mu_x * b.fxy,
-                            b.fxy * b.fxy,
-                            b.kz * b.kz,
-                            b.kz * b.cz + b.cz,
-                            0.5 * (1.0 + u),
-                            0.5 * (1.0 - u),
-                            2.0 * b.az_c,
-                            2.0 * b.ax_s};
+        P.rq[q] = bloch_real(b);
     }
     // the fast variant's real-dipole cell function works in the relaxed frame
     P.frame = state_frame(s);
@@ -1071,6 +1108,109 @@ int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im) {
     if (R.im && im) CK(cudaMemcpyAsync(im, R.im, bytes, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return MBG_OK;
+}
+
+int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const double *e_seq, double *state,
+                     int32_t n_rec, const int32_t *quantity, const int32_t *ri, const int32_t *rj,
+                     const int64_t *every, double *const *re, double *const *im) {
+    if (!s || B < 1 || !medium || !e_seq || !state || n_rec < 0 || (n_rec && (!quantity || !ri || !rj || !every || !re)))
+        return MBG_E_ARG;
+    if (s->g.num_x != 1) return fail(s, MBG_E_ARG, "batched points need a single-grid-point solver (num_x = 1)");
+    if (s->g.levels < 2 || s->qm.empty()) return fail(s, MBG_E_STATE, "quantum constants not set");
+    if (n_rec > kMaxRecords) return fail(s, MBG_E_UNSUPPORTED, "too many records (max 64)");
+    const int nq = (int)s->qm.size(), N = s->g.levels;
+    for (int b = 0; b < B; ++b)
+        if (medium[b] < 0 || medium[b] >= nq) return fail(s, MBG_E_ARG, "medium index out of range");
+    BatchRecs R;
+    std::memset(&R, 0, sizeof(R));
+    R.n = n_rec;
+    for (int r = 0; r < n_rec; ++r) {
+        if ((quantity[r] != MBG_Q_D && quantity[r] != MBG_Q_INV) || every[r] < 1 || ri[r] < 0 || rj[r] < 0 ||
+            ri[r] >= N || rj[r] >= N || (quantity[r] == MBG_Q_INV && !s->bloch))
+            return fail(s, MBG_E_ARG, "batched records: density entries (or the two-level inversion) only");
+        R.q[r] = quantity[r];
+        R.i[r] = ri[r];
+        R.j[r] = rj[r];
+        R.every[r] = every[r];
+        R.rows[r] = (s->g.num_t - 1) / every[r] + 1;
+    }
+    cudaSetDevice(s->g.device);
+    const int words = s->words;
+    double *d_e = nullptr, *d_s = nullptr;
+    int *d_m = nullptr;
+    std::vector<double *> bufs;
+    auto release = [&]() {
+        dfree(s->stream, d_e);
+        dfree(s->stream, d_s);
+        dfree(s->stream, d_m);
+        for (double *p : bufs) dfree(s->stream, p);
+        cudaStreamSynchronize(s->stream);
+    };
+    auto step = [&](cudaError_t e, const char *what) {
+        if (e == cudaSuccess) return true;
+        s->err = std::string(what) + ": " + cudaGetErrorString(e);
+        return false;
+    };
+    const size_t eb = sizeof(double) * (size_t)s->g.num_t * B, sb = sizeof(double) * (size_t)words * B;
+    bool ok = step(dalloc(s->stream, &d_e, eb), "alloc") && step(dalloc(s->stream, &d_s, sb), "alloc") &&
+              step(cudaMallocAsync(reinterpret_cast<void **>(&d_m), sizeof(int) * B, s->stream), "alloc") &&
+              step(cudaMemcpyAsync(d_e, e_seq, eb, cudaMemcpyHostToDevice, s->stream), "copy") &&
+              step(cudaMemcpyAsync(d_s, state, sb, cudaMemcpyHostToDevice, s->stream), "copy") &&
+              step(cudaMemcpyAsync(d_m, medium, sizeof(int) * B, cudaMemcpyHostToDevice, s->stream), "copy");
+    for (int r = 0; ok && r < n_rec; ++r) {
+        const size_t rb = sizeof(double) * (size_t)R.rows[r] * B;
+        ok = step(dalloc(s->stream, &R.re[r], rb), "alloc") &&
+             step(cudaMemsetAsync(R.re[r], 0, rb, s->stream), "memset");
+        bufs.push_back(R.re[r]);
+        if (ok && R.q[r] == MBG_Q_D && R.i[r] != R.j[r]) {
+            ok = step(dalloc(s->stream, &R.im[r], rb), "alloc") &&
+                 step(cudaMemsetAsync(R.im[r], 0, rb, s->stream), "memset");
+            bufs.push_back(R.im[r]);
+        }
+    }
+    if (ok) {
+        cudaError_t e;
+        if (s->bloch) {
+            BlochBatchParams P;
+            std::memset(&P, 0, sizeof(P));
+            P.B = B;
+            P.num_t = s->g.num_t;
+            P.e_seq = d_e;
+            P.state = d_s;
+            P.medium = d_m;
+            P.R = R;
+            P.n_qm = nq;
+            P.real_dipole = 1;
+            for (int q = 0; q < nq; ++q) {
+                std::memcpy(&P.qm[q], s->qm[q].bloch, sizeof(BlochQm));
+                P.rq[q] = bloch_real(P.qm[q]);
+                P.real_dipole &= real_dipole(P.qm[q]) ? 1 : 0;
+            }
+            e = s->g.exact ? exact::launch_batch_bloch(P, s->stream) : fast::launch_batch_bloch(P, s->stream);
+        } else {
+            switch (N) {
+                case 2: e = batch_dense_n<2>(s, B, R, d_e, d_s, d_m); break;
+                case 3: e = batch_dense_n<3>(s, B, R, d_e, d_s, d_m); break;
+                case 4: e = batch_dense_n<4>(s, B, R, d_e, d_s, d_m); break;
+                case 5: e = batch_dense_n<5>(s, B, R, d_e, d_s, d_m); break;
+                case 6: e = batch_dense_n<6>(s, B, R, d_e, d_s, d_m); break;
+                case 7: e = batch_dense_n<7>(s, B, R, d_e, d_s, d_m); break;
+                case 8: e = batch_dense_n<8>(s, B, R, d_e, d_s, d_m); break;
+                default: e = cudaErrorInvalidValue;
+            }
+        }
+        ok = step(e, "batch kernel");
+        if (ok) ++s->launches;
+    }
+    for (int r = 0; ok && r < n_rec; ++r) {
+        const size_t rb = sizeof(double) * (size_t)R.rows[r] * B;
+        ok = step(cudaMemcpyAsync(re[r], R.re[r], rb, cudaMemcpyDeviceToHost, s->stream), "copy");
+        if (ok && R.im[r] && im && im[r]) ok = step(cudaMemcpyAsync(im[r], R.im[r], rb, cudaMemcpyDeviceToHost, s->stream), "copy");
+    }
+    if (ok) ok = step(cudaMemcpyAsync(state, d_s, sb, cudaMemcpyDeviceToHost, s->stream), "copy");
+    if (ok) ok = step(cudaStreamSynchronize(s->stream), "batch run");
+    release();
+    return ok ? MBG_OK : MBG_E_CUDA;
 }
 
 int mbg_halo_words(const mbg_solver *s, int32_t *words) {

@@ -742,6 +742,38 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
     }
 }
 
+// batched single points (see BatchParams): one thread per two-level system,
+// the reference's rotation order (bloch_cell_real / bloch_cell, the Bloch
+// vector in the reference's own frame)
+__global__ void bloch_batch_kernel(const __grid_constant__ BlochBatchParams P) {
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= P.B) return;
+    const int m = P.medium[b];
+    const BlochQm &q = P.qm[m];
+    double x = P.state[b], y = P.state[P.B + b], z = P.state[2 * (long long)P.B + b];
+    for (long long n = 1; n < P.num_t; ++n) {
+        const double e = P.e_seq[(n - 1) * P.B + b];
+        if (P.real_dipole)
+            bloch_cell_real(q, P.rq[m], e, x, y, z);
+        else
+            bloch_cell(q, e, x, y, z);
+        for (int r = 0; r < P.R.n; ++r) {
+            if (n % P.R.every[r]) continue;
+            const long long idx = b * P.R.rows[r] + n / P.R.every[r];
+            double vre = 0.0, vim = 0.0;
+            if (P.R.q[r] == MBG_Q_D)
+                bloch_entry(P.R.i[r], P.R.j[r], x, y, z, vre, vim);
+            else
+                vre = -z;  // inversion (_kernels.py:538-539)
+            P.R.re[r][idx] = vre;
+            if (P.R.im[r]) P.R.im[r][idx] = vim;
+        }
+    }
+    P.state[b] = x;
+    P.state[P.B + b] = y;
+    P.state[2 * (long long)P.B + b] = z;
+}
+
 }  // namespace
 
 int bloch_cta_tile() { return kBlochCtaTile; }
@@ -789,6 +821,12 @@ cudaError_t launch_wave_masks(const Launch &L, long long n_steps, long long last
                               unsigned char *checks, cudaStream_t st) {
     const unsigned blocks = (unsigned)((n_steps + 255) / 256);
     wave_mask_kernel<<<blocks, 256, 0, st>>>(L, n_steps, last_step, masks, checks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_bloch(const BlochBatchParams &P, cudaStream_t st) {
+    const unsigned blocks = (unsigned)((P.B + 127) / 128);
+    bloch_batch_kernel<<<blocks, 128, 0, st>>>(P);
     return cudaGetLastError();
 }
 

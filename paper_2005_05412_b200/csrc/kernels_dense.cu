@@ -8,9 +8,11 @@
 namespace mbg {
 namespace MBG_VARIANT {
 namespace dense {
-#define MBG_DECL(n)                                                                  \
-    cudaError_t launch_split_##n(const void *params, long long tiles, cudaStream_t st); \
-    cudaError_t launch_rk4_##n(const void *params, long long tiles, cudaStream_t st);
+#define MBG_DECL(n)                                                                        \
+    cudaError_t launch_split_##n(const void *params, long long tiles, cudaStream_t st);       \
+    cudaError_t launch_rk4_##n(const void *params, long long tiles, cudaStream_t st);         \
+    cudaError_t launch_batch_split_##n(const void *params, int systems, cudaStream_t st);     \
+    cudaError_t launch_batch_rk4_##n(const void *params, int systems, cudaStream_t st);
 MBG_DECL(2)
 MBG_DECL(3)
 MBG_DECL(4)
@@ -43,6 +45,24 @@ cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStr
         case 8: return dense::launch_rk4_8(params, tiles, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_batch_dense(int n, bool rk4, const void *params, int systems, cudaStream_t st) {
+#define MBG_BATCH_CASE(k)                                                                  \
+    case k:                                                                                \
+        return rk4 ? dense::launch_batch_rk4_##k(params, systems, st)                      \
+                   : dense::launch_batch_split_##k(params, systems, st);
+    switch (n) {
+        MBG_BATCH_CASE(2)
+        MBG_BATCH_CASE(3)
+        MBG_BATCH_CASE(4)
+        MBG_BATCH_CASE(5)
+        MBG_BATCH_CASE(6)
+        MBG_BATCH_CASE(7)
+        MBG_BATCH_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef MBG_BATCH_CASE
 }
 
 }  // namespace MBG_VARIANT

@@ -693,6 +693,57 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) 
         dense_dispatch<N, RK4, Q, false>(P, sm, t_lo, t_hi, base);
 }
 
+// ---------------------------------------------------------------------------
+// batched single points: one thread per system, all steps in one launch
+template <int N, bool RK4, class Q, bool RA>
+__global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4))
+    dense_batch_kernel(const __grid_constant__ BatchParams<N, Q> P) {
+    using Lay = Layout<N, RK4>;
+    constexpr int NW = N * N, W = Lay::TW;
+    extern __shared__ double sm[];
+    double *col = sm + 6 * W + threadIdx.x;  // same column layout as the step kernel
+    const long long b = (long long)blockIdx.x * W + threadIdx.x;
+    if (b >= P.B) return;  // no barriers below
+    const Q &q = P.qm[P.medium[b]];
+    RegVec<NW> rA;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const double v = P.state[w * (long long)P.B + b];
+        if constexpr (Lay::kRegState) rA[w] = v; else col[w * W] = v;
+    }
+    for (long long n = 1; n < P.num_t; ++n) {
+        cell_step<N, RK4, RA>(q, P.e_seq[(n - 1) * P.B + b], col, rA);
+        for (int r = 0; r < P.R.n; ++r) {
+            if (n % P.R.every[r]) continue;
+            const long long idx = b * P.R.rows[r] + n / P.R.every[r];
+            const int a = P.R.i[r], c = P.R.j[r];
+            double vre = 0.0, vim = 0.0;
+            if constexpr (Lay::kRegState) {
+#pragma unroll
+                for (int u = 0; u < N; ++u)
+#pragma unroll
+                    for (int v = 0; v < N; ++v)
+                        if (u == a && v == c) herm<N>(rA, u, v, vre, vim);
+            } else {
+                SmemVec<W> A{col};
+                if (a == c) {
+                    vre = A[a];
+                } else if (a < c) {
+                    vre = A[wre(N, a, c)];
+                    vim = A[wim(N, a, c)];
+                } else {
+                    vre = A[wre(N, c, a)];
+                    vim = -A[wim(N, c, a)];
+                }
+            }
+            P.R.re[r][idx] = vre;
+            if (P.R.im[r]) P.R.im[r][idx] = vim;
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) P.state[w * (long long)P.B + b] = Lay::kRegState ? rA[w] : col[w * W];
+}
+
 }  // namespace dense
 }  // namespace MBG_VARIANT
 }  // namespace mbg

@@ -29,6 +29,38 @@ static cudaError_t launch_n(const void *params, long long tiles, cudaStream_t st
     return cudaGetLastError();
 }
 
+template <int N, bool RK4, class Q>
+static cudaError_t batch_n(const void *params, int systems, cudaStream_t st) {
+    const auto &P = *static_cast<const BatchParams<N, Q> *>(params);
+    static_assert(sizeof(BatchParams<N, Q>) <= 32764, "kernel parameter block over the 32 KB launch limit");
+    constexpr size_t smem = Layout<N, RK4>::smem_bytes();
+    constexpr int W = Layout<N, RK4>::TW;
+#if defined(MBG_EXACT) && MBG_EXACT
+    constexpr bool kRa = false;
+#else
+    constexpr bool kRa = RK4 || Layout<N, RK4>::kRegState;  // as the step kernel chooses
+#endif
+    static bool configured[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    const bool ra = kRa && P.real_a;
+    if (!configured[dev][ra]) {
+        cudaError_t err = ra ? cudaFuncSetAttribute(dense_batch_kernel<N, RK4, Q, kRa>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(dense_batch_kernel<N, RK4, Q, false>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err != cudaSuccess) return err;
+        configured[dev][ra] = true;
+    }
+    const unsigned blocks = (unsigned)((systems + W - 1) / W);
+    if (ra)
+        dense_batch_kernel<N, RK4, Q, kRa><<<blocks, W, smem, st>>>(P);
+    else
+        dense_batch_kernel<N, RK4, Q, false><<<blocks, W, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
 #define MBG_CAT2(a, b) a##b
 #define MBG_CAT(a, b) MBG_CAT2(a, b)
 
@@ -42,6 +74,18 @@ cudaError_t MBG_CAT(launch_split_, MBG_LEVELS)(const void *params, long long til
 
 cudaError_t MBG_CAT(launch_rk4_, MBG_LEVELS)(const void *params, long long tiles, cudaStream_t st) {
     return launch_n<MBG_LEVELS, true, Rk4Qm<MBG_LEVELS>>(params, tiles, st);
+}
+
+cudaError_t MBG_CAT(launch_batch_split_, MBG_LEVELS)(const void *params, int systems, cudaStream_t st) {
+#if MBG_LEVELS >= 3
+    return batch_n<MBG_LEVELS, false, DenseQm<MBG_LEVELS>>(params, systems, st);
+#else
+    return cudaErrorInvalidValue;
+#endif
+}
+
+cudaError_t MBG_CAT(launch_batch_rk4_, MBG_LEVELS)(const void *params, int systems, cudaStream_t st) {
+    return batch_n<MBG_LEVELS, true, Rk4Qm<MBG_LEVELS>>(params, systems, st);
 }
 
 }  // namespace dense

@@ -90,6 +90,8 @@ struct BlochWave {
                                   unsigned long long *masks, unsigned char *checks, cudaStream_t st); \
     cudaError_t launch_dense_split(int n, const void *params, long long tiles, cudaStream_t st); \
     cudaError_t launch_dense_rk4(int n, const void *params, long long tiles, cudaStream_t st);   \
+    cudaError_t launch_batch_dense(int n, bool rk4, const void *params, int systems, cudaStream_t st); \
+    cudaError_t launch_batch_bloch(const BlochBatchParams &P, cudaStream_t st);                   \
     }
 
 MBG_DECLARE_LAUNCHERS(fast)

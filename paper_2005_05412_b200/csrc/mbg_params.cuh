@@ -163,6 +163,41 @@ struct DenseParams {
     Q qm[kMaxDenseQm];
 };
 
+// Batched single-point systems (Nx = 1, solver_fdtd.py:89-96, 347-349): the
+// field is only source-driven there, so every system's E^n is precomputed on
+// the host and one thread per system steps its density matrix and writes its
+// density records (rows [B][rows]; E / H records are filled on the host).
+struct BatchRecs {
+    int n;
+    int q[kMaxRecords], i[kMaxRecords], j[kMaxRecords];
+    long long every[kMaxRecords], rows[kMaxRecords];
+    double *re[kMaxRecords], *im[kMaxRecords];
+};
+
+template <int N, class Q>
+struct BatchParams {
+    int B;
+    long long num_t;
+    const double *e_seq;  // [num_t][B]
+    double *state;        // [words][B], in and out
+    const int *medium;    // [B] constant-set index
+    int n_qm, real_a;
+    Q qm[kMaxDenseQm];
+    BatchRecs R;
+};
+
+struct BlochBatchParams {
+    int B;
+    long long num_t;
+    const double *e_seq;
+    double *state;  // Bloch (x, y, z) planes
+    const int *medium;
+    int n_qm, real_dipole;
+    BlochQm qm[kMaxQm];
+    BlochReal rq[kMaxQm];
+    BatchRecs R;
+};
+
 // shared helpers (host + device)
 // last region r with start[r] <= m (0 if none); starts are non-decreasing,
 // empty regions repeat a start and are skipped by taking the last match

@@ -72,6 +72,8 @@ SIGNATURES = {
     "mbg_set_record_rows": (C.c_int, [_h, C.c_int32, C.c_int64]),
     "mbg_download_record_rows": (C.c_int, [_h, C.c_int32, C.c_int64, C.c_int64, _dp, _dp]),
     "mbg_set_record_row0": (C.c_int, [_h, C.c_int32, C.c_int64]),
+    "mbg_batch_points": (C.c_int, [_h, C.c_int32, _i32p, _dp, _dp, C.c_int32, _i32p, _i32p, _i32p, _i64p,
+                                   C.POINTER(_dp), C.POINTER(_dp)]),
     "mbg_halo_words": (C.c_int, [_h, _i32p]),
     "mbg_pack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
     "mbg_unpack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
