@@ -89,6 +89,20 @@ __device__ __forceinline__ double recip_pos(double d) {
 #endif
 }
 
+// symmetric complex matrix as two upper triangles (row-major, i <= j)
+template <int N>
+struct SymMat {
+    double re[N * (N + 1) / 2], im[N * (N + 1) / 2];
+    static constexpr int at(int i, int j) {
+        return i <= j ? i * N - i * (i - 1) / 2 + (j - i) : j * N - j * (j - 1) / 2 + (i - j);
+    }
+    __device__ __forceinline__ double &r(int i, int j) { return re[at(i, j)]; }
+    __device__ __forceinline__ double &m(int i, int j) { return im[at(i, j)]; }
+};
+
+template <int N, class VA, class VB, class MG, class VR>
+__device__ __forceinline__ double congruence(const DenseQm<N> &q, VA &A, VB &B, MG &G, VR &raw);
+
 // ---------------------------------------------------------------------------
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
 template <int N, bool RA, class VA, class VB, class MG, class VR>
@@ -110,106 +124,111 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
         }
     if constexpr (RA) {
         // Real Hamiltonian and dipole (fast variant): A real symmetric, so
-        // 2 (I + iA)^-1 = 2 (I - iA)(I + A^2)^-1 = 2P - 2iAP with P = (I + A^2)^-1
-        // real, obtained by a real in-place Gauss-Jordan of (I + A^2)/2 (SPD,
-        // ~I/2, no pivoting): a quarter of the complex inversion's work.
-        // G.m <- Ah = A/2 (the host's halved constants), G.r <- (I + A^2)/2
+        // U = (I + iA)^-1 (I - iA) = (2P - I) - 2iAP with P = (I + A^2)^-1 real
+        // symmetric, and AP symmetric too: both parts of U live as upper
+        // triangles (N(N+1) words instead of 2N^2).  (I + A^2)/2 (SPD, ~I/2) is
+        // inverted by the symmetric sweep operator (no pivoting), which ends at
+        // -((I + A^2)/2)^-1 = -2P.
+        SymMat<N> S;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+            for (int j = i; j < N; ++j) S.m(i, j) = mad(e, q.bf_im[i * N + j], q.bc_im[i * N + j]);  // A/2
 #pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
             for (int j = i; j < N; ++j) {
-                G.m(i, j) = mad(e, q.bf_im[i * N + j], q.bc_im[i * N + j]);
-                if (j != i) G.m(j, i) = G.m(i, j);
+                double acc = S.m(i, 0) * S.m(0, j);
+#pragma unroll
+                for (int k = 1; k < N; ++k) acc = mad(S.m(i, k), S.m(k, j), acc);
+                S.r(i, j) = mad(2.0, acc, i == j ? 0.5 : 0.0);  // (I + A^2)/2 = I/2 + 2 (A/2)^2
             }
 #pragma unroll
-        for (int i = 0; i < N; ++i)
+        for (int k = 0; k < N; ++k) {  // sweep k: a_ij -= a_ik a_kj / a_kk, a_ik /= a_kk, a_kk = -1/a_kk
+            const double d = recip_pos(S.r(k, k));
+            double t[N];
 #pragma unroll
-            for (int j = i; j < N; ++j) {
-                double acc = G.m(i, 0) * G.m(0, j);
+            for (int i = 0; i < N; ++i) t[i] = i == k ? 0.0 : S.r(i, k) * d;
 #pragma unroll
-                for (int k = 1; k < N; ++k) acc = mad(G.m(i, k), G.m(k, j), acc);
-                G.r(i, j) = mad(2.0, acc, i == j ? 0.5 : 0.0);  // (I + A^2)/2 = I/2 + 2 Ah^2
-                if (j != i) G.r(j, i) = G.r(i, j);
-            }
+            for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            const double ip = recip_pos(G.r(k, k));
+                for (int j = i; j < N; ++j)
+                    if (i != k && j != k) S.r(i, j) = mad(-t[i], S.r(k, j), S.r(i, j));
 #pragma unroll
-            for (int j = 0; j < N; ++j)
-                if (j != k) G.r(k, j) *= ip;
-            G.r(k, k) = ip;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                if (i == k) continue;
-                const double f = G.r(i, k);
-#pragma unroll
-                for (int j = 0; j < N; ++j)
-                    if (j != k) G.r(i, j) = mad(-f, G.r(k, j), G.r(i, j));
-                G.r(i, k) = -f * ip;
-            }
+            for (int i = 0; i < N; ++i)
+                if (i != k) S.r(i, k) = t[i];
+            S.r(k, k) = -d;
         }
-        // G.r = 2P; imaginary part -2AP = -2 Ah (2P), row by row in place: row
-        // i of the product reads only row i of Ah (its lower part, j < i, still
-        // holds Ah; the upper part is overwritten once the row is done)
+        // Im U = -2AP = -4 (A/2) P = 2 (A/2) S.r, in place from the last row up:
+        // row i reads A/2 at (i, k >= i) -- its own, rewritten after the row
+        // -- and at (k < i, i), rows not rewritten yet
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
+        for (int i = N - 1; i >= 0; --i) {
             double t[N];
 #pragma unroll
             for (int j = i; j < N; ++j) {
-                double acc = G.m(i, 0) * G.r(0, j);
+                double acc = S.m(i, 0) * S.r(0, j);
 #pragma unroll
-                for (int k = 1; k < N; ++k) acc = mad(G.m(i, k), G.r(k, j), acc);
-                t[j] = -2.0 * acc;
+                for (int k = 1; k < N; ++k) acc = mad(S.m(i, k), S.r(k, j), acc);
+                t[j] = 2.0 * acc;
             }
 #pragma unroll
-            for (int j = i; j < N; ++j) G.m(i, j) = t[j];
+            for (int j = i; j < N; ++j) S.m(i, j) = t[j];
         }
+        // Re U = 2P - I = -S.r - I
 #pragma unroll
         for (int i = 0; i < N; ++i)
 #pragma unroll
-            for (int j = 0; j < i; ++j) G.m(i, j) = G.m(j, i);
+            for (int j = i; j < N; ++j) S.r(i, j) = i == j ? -S.r(i, j) - 1.0 : -S.r(i, j);
+        return congruence<N>(q, A, B, S, raw);
     } else {
-    // G = (B/2)^-1 = 2 (I + iA)^-1: the host halves bc and bf (exact), so the
-    // Gauss-Jordan inverse (in place, no pivoting) is already 2(I + iA)^-1
+        // G = (B/2)^-1 = 2 (I + iA)^-1: the host halves bc and bf (exact), so the
+        // Gauss-Jordan inverse (in place, no pivoting) is already 2(I + iA)^-1
 #pragma unroll
-    for (int i = 0; i < N * N; ++i) {
-        G.r(i / N, i % N) = mad(e, q.bf_re[i], q.bc_re[i]);
-        G.m(i / N, i % N) = mad(e, q.bf_im[i], q.bc_im[i]);
-    }
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        const double pr = G.r(k, k), pi = G.m(k, k);
-        const double rd = recip_pos(mad(pi, pi, pr * pr));
-        const double ir = pr * rd, ii = -pi * rd;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            if (j == k) continue;
-            const double xr = G.r(k, j), xi = G.m(k, j);
-            G.r(k, j) = mad(xr, ir, -(xi * ii));
-            G.m(k, j) = mad(xr, ii, xi * ir);
+        for (int i = 0; i < N * N; ++i) {
+            G.r(i / N, i % N) = mad(e, q.bf_re[i], q.bc_re[i]);
+            G.m(i / N, i % N) = mad(e, q.bf_im[i], q.bc_im[i]);
         }
-        G.r(k, k) = ir;
-        G.m(k, k) = ii;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-            if (i == k) continue;
-            const double fr = G.r(i, k), fi = G.m(i, k);
+        for (int k = 0; k < N; ++k) {
+            const double pr = G.r(k, k), pi = G.m(k, k);
+            const double rd = recip_pos(mad(pi, pi, pr * pr));
+            const double ir = pr * rd, ii = -pi * rd;
 #pragma unroll
             for (int j = 0; j < N; ++j) {
                 if (j == k) continue;
-                const double kr = G.r(k, j), ki = G.m(k, j);
-                G.r(i, j) = mad(-fr, kr, mad(fi, ki, G.r(i, j)));
-                G.m(i, j) = mad(-fr, ki, mad(-fi, kr, G.m(i, j)));
+                const double xr = G.r(k, j), xi = G.m(k, j);
+                G.r(k, j) = mad(xr, ir, -(xi * ii));
+                G.m(k, j) = mad(xr, ii, xi * ir);
             }
-            G.r(i, k) = mad(-fr, ir, fi * ii);
-            G.m(i, k) = mad(-fr, ii, -(fi * ir));
-        }
-    }
-    }
-    // U = 2(I + iA)^-1 - I = G - I
+            G.r(k, k) = ir;
+            G.m(k, k) = ii;
 #pragma unroll
-    for (int i = 0; i < N; ++i) G.r(i, i) -= 1.0;
-    // rho' = U r1 U^H, one row at a time; second relaxation half step fused
+            for (int i = 0; i < N; ++i) {
+                if (i == k) continue;
+                const double fr = G.r(i, k), fi = G.m(i, k);
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    if (j == k) continue;
+                    const double kr = G.r(k, j), ki = G.m(k, j);
+                    G.r(i, j) = mad(-fr, kr, mad(fi, ki, G.r(i, j)));
+                    G.m(i, j) = mad(-fr, ki, mad(-fi, kr, G.m(i, j)));
+                }
+                G.r(i, k) = mad(-fr, ir, fi * ii);
+                G.m(i, k) = mad(-fr, ii, -(fi * ir));
+            }
+        }
+        // U = 2(I + iA)^-1 - I = G - I
+#pragma unroll
+        for (int i = 0; i < N; ++i) G.r(i, i) -= 1.0;
+        return congruence<N>(q, A, B, G, raw);
+    }
+}
+
+// rho' = U r1 U^H, one row at a time; second relaxation half step and the
+// polarisation trace fused (_kernels.py:87-160)
+template <int N, class VA, class VB, class MG, class VR>
+__device__ __forceinline__ double congruence(const DenseQm<N> &q, VA &A, VB &B, MG &G, VR &raw) {
     double acc_p = 0.0;  // raw[i]: row i's diagonal before the second half relaxation
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -682,10 +701,9 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) 
 #if defined(MBG_EXACT) && MBG_EXACT
     constexpr bool kRa = false;  // the exact variant keeps the reference's complex arithmetic
 #else
-    // real operators: RK4 always; splitting for the register-state kernels
-    // (N <= 4: cfg3 6.28e10 -> 7.07e10) -- at six levels the extra phase of
-    // the real inversion costs more in spills than it saves (4.80e9 -> 4.30e9)
-    constexpr bool kRa = RK4 || Layout<N, RK4>::kRegState;
+    // real operators (the choice is per run, from the host's exact test):
+    // symmetric-triangle U for the splitting step, real H for RK4
+    constexpr bool kRa = true;
 #endif
     if (kRa && P.real_a)
         dense_dispatch<N, RK4, Q, kRa>(P, sm, t_lo, t_hi, base);

@@ -38,7 +38,7 @@ static cudaError_t batch_n(const void *params, int systems, cudaStream_t st) {
 #if defined(MBG_EXACT) && MBG_EXACT
     constexpr bool kRa = false;
 #else
-    constexpr bool kRa = RK4 || Layout<N, RK4>::kRegState;  // as the step kernel chooses
+    constexpr bool kRa = true;  // as the step kernel chooses
 #endif
     static bool configured[64][2] = {};
     int dev = 0;

@@ -24,13 +24,16 @@ def _diagonal_basis(n):
     return rows
 
 
-def random_medium(api, rng, dim, rate_scale=1e11, freq_scale=1e14, dipole_scale=1e-29, density=1e24):
+def random_medium(api, rng, dim, rate_scale=1e11, freq_scale=1e14, dipole_scale=1e-29, density=1e24, real=False):
     """Random valid N-level description; same draw sequence as the reference's
-    test helper ``random_description`` (pkg/tests/conftest.py:49-73)."""
+    test helper ``random_description`` (pkg/tests/conftest.py:49-73).  ``real``:
+    the same draws with the imaginary parts of H and the dipole dropped."""
     n_off = dim * (dim - 1) // 2
     energies = np.sort(rng.uniform(0.0, 1.0, dim)) * api.HBAR * freq_scale
     off_h = (rng.standard_normal(n_off) + 1j * rng.standard_normal(n_off)) * api.HBAR * freq_scale * 0.05
     off_mu = (rng.standard_normal(n_off) + 1j * rng.standard_normal(n_off)) * dipole_scale
+    if real:
+        off_h, off_mu = off_h.real.astype(complex), off_mu.real.astype(complex)
     rates = rng.uniform(0.0, 1.0, (dim, dim)) * rate_scale
     np.fill_diagonal(rates, 0.0)
     basis = _diagonal_basis(dim)
@@ -42,11 +45,11 @@ def random_medium(api, rng, dim, rate_scale=1e11, freq_scale=1e14, dipole_scale=
         api.LindbladRelaxation(rates, deph))
 
 
-def random_case(dim, seed, nx=512, end=20e-15, whole=False, stepper="splitting"):
+def random_case(dim, seed, nx=512, end=20e-15, whole=False, stepper="splitting", real=False):
     def build(api):
         rng = np.random.default_rng(seed)
-        desc = random_medium(api, rng, dim)
-        act = api.ensure_material(api.Material(f"Rand{dim}_{seed}", qm=desc))
+        desc = random_medium(api, rng, dim, real=real)
+        act = api.ensure_material(api.Material(f"Rand{dim}_{seed}" + ("r" if real else ""), qm=desc))
         vac = api.ensure_material(api.Material("Vacuum"))
         dev = api.Device(f"rand{dim}")
         dev.add_region(api.Region("v", vac.id, 0.0, 5e-6))

@@ -112,3 +112,22 @@ def test_gpu_matches_oracle_on_fresh_seeds():
         assert bad == 0
         for r, ref in zip(got, recs):
             assert rel_err(r.data, ref) <= TOL, (dim, r.name, rel_err(r.data, ref))
+
+
+@pytest.mark.parametrize("stepper", ["splitting", "rk4"])
+@pytest.mark.parametrize("dim", [3, 4, 5, 6, 7, 8])
+def test_real_media_fast_paths_match_the_oracle(dim, stepper):
+    """Real H0 and dipole: the symmetric-triangle inversion (splitting) and
+    the real-H commutator (RK4) of the fast variant against the CPU oracle."""
+    import oracle as orc
+    from cases import random_case
+
+    mb.clear_material_library()
+    build, _ = random_case(dim, 950 + dim, nx=600, end=25e-15, stepper=stepper, real=True)
+    dev, sce = build(mb)
+    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    got = solver.run()
+    recs, bad = orc.run_oracle(solver.plan)
+    assert bad == 0
+    for r, ref in zip(got, recs):
+        assert rel_err(r.data, ref) <= TOL, (dim, stepper, r.name, rel_err(r.data, ref))
