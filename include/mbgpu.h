@@ -158,7 +158,7 @@ int mbg_set_record_row0(mbg_solver *s, int32_t r, int64_t row0);
  * grid point the field is source-driven only, so e_seq [num_t][B] holds every
  * system's E at every step (computed by the caller from its sources), state
  * [words][B] the initial packed states (overwritten with the final ones).
- * Density records (MBG_Q_D with 0-based i, j; MBG_Q_INV for two-level media)
+ * Density records (MBG_Q_D with 0-based i, j; MBG_Q_INV for two-level media, either stepper)
  * of rows (num_t - 1)/every + 1 are written to re[r] / im[r] as [B][rows];
  * row 0 (the initial state) is left to the caller.  Blocking. */
 int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const double *e_seq, double *state,

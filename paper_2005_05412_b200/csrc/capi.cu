@@ -1126,7 +1126,7 @@ int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const doub
     R.n = n_rec;
     for (int r = 0; r < n_rec; ++r) {
         if ((quantity[r] != MBG_Q_D && quantity[r] != MBG_Q_INV) || every[r] < 1 || ri[r] < 0 || rj[r] < 0 ||
-            ri[r] >= N || rj[r] >= N || (quantity[r] == MBG_Q_INV && !s->bloch))
+            ri[r] >= N || rj[r] >= N || (quantity[r] == MBG_Q_INV && N != 2))
             return fail(s, MBG_E_ARG, "batched records: density entries (or the two-level inversion) only");
         R.q[r] = quantity[r];
         R.i[r] = ri[r];

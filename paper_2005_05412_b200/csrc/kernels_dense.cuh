@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4))
             const long long idx = b * P.R.rows[r] + n / P.R.every[r];
             const int a = P.R.i[r], c = P.R.j[r];
             double vre = 0.0, vim = 0.0;
-            if constexpr (Lay::kRegState) {
+            if (P.R.q[r] == MBG_Q_INV) {  // two-level inversion rho_11 - rho_00 (_kernels.py:391-392)
+                if constexpr (Lay::kRegState) vre = rA[1] - rA[0];
+                else vre = col[W] - col[0];
+            } else if constexpr (Lay::kRegState) {
 #pragma unroll
                 for (int u = 0; u < N; ++u)
 #pragma unroll

@@ -71,17 +71,23 @@ def test_three_level_batch_equals_single_runs(stepper, exact):
             assert np.array_equal(a.data, b.data), (v, a.name, rel_err(b.data, a.data))
 
 
+@pytest.mark.parametrize("stepper", ["splitting", "rk4"])
 @pytest.mark.parametrize("exact", [False, True])
-def test_two_level_batch_matches_single_runs(exact):
-    """Bloch systems (the reference's rotation order in the batch kernel)."""
+def test_two_level_batch_matches_single_runs(exact, stepper):
+    """Bloch systems (the reference's rotation order in the batch kernel;
+    the single solver's fast variant steps a relaxed frame, so 1e-9) and
+    two-level RK4 (the same cell function: bit for bit)."""
     variants = [dict(scale=s, t2=t, tag=g) for s, t, g in ((1.0, 1e12, ""), (0.3, 1e12, ""), (3.0, 5e11, "b"))]
     mb.clear_material_library()
-    batch = run_points([_two_level(**v) for v in variants], exact=exact)
+    batch = run_points([_two_level(**v) for v in variants], stepper=stepper, exact=exact)
     for v, got in zip(variants, batch):
-        ref = _alone(_two_level, "splitting", exact, **v)
+        ref = _alone(_two_level, stepper, exact, **v)
         for a, b in zip(ref, got):
             assert a.data.shape == b.data.shape
-            assert rel_err(b.data, a.data) <= 1e-9, (v, a.name, rel_err(b.data, a.data))
+            if stepper == "rk4":
+                assert np.array_equal(a.data, b.data), (v, a.name, rel_err(b.data, a.data))
+            else:
+                assert rel_err(b.data, a.data) <= 1e-9, (v, a.name, rel_err(b.data, a.data))
 
 
 @pytest.mark.parametrize("case,build,stepper", [("song_point", _song, "splitting"), ("song_point_rk4", _song, "rk4"),
