@@ -133,84 +133,155 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// smallest eigenvalue of a complex Hermitian n x n matrix (n <= 8) through the
-// real symmetric 2n x 2n embedding [[Re, -Im], [Im, Re]] and cyclic Jacobi
-__device__ double min_eigenvalue(const double *re, const double *im, int n) {
-    double a[16][16];
-    const int m = 2 * n;
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            a[i][j] = a[i + n][j + n] = re[i * n + j];
-            a[i + n][j] = im[i * n + j];
-            a[i][j + n] = -im[i * n + j];
-        }
+// smallest eigenvalue of a complex Hermitian N x N matrix by cyclic complex
+// Jacobi: each off-diagonal element's phase is moved into its column/row, then
+// a real plane rotation zeroes it (a quarter of the real 2N x 2N embedding's
+// work, compile-time indices so the matrix stays in registers)
+template <int N>
+__device__ double min_eigenvalue_herm(double (&re)[N * N], double (&im)[N * N]) {
     for (int sweep = 0; sweep < 30; ++sweep) {
         double off = 0.0, scale = 0.0;
-        for (int p = 0; p < m; ++p) {
-            scale += a[p][p] * a[p][p];
-            for (int q = p + 1; q < m; ++q) off += a[p][q] * a[p][q];
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+            scale += re[p * N + p] * re[p * N + p];
+#pragma unroll
+            for (int q = p + 1; q < N; ++q) off += re[p * N + q] * re[p * N + q] + im[p * N + q] * im[p * N + q];
         }
         if (off <= 1e-32 * (scale + 1e-300)) break;
-        for (int p = 0; p < m; ++p)
-            for (int q = p + 1; q < m; ++q) {
-                const double apq = a[p][q];
-                if (apq == 0.0) continue;
-                const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+#pragma unroll
+        for (int p = 0; p < N; ++p)
+#pragma unroll
+            for (int q = p + 1; q < N; ++q) {
+                const double ar = re[p * N + q], ai = im[p * N + q];
+                const double mag = sqrt(ar * ar + ai * ai);
+                if (mag == 0.0) continue;
+                const double ur = ar / mag, ui = ai / mag;  // a_pq = mag u
+                // column q times conj(u), row q times u: a_pq becomes mag, a_qq unchanged
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    if (k == q) continue;
+                    const double xr = re[k * N + q], xi = im[k * N + q];
+                    re[k * N + q] = xr * ur + xi * ui;
+                    im[k * N + q] = xi * ur - xr * ui;
+                    re[q * N + k] = re[k * N + q];
+                    im[q * N + k] = -im[k * N + q];
+                }
+                const double theta = (re[q * N + q] - re[p * N + p]) / (2.0 * mag);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                 const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
-                for (int k = 0; k < m; ++k) {
-                    const double akp = a[k][p], akq = a[k][q];
-                    a[k][p] = c * akp - sn * akq;
-                    a[k][q] = sn * akp + c * akq;
-                }
-                for (int k = 0; k < m; ++k) {
-                    const double apk = a[p][k], aqk = a[q][k];
-                    a[p][k] = c * apk - sn * aqk;
-                    a[q][k] = sn * apk + c * aqk;
+                const double app = re[p * N + p], aqq = re[q * N + q];
+                re[p * N + p] = app - t * mag;
+                re[q * N + q] = aqq + t * mag;
+                re[p * N + q] = im[p * N + q] = re[q * N + p] = im[q * N + p] = 0.0;
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    if (k == p || k == q) continue;
+                    const double pr = re[k * N + p], pi = im[k * N + p];
+                    const double qr = re[k * N + q], qi = im[k * N + q];
+                    re[k * N + p] = c * pr - sn * qr;
+                    im[k * N + p] = c * pi - sn * qi;
+                    re[k * N + q] = sn * pr + c * qr;
+                    im[k * N + q] = sn * pi + c * qi;
+                    re[p * N + k] = re[k * N + p];
+                    im[p * N + k] = -im[k * N + p];
+                    re[q * N + k] = re[k * N + q];
+                    im[q * N + k] = -im[k * N + q];
                 }
             }
     }
-    double mn = a[0][0];
-    for (int p = 1; p < m; ++p) mn = fmin(mn, a[p][p]);
+    double mn = re[0];
+#pragma unroll
+    for (int p = 1; p < N; ++p) mn = fmin(mn, re[p * N + p]);
     return mn;
 }
 
-__global__ void invariants_kernel(const Launch L, int levels, int bloch, const BlochFrame F,
-                                  unsigned long long *out) {
-    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= L.win_n) return;
+template <int N>
+__device__ double packed_min_eigenvalue(const double *s, long long P, double &tr) {
+    double re[N * N], im[N * N];
+    tr = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        re[i * N + i] = s[i * P];
+        im[i * N + i] = 0.0;
+        tr += re[i * N + i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+            const int w = N + 2 * pair_index(N, i, j);
+            re[i * N + j] = re[j * N + i] = s[w * P];
+            im[i * N + j] = s[(w + 1) * P];
+            im[j * N + i] = -s[(w + 1) * P];
+        }
+    return min_eigenvalue_herm<N>(re, im);
+}
+
+// per-cell (|trace - 1|, min eigenvalue); false for cells without a density matrix
+__device__ __forceinline__ bool cell_invariants(const Launch &L, int levels, int bloch, const BlochFrame &F,
+                                                long long l, double &trace_dev, double &min_eig) {
+    if (l >= L.win_n) return false;
     const long long c = L.win_lo + l;
-    if (c < L.own_lo || c >= L.own_hi) return;
+    if (c < L.own_lo || c >= L.own_hi) return false;
     const int qm = L.rg.qm[region_of(L.rg.e_start, L.rg.n, c)];
-    if (qm < 0) return;
+    if (qm < 0) return false;
     const double *s = L.s_in + l;
     const long long P = L.plane;
-    double trace_dev = 0.0, min_eig;
+    trace_dev = 0.0;
     if (bloch) {
         // eigenvalues (1 +- |v|)/2; trace and Hermiticity exact in this form
         double x, y, z;
         frame_true(F, qm, s[0], s[P], s[2 * P], x, y, z);
         min_eig = 0.5 * (1.0 - sqrt(x * x + y * y + z * z));
     } else {
-        const int n = levels;
-        double re[64], im[64], tr = 0.0;
-        for (int i = 0; i < n; ++i) {
-            re[i * n + i] = s[i * P];
-            im[i * n + i] = 0.0;
-            tr += re[i * n + i];
+        double tr = 0.0;
+        switch (levels) {
+            case 2: min_eig = packed_min_eigenvalue<2>(s, P, tr); break;
+            case 3: min_eig = packed_min_eigenvalue<3>(s, P, tr); break;
+            case 4: min_eig = packed_min_eigenvalue<4>(s, P, tr); break;
+            case 5: min_eig = packed_min_eigenvalue<5>(s, P, tr); break;
+            case 6: min_eig = packed_min_eigenvalue<6>(s, P, tr); break;
+            case 7: min_eig = packed_min_eigenvalue<7>(s, P, tr); break;
+            default: min_eig = packed_min_eigenvalue<8>(s, P, tr); break;
         }
-        for (int i = 0; i < n; ++i)
-            for (int j = i + 1; j < n; ++j) {
-                const int w = n + 2 * pair_index(n, i, j);
-                re[i * n + j] = re[j * n + i] = s[w * P];
-                im[i * n + j] = s[(w + 1) * P];
-                im[j * n + i] = -s[(w + 1) * P];
-            }
         trace_dev = fabs(tr - 1.0);
-        min_eig = min_eigenvalue(re, im, n);
     }
-    atomicMax(&out[0], dkey(trace_dev));
-    atomicMin(&out[2], dkey(min_eig));
+    return true;
+}
+
+// warp and block reductions first: one pair of atomics per block, not per
+// cell (4M same-address atomics cost milliseconds per monitor step)
+__global__ void __launch_bounds__(128) invariants_kernel(const Launch L, int levels, int bloch, const BlochFrame F,
+                                                         unsigned long long *out) {
+    __shared__ unsigned long long s_max[4], s_min[4];
+    const long long l = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double tdev = 0.0, mev = 0.0;
+    unsigned long long kmax = dkey(0.0), kmin = ~0ull;
+    if (cell_invariants(L, levels, bloch, F, l, tdev, mev)) {
+        kmax = dkey(tdev);
+        kmin = dkey(mev);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmax, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmin, o);
+        kmax = a > kmax ? a : kmax;
+        kmin = b < kmin ? b : kmin;
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_max[w] = kmax;
+        s_min[w] = kmin;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            kmax = s_max[i] > kmax ? s_max[i] : kmax;
+            kmin = s_min[i] < kmin ? s_min[i] : kmin;
+        }
+        atomicMax(&out[0], kmax);
+        if (kmin != ~0ull) atomicMin(&out[2], kmin);
+    }
 }
 
 unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
