@@ -415,3 +415,46 @@ def test_streamed_records_with_the_invariant_monitor():
     for x, y in zip(ra, rb):
         assert np.array_equal(x.data, y.data), x.name
     assert a.invariant_report == b.invariant_report
+
+
+def test_two_level_equivalence_bloch_vs_three_level_kernel():
+    """The reference's 2-level equivalence check (test_acceptance.py:163-190:
+    Bloch form vs the generic N-level step) across the GPU's two kernel
+    families: a two-level medium run by the Bloch kernel and the same medium
+    embedded in three levels (an isolated, empty third level) run by the
+    N-level kernel, 10^4 steps, E and the two-level block within 1e-9."""
+    qm2 = mb.two_level_description(1e24, 2 * math.pi * 2e14, 6.24e-11, 1e11, 1e12, -1.0)
+    h0 = np.zeros(3)
+    h0[:2] = np.real(np.diag(qm2.hamiltonian.matrix()))
+    mu_off = np.zeros(3, dtype=complex)
+    mu_off[0] = qm2.dipole_op.matrix()[0, 1]  # pair (0, 1) first in storage order
+    rates = np.zeros((3, 3))
+    rates[:2, :2] = qm2.dissipator.rates
+    deph = np.zeros(3)
+    deph[0] = 1e12 - 0.5 * 1e11
+    qm3 = mb.QmDescription(1e24, mb.QmOperator(h0), mb.QmOperator(np.zeros(3), mu_off),
+                           mb.LindbladRelaxation(rates, deph))
+
+    def build(qm, rho0, tag):
+        mb.clear_material_library()
+        mb.add_material(mb.Material("Vacuum"))
+        mb.add_material(mb.Material("Act" + tag, qm=qm))
+        dev = mb.Device("eq")
+        dev.add_region(mb.Region("l", "Vacuum", 0.0, 7.5e-6))
+        dev.add_region(mb.Region("a", "Act" + tag, 7.5e-6, 142.5e-6))
+        dev.add_region(mb.Region("r", "Vacuum", 142.5e-6, 150e-6))
+        dt0 = 0.5 * (150e-6 / 1023) / mb.C0
+        sce = mb.Scenario("s", 1024, 10000 * dt0 * (1 - 1e-12), mb.QmOperator(rho0))
+        sce.add_source(mb.SechPulse("s", 0.0, "hard", 4.2186e9, 2e14, 10.0, 2e14))
+        sce.add_record(mb.Record("e", quantity="e", interval=50 * dt0))
+        for i, j in ((1, 1), (2, 2), (1, 2)):
+            sce.add_record(mb.Record(f"d{i}{j}", quantity="d", i=i, j=j, interval=50 * dt0))
+        return mb.GpuFdtdSolver(dev, sce)
+
+    two = build(qm2, [1.0, 0.0], "2")
+    three = build(qm3, [1.0, 0.0, 0.0], "3")
+    assert two.grid.num_t - 1 == 10000 and three.plan.levels == 3
+    ra, rb = two.run(), three.run()
+    for a, b in zip(ra, rb):
+        scale = np.max(np.abs(a.data))
+        assert np.max(np.abs(a.data - b.data)) <= 1e-9 * scale, (a.name, np.max(np.abs(a.data - b.data)) / scale)
