@@ -103,7 +103,9 @@ def test_gloo_ranks_match_oracle_bitwise(world, k, period, case):
                                                ("rand4_rk4", 2, None), ("cfg4_r14", 4, None),
                                                # N-level periods that are not one launch: 3 launches of k = 4,
                                                # and a period that is not a multiple of k
-                                               ("rand6_split", 2, 12), ("cfg4_r14", 3, 10), ("rand3_split", 3, 29)])
+                                               ("rand6_split", 2, 12), ("cfg4_r14", 3, 10), ("rand3_split", 3, 29),
+                                               # eight slabs, as on a full B200 box
+                                               ("cfg2_r16", 8, None), ("cfg4_r14", 8, None)])
 def test_native_slabs_on_one_gpu_match_single_domain(case, count, period):
     """Windowed solvers (persistent multi-chunk launches between exchanges for
     the two-level / classical kernels) bit-identical to the single domain."""
