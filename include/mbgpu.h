@@ -139,6 +139,11 @@ int mbg_poll_nonfinite(mbg_solver *s, int64_t *bad_step); /* syncs; -1 when all 
  * out[0] max |trace - 1|, out[1] max Hermiticity deviation, out[2] min eigenvalue
  * over the owned quantum cells (+inf when there are none) */
 int mbg_invariants(mbg_solver *s, double *out);
+/* the same statistics folded into device-resident running maxima / minima
+ * without a host synchronisation (queued on the solver stream at every
+ * monitored step); mbg_invariants_read syncs and returns them */
+int mbg_invariants_accumulate(mbg_solver *s);
+int mbg_invariants_read(mbg_solver *s, double *out);
 int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols);
 int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im);
 /* Streamed records (the reference keeps every row in host memory,

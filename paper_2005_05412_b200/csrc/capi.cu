@@ -69,6 +69,7 @@ struct mbg_solver {
     double *src_values = nullptr;
     std::vector<Rec> recs;
     unsigned long long *bad = nullptr;
+    unsigned long long *inv = nullptr;  // running invariant keys (mbg_invariants_accumulate)
     double *ck_e = nullptr, *ck_h = nullptr, *ck_s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t marks[MBG_MAX_MARKS] = {};
@@ -488,6 +489,7 @@ void mbg_destroy(mbg_solver *s) {
         dfree(st, s->s[b]);
     }
     dfree(st, s->bad);
+    dfree(st, s->inv);
     dfree(st, s->wave);
     dfree(st, s->wave_items);
     dfree(st, s->ck_e);
@@ -1037,6 +1039,34 @@ int mbg_invariants(mbg_solver *s, double *out) {
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
     dfree(s->stream, d);
+    CK(cudaStreamSynchronize(s->stream));
+    out[0] = from_key(h[0]);
+    out[1] = 0.0;  // Hermitian-packed state: exactly Hermitian
+    out[2] = h[2] == ~0ull ? INFINITY : from_key(h[2]);
+    return MBG_OK;
+}
+
+static const unsigned long long kInvInit[3] = {0x8000000000000000ull, 0x8000000000000000ull, ~0ull};
+
+int mbg_invariants_accumulate(mbg_solver *s) {
+    if (!s) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    if (!s->inv) {
+        CK(dalloc(s->stream, reinterpret_cast<double **>(&s->inv), sizeof(kInvInit)));
+        CK(cudaMemcpyAsync(s->inv, kInvInit, sizeof(kInvInit), cudaMemcpyHostToDevice, s->stream));
+    }
+    if (int rc = sync_frame(s)) return rc;
+    const Launch L = base_launch(s);
+    if (s->words > 0) CK(launch_invariants(L, s->g.levels, s->bloch ? 1 : 0, state_frame(s), s->inv, s->stream));
+    ++s->launches;
+    return MBG_OK;
+}
+
+int mbg_invariants_read(mbg_solver *s, double *out) {
+    if (!s || !out) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    unsigned long long h[3] = {kInvInit[0], kInvInit[1], kInvInit[2]};
+    if (s->inv) CK(cudaMemcpyAsync(h, s->inv, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     out[0] = from_key(h[0]);
     out[1] = 0.0;  // Hermitian-packed state: exactly Hermitian

@@ -17,7 +17,6 @@ and the mblight CLI resolve to this solver.
 from __future__ import annotations
 
 import ctypes as C
-import math
 import sys
 
 import numpy as np
@@ -255,8 +254,11 @@ class GpuFdtdSolver:
 
     def _run_on(self, h, poll_every: int = 1 << 14):
         """Sample row 0, then advance steps 1..num_t-1 in chunks, polling the
-        device-side non-finite flag between chunks (a chunk is a multiple of the
-        1024-step scan cadence, so the first failing scan is the one reported)."""
+        device-side non-finite flag every ``poll_every`` steps and at the end
+        (the device keeps the first failing scan step, so that is the one
+        reported).  With the invariant monitor the chunks end on monitored
+        steps, where the statistics are folded on the device without a host
+        synchronisation and read once at the end."""
         num_t = self.grid.num_t
         segment = self._segment_steps()
         if segment:
@@ -264,27 +266,33 @@ class GpuFdtdSolver:
         h.call("mbg_sample", 0)
         monitor = self._monitor_cadence()
         if monitor is not None:
-            self._update_invariants(h)
+            h.call("mbg_invariants_accumulate")
         chunk = poll_every if monitor is None else max(1, monitor)
         if segment:
             chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
         n = 1
+        since = 0
         h.call("mbg_event_begin")
         while n < num_t:
             cnt = min(chunk, num_t - n)
             h.call("mbg_advance", n, cnt)
             n += cnt
-            bad = C.c_int64(-1)
-            h.call("mbg_poll_nonfinite", C.byref(bad))
-            if bad.value >= 0:
-                raise SolverError(f"non-finite electric field at step {bad.value}")
+            since += cnt
+            if monitor is not None and (n - 1) % monitor == 0:
+                h.call("mbg_invariants_accumulate")
             if segment:
                 self._drain_streams(h, n - 1)
-            if monitor is not None and (n - 1) % monitor == 0:
-                self._update_invariants(h)
+            if since >= poll_every or n >= num_t or segment:
+                since = 0
+                bad = C.c_int64(-1)
+                h.call("mbg_poll_nonfinite", C.byref(bad))
+                if bad.value >= 0:
+                    raise SolverError(f"non-finite electric field at step {bad.value}")
         ms = C.c_float(0)
         h.call("mbg_event_end", C.byref(ms))
         self.kernel_ms = float(ms.value)
+        if monitor is not None:
+            self._read_invariants(h)
         launches = C.c_int64(0)
         h.call("mbg_launch_count", C.byref(launches))
         self.launches = int(launches.value)
@@ -296,16 +304,12 @@ class GpuFdtdSolver:
             return None
         return min((p.every for p in self.plan.plans), default=256)
 
-    def _update_invariants(self, h):
-        """Device reduction over every quantum cell (mbg_invariants)."""
+    def _read_invariants(self, h):
+        """The device-side running statistics of every monitored step."""
         out = np.zeros(3)
-        h.call("mbg_invariants", native.ptr(out))
-        rep = self.invariant_report
-        if rep is None:
-            rep = self.invariant_report = {"max_trace_dev": 0.0, "max_herm_dev": 0.0, "min_eigenvalue": math.inf}
-        rep["max_trace_dev"] = max(rep["max_trace_dev"], float(out[0]))
-        rep["max_herm_dev"] = max(rep["max_herm_dev"], float(out[1]))
-        rep["min_eigenvalue"] = min(rep["min_eigenvalue"], float(out[2]))
+        h.call("mbg_invariants_read", native.ptr(out))
+        self.invariant_report = {"max_trace_dev": float(out[0]), "max_herm_dev": float(out[1]),
+                                 "min_eigenvalue": float(out[2])}
 
 
 def _rk4_factory(device, scenario, **kw):
