@@ -143,6 +143,10 @@ int mbg_invariants(mbg_solver *s, double *out);
  * without a host synchronisation (queued on the solver stream at every
  * monitored step); mbg_invariants_read syncs and returns them */
 int mbg_invariants_accumulate(mbg_solver *s);
+/* two-level splitting media: the step kernels fold the monitor themselves at
+ * every step that is a multiple of `every` (0: off), in the same running
+ * statistics -- no launch split at the monitored steps */
+int mbg_set_monitor(mbg_solver *s, int64_t every);
 int mbg_invariants_read(mbg_solver *s, double *out);
 int mbg_record_shape(const mbg_solver *s, int32_t r, int64_t *rows, int64_t *cols);
 int mbg_download_record(mbg_solver *s, int32_t r, double *re, double *im);

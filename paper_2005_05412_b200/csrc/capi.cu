@@ -70,6 +70,7 @@ struct mbg_solver {
     std::vector<Rec> recs;
     unsigned long long *bad = nullptr;
     unsigned long long *inv = nullptr;  // running invariant keys (mbg_invariants_accumulate)
+    long long inv_every = 0;            // two-level kernels fold the monitor every inv_every steps
     double *ck_e = nullptr, *ck_h = nullptr, *ck_s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t marks[MBG_MAX_MARKS] = {};
@@ -153,6 +154,8 @@ Launch base_launch(const mbg_solver *s) {
         L.rec_im[r] = R.im;
     }
     L.bad_step = s->bad;
+    L.inv = s->inv_every > 0 ? s->inv : nullptr;
+    L.inv_every = s->inv_every;
     L.rg = s->rg;
     return L;
 }
@@ -1059,6 +1062,18 @@ int mbg_invariants_accumulate(mbg_solver *s) {
     const Launch L = base_launch(s);
     if (s->words > 0) CK(launch_invariants(L, s->g.levels, s->bloch ? 1 : 0, state_frame(s), s->inv, s->stream));
     ++s->launches;
+    return MBG_OK;
+}
+
+int mbg_set_monitor(mbg_solver *s, int64_t every) {
+    if (!s || every < 0) return MBG_E_ARG;
+    if (every > 0 && !s->bloch) return fail(s, MBG_E_UNSUPPORTED, "the fused monitor is for two-level splitting media");
+    cudaSetDevice(s->g.device);
+    if (every > 0 && !s->inv) {
+        CK(dalloc(s->stream, reinterpret_cast<double **>(&s->inv), sizeof(kInvInit)));
+        CK(cudaMemcpyAsync(s->inv, kInvInit, sizeof(kInvInit), cudaMemcpyHostToDevice, s->stream));
+    }
+    s->inv_every = every;
     return MBG_OK;
 }
 

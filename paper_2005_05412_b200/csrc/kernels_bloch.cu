@@ -63,6 +63,22 @@ __device__ __forceinline__ void st2(double *p, double a, double b) {
     *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
+// order-preserving key of a double (atomicMin over doubles), as the monitor kernel's
+__device__ __forceinline__ unsigned long long order_key(double v) {
+    const unsigned long long b = __double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// fused invariant monitor of a two-level warp: min over its lanes' keys, one atomic
+__device__ __forceinline__ void fold_min_eig(unsigned long long *inv, unsigned long long key) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, key, o);
+        key = other < key ? other : key;
+    }
+    if ((threadIdx.x & 31) == 0 && key != ~0ull) atomicMin(inv + 2, key);
+}
+
 // _kernels.py:200-232, same expression order (each mad(a, b, c) is the
 // reference's "c + a*b" term)
 __device__ __forceinline__ double bloch_cell(const BlochQm &q, double e, double &x, double &y, double &z) {
@@ -344,6 +360,19 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
             }
+            if (L.inv && n % L.inv_every == 0) {  // eigenvalues (1 +- |v|)/2 (_kernels.py:541-546)
+                unsigned long long key = ~0ull;
+#pragma unroll
+                for (int i = 0; i < C; ++i) {
+                    const long long c = base + i * 32 + lane;
+                    if (c < t_lo || c >= t_hi || c < L.own_lo || c >= L.own_hi || qi[i] < 0) continue;
+                    double x, y, z;
+                    frame_true(P.frame, qi[i], X[i], Y[i], Z[i], x, y, z);
+                    const unsigned long long kk = order_key(0.5 * (1.0 - sqrt(x * x + y * y + z * z)));
+                    key = kk < key ? kk : key;
+                }
+                fold_min_eig(L.inv, key);
+            }
         }
     }
     // ---- write back the tile's result cells -------------------------------------
@@ -399,7 +428,7 @@ struct SharedSpan {
 // material the stepper constants are constant-bank operands.
 // hook(): runs once the tile's loads are in flight, before the first step
 // (the persistent kernel stages its step masks and claims its next item there)
-template <bool QM, bool ONE_QM, bool REAL, bool A1, class Span, class Hook>
+template <bool QM, bool ONE_QM, bool REAL, bool A1, bool MON, class Span, class Hook>
 __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &K, const Span &span, int r_e, int r_h,
                                              const Hook &hook) {
     __shared__ double seam_e[2][kBlochWarpsPerBlock], seam_h[2][kBlochWarpsPerBlock];
@@ -494,6 +523,19 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
             }
+            if (MON && QM && L.inv && n % L.inv_every == 0) {  // fused invariant monitor (see run_tile)
+                unsigned long long key = ~0ull;
+#pragma unroll
+                for (int i = 0; i < C; ++i) {
+                    const long long c = first + i;
+                    if (c < t_lo || c >= t_hi || c < L.own_lo || c >= L.own_hi) continue;
+                    double x, y, z;
+                    frame_true(P.frame, qmi, X[i], Y[i], Z[i], x, y, z);
+                    const unsigned long long kk = order_key(0.5 * (1.0 - sqrt(x * x + y * y + z * z)));
+                    key = kk < key ? kk : key;
+                }
+                fold_min_eig(L.inv, key);
+            }
         }
     }
     const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
@@ -540,17 +582,22 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk 
     const int re = region_of(L.rg.e_start, L.rg.n, base), rh = region_of(L.rg.h_start, L.rg.n, base);
     const int qm = L.rg.qm[re];
     const bool a1 = L.rg.a[re] == 1.0;  // lossless region (the fast variant fuses the p term)
+    // MON: the fused invariant monitor; the hot single-medium variants get a
+    // monitor-free instantiation so the unmonitored step loop is unchanged
     if (qm < 0)
-        a1 ? interior_cta<false, true, false, true>(P, K, span, re, rh, hook)
-           : interior_cta<false, true, false, false>(P, K, span, re, rh, hook);
+        a1 ? interior_cta<false, true, false, true, false>(P, K, span, re, rh, hook)
+           : interior_cta<false, true, false, false, false>(P, K, span, re, rh, hook);
+    else if (P.real_dipole && P.n_qm == 1 && !L.inv)
+        a1 ? interior_cta<true, true, true, true, false>(P, K, span, re, rh, hook)
+           : interior_cta<true, true, true, false, false>(P, K, span, re, rh, hook);
     else if (P.real_dipole && P.n_qm == 1)
-        a1 ? interior_cta<true, true, true, true>(P, K, span, re, rh, hook)
-           : interior_cta<true, true, true, false>(P, K, span, re, rh, hook);
+        a1 ? interior_cta<true, true, true, true, true>(P, K, span, re, rh, hook)
+           : interior_cta<true, true, true, false, true>(P, K, span, re, rh, hook);
     else if (P.real_dipole)
-        interior_cta<true, false, true, false>(P, K, span, re, rh, hook);
+        interior_cta<true, false, true, false, true>(P, K, span, re, rh, hook);
     else
-        P.n_qm == 1 ? interior_cta<true, true, false, false>(P, K, span, re, rh, hook)
-                    : interior_cta<true, false, false, false>(P, K, span, re, rh, hook);
+        P.n_qm == 1 ? interior_cta<true, true, false, false, true>(P, K, span, re, rh, hook)
+                    : interior_cta<true, false, false, false, true>(P, K, span, re, rh, hook);
 }
 
 // one warp over the result range [t_lo, t_hi) of at most 32*C - 2k cells

@@ -66,6 +66,10 @@ struct Launch {
     unsigned long long step_mask[kMaxTileSteps];  // bit r: record r samples at fused step s
     unsigned char check[kMaxTileSteps];           // 1: non-finite scan at fused step s
     unsigned long long *bad_step;
+    // two-level invariant monitor fused into the record steps (null: off):
+    // running min-eigenvalue key at inv[2], every inv_every steps
+    unsigned long long *inv;
+    long long inv_every;
     Regions rg;
 };
 

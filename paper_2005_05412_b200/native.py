@@ -69,6 +69,7 @@ SIGNATURES = {
     "mbg_invariants": (C.c_int, [_h, _dp]),
     "mbg_invariants_accumulate": (C.c_int, [_h]),
     "mbg_invariants_read": (C.c_int, [_h, _dp]),
+    "mbg_set_monitor": (C.c_int, [_h, C.c_int64]),
     "mbg_record_shape": (C.c_int, [_h, C.c_int32, _i64p, _i64p]),
     "mbg_download_record": (C.c_int, [_h, C.c_int32, _dp, _dp]),
     "mbg_set_record_rows": (C.c_int, [_h, C.c_int32, C.c_int64]),

@@ -256,18 +256,24 @@ class GpuFdtdSolver:
         """Sample row 0, then advance steps 1..num_t-1 in chunks, polling the
         device-side non-finite flag every ``poll_every`` steps and at the end
         (the device keeps the first failing scan step, so that is the one
-        reported).  With the invariant monitor the chunks end on monitored
-        steps, where the statistics are folded on the device without a host
-        synchronisation and read once at the end."""
+        reported).  The invariant monitor's statistics are folded on the device
+        without a host synchronisation (inside the two-level step kernels, or
+        by a reduction at each monitored step) and read once at the end."""
         num_t = self.grid.num_t
         segment = self._segment_steps()
         if segment:
             self._open_streams(h, segment)
         h.call("mbg_sample", 0)
-        monitor = self._monitor_cadence()
-        if monitor is not None:
-            h.call("mbg_invariants_accumulate")
-        chunk = poll_every if monitor is None else max(1, monitor)
+        every = self._monitor_cadence()
+        if every is not None:
+            h.call("mbg_invariants_accumulate")  # the initial state
+        # two-level splitting: the step kernels fold the monitor at its steps
+        # themselves; otherwise the run stops at each monitored step for it
+        fused = every is not None and self.plan.levels == 2 and self.stepper == "splitting"
+        if fused:
+            h.call("mbg_set_monitor", every)
+        split = None if fused else every
+        chunk = poll_every if split is None else max(1, split)
         if segment:
             chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
         n = 1
@@ -278,7 +284,7 @@ class GpuFdtdSolver:
             h.call("mbg_advance", n, cnt)
             n += cnt
             since += cnt
-            if monitor is not None and (n - 1) % monitor == 0:
+            if split is not None and (n - 1) % split == 0:
                 h.call("mbg_invariants_accumulate")
             if segment:
                 self._drain_streams(h, n - 1)
@@ -291,7 +297,7 @@ class GpuFdtdSolver:
         ms = C.c_float(0)
         h.call("mbg_event_end", C.byref(ms))
         self.kernel_ms = float(ms.value)
-        if monitor is not None:
+        if every is not None:
             self._read_invariants(h)
         launches = C.c_int64(0)
         h.call("mbg_launch_count", C.byref(launches))

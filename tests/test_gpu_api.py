@@ -458,3 +458,40 @@ def test_two_level_equivalence_bloch_vs_three_level_kernel():
     for a, b in zip(ra, rb):
         scale = np.max(np.abs(a.data))
         assert np.max(np.abs(a.data - b.data)) <= 1e-9 * scale, (a.name, np.max(np.abs(a.data - b.data)) / scale)
+
+
+@pytest.mark.parametrize("case", ["sit_hard_whole", "multi_material", "cfg2_r16"])
+def test_fused_two_level_monitor_equals_stepwise_numpy(case):
+    """The two-level step kernels fold the monitor themselves (mbg_set_monitor):
+    the report equals numpy's eigenvalues (1 - |v|)/2 of the state downloaded
+    at every monitored step of a stepwise run (_kernels.py:541-546)."""
+    from paper_2005_05412_b200 import native
+
+    dev, sce, stepper = build_case(case)
+    fused = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    fused.run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case(case)
+    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    every = min(p.every for p in s.plan.plans)
+    cells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in s.plan.groups])
+    h = s.open_handle()
+    mins = []
+    try:
+        s.upload_initial_state(h)
+        h.call("mbg_sample", 0)
+        words = np.zeros((3, s.grid.num_x))
+        n = 0
+        while True:
+            h.call("mbg_download_state", native.ptr(words))
+            v = words[:, cells]
+            mins.append(0.5 * (1.0 - np.max(np.sqrt(np.sum(v * v, axis=0)))))
+            if n + every > s.grid.num_t - 1:
+                break
+            h.call("mbg_advance", n + 1, every)
+            n += every
+    finally:
+        h.close()
+    rep = fused.invariant_report
+    assert rep["max_trace_dev"] == 0.0 and rep["max_herm_dev"] == 0.0
+    assert rep["min_eigenvalue"] == pytest.approx(min(mins), abs=1e-15)
