@@ -64,6 +64,11 @@ extern "C" {
 /* mbg_grid.flags: one kernel launch per k fused steps instead of the
    persistent wavefront launch (two-level / classical, non-windowed solvers) */
 #define MBG_FLAG_PER_LAUNCH 1
+/* two-level / classical media: always the persistent wavefront launch (by
+ * default it is used when a fused chunk has at least one tile per SM; a
+ * narrower domain is a chain of few tiles, faster as one launch per chunk
+ * with a whole SM per tile) */
+#define MBG_FLAG_PERSISTENT 2
 
 typedef struct mbg_solver mbg_solver;
 

@@ -842,6 +842,17 @@ static int check_ready(mbg_solver *s) {
 namespace {
 
 // the whole step range in one persistent launch (kernels_bloch.cu, BlochWave)
+// the persistent wavefront pays off when a chunk has at least one tile per
+// SM; a few-tile domain (cfg1: 17 tiles) is a dependency chain whose items
+// run faster with a whole SM each, one launch per chunk (73 vs 200 ms)
+bool wave_worthwhile(const mbg_solver *s, int tw) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->g.device) != cudaSuccess || sms <= 0)
+        sms = 148;
+    const long long tiles = s->win_n / std::max(1, tw - 2 * s->k);
+    return tiles >= sms;
+}
+
 int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
     const int k = s->k;
     Launch L = base_launch(s);
@@ -975,7 +986,8 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     }
     cudaSetDevice(s->g.device);
     const int tw = tile_width(s);
-    if ((s->bloch || s->g.levels == 0) && !(s->g.flags & MBG_FLAG_PER_LAUNCH) && n_steps > s->k)
+    if ((s->bloch || s->g.levels == 0) && !(s->g.flags & MBG_FLAG_PER_LAUNCH) && n_steps > s->k &&
+        ((s->g.flags & MBG_FLAG_PERSISTENT) || wave_worthwhile(s, tw)))
         return advance_wave(s, first, n_steps, tw);
     long long n = first;
     const long long end = first + n_steps;

@@ -47,8 +47,10 @@ class GpuFdtdSolver:
       ``tile_steps`` -- time steps fused per kernel launch (k; default per N),
       ``exact``      -- disable FMA contraction (bit-exact two-level path),
       ``gpu``        -- CUDA device ordinal,
-      ``persistent`` -- two-level / classical runs: one persistent wavefront
-                        launch per advance (False: one launch per k steps),
+      ``persistent`` -- two-level / classical runs: True = one persistent
+                        wavefront launch per advance, False = one launch per
+                        k steps, None (default) = the wavefront when a fused
+                        chunk has at least one tile per SM,
       ``record_segment`` -- stream the records: keep only the rows of this
                         many time steps in HBM and copy completed rows into
                         the host result arrays after every segment (None:
@@ -57,7 +59,7 @@ class GpuFdtdSolver:
     """
 
     def __init__(self, device, scenario, stepper="splitting", threads=None, seed=None,
-                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=True,
+                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=None,
                  record_segment=None):
         self.plan = build_plan(device, scenario, stepper, seed)
         self.device = device
@@ -71,7 +73,7 @@ class GpuFdtdSolver:
         self.tile_steps = tile_steps
         self.exact = bool(exact)
         self.gpu = int(gpu)
-        self.persistent = bool(persistent)
+        self.persistent = None if persistent is None else bool(persistent)
         self.record_segment = record_segment
         self._host_rows = None
         self.results = None
@@ -99,7 +101,7 @@ class GpuFdtdSolver:
         s.tile_steps = int(self.tile_steps or 0)
         s.exact = 1 if self.exact else 0
         s.device = self.gpu
-        s.flags = 0 if self.persistent else native.MBG_FLAG_PER_LAUNCH
+        s.flags = {None: 0, True: native.MBG_FLAG_PERSISTENT, False: native.MBG_FLAG_PER_LAUNCH}[self.persistent]
         s.win_lo, s.win_hi = win if win is not None else (0, g.num_x)
         s.own_lo, s.own_hi = own if own is not None else (s.win_lo, s.win_hi)
         return s

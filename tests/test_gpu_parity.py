@@ -82,7 +82,7 @@ def test_persistent_wavefront_matches_per_launch(name, k):
     their neighbours of the previous chunk) against one launch per k steps."""
     _, ref = _run(name, tile_steps=k, persistent=False)
     mb.clear_material_library()
-    solver, got = _run(name, tile_steps=k)
+    solver, got = _run(name, tile_steps=k, persistent=True)
     assert solver.launches < solver.grid.num_t // 2
     for a, b in zip(ref, got):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name

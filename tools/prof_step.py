@@ -37,7 +37,7 @@ if a.config == "cfg5":
 else:
     dev, sce = getattr(configs, a.config)(mb, **kw, **({"steps": total} if a.config != "cfg1" else {}))
 sol = mb.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact,
-                       persistent=not a.per_launch)
+                       persistent=False if a.per_launch else None)
 h = sol.open_handle()
 sol.upload_initial_state(h)
 k = C.c_int32(0)
