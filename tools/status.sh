@@ -4,6 +4,7 @@
 set -e
 cd "$(dirname "$0")/.."
 run() { echo -n "$*: "; timeout 300 python tools/prof_step.py "$@" | grep -o "device.*"; }
+run cfg1 --steps 26196                      # two-level SIT, 32768 cells, the full run (one launch per chunk)
 run cfg2 --steps 20000                      # two-level, 2^22 cells, the full 20000-step run (persistent kernel)
 run cfg3 --steps 96                         # three-level Lambda medium, 2^23 cells (real-operator path)
 run cfg4 --steps 96                         # six-level QCL-like medium, 2^24 cells (complex Hamiltonian)
