@@ -164,7 +164,9 @@ def run_reference(args, world, rank):
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as orc
 
-    import paper_2005_05412_b200 as mb
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mb
     from paper_2005_05412_b200.plan import build_plan
 
     dev, sce = build_workload(mb, args.gpus)
@@ -214,7 +216,9 @@ MARK_STEPS = 31  # per-step advance timing marks (mbg_mark slots 2..63)
 def run_mine(args, world, rank, local):
     import ctypes as C
 
-    import paper_2005_05412_b200 as mb
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mb
     from paper_2005_05412_b200 import native
 
     dev, sce = build_workload(mb, args.gpus)
@@ -223,7 +227,7 @@ def run_mine(args, world, rank, local):
         return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT, clock_sampler=ClockSampler,
                                 rebuild=lambda: build_workload(mb, args.gpus))
 
-    solver = mb.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+    solver = gpu.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
     plan = solver.plan
     num_t = plan.grid.num_t
     nx = plan.grid.num_x
@@ -334,7 +338,7 @@ def run_mine(args, world, rank, local):
     for it in range(args.warmup + args.steps):
         mb.clear_material_library()
         d2, s2 = build_workload(mb, 1)
-        sol = mb.GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
+        sol = gpu.GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
         t0 = time.perf_counter()
         res = sol.run()
         dt_run = time.perf_counter() - t0
@@ -378,7 +382,9 @@ def n_level_samples(local, chunks=16):
     headline, not the headline), with the roofline of SURVEY 8(d)."""
     import ctypes as C
 
-    import paper_2005_05412_b200 as mb
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mb
     from paper_2005_05412_b200 import configs, native
 
     peak = C.c_double(0)
@@ -387,7 +393,7 @@ def n_level_samples(local, chunks=16):
     for name, n in (("cfg3", 3), ("cfg4", 6)):
         mb.clear_material_library()
         dev, sce = getattr(configs, name)(mb)
-        sol = mb.GpuFdtdSolver(dev, sce, gpu=local)
+        sol = gpu.GpuFdtdSolver(dev, sce, gpu=local)
         h = sol.open_handle()
         sol.upload_initial_state(h)
         k = C.c_int32(0)

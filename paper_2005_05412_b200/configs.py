@@ -96,7 +96,8 @@ def _splitmix(api):
     return fn
 
 
-def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", replicas=1):
+def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", replicas=1,
+         quantities=("e", "d11", "d22", "inv")):
     """cfg 1 lengthened to 2^22 cells with T1 = 1 ns, T2 = 1 ps, drawn inversion.
 
     ``replicas`` G > 1 builds the weak-scaling variant: G copies of the 150 um
@@ -122,7 +123,7 @@ def cfg2(api, nx=1 << 22, steps=20000, cells=None, stress=False, tag="", replica
     sce.add_source(sit_source(api))
     if cells is None:
         cells = (16, nx // 2, nx - 17) if stress else (16, 4096, 8192)
-    _add_records(api, dev, sce, cells, ("e", "d11", "d22", "inv"))
+    _add_records(api, dev, sce, cells, quantities)
     return dev, sce
 
 

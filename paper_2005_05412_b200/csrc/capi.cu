@@ -471,9 +471,12 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
         cudaMemsetAsync(s->h[b], 0, fb, s->stream);
         cudaMemsetAsync(s->s[b], 0, sb, s->stream);
     }
-    if (dalloc(s->stream, reinterpret_cast<double **>(&s->bad), sizeof(unsigned long long)) != cudaSuccess)
+    // [0] first failing scan step (~0: none), [1] stall flag of the persistent
+    // launches: sticky -- only check_stall clears it, after reporting it
+    if (dalloc(s->stream, reinterpret_cast<double **>(&s->bad), 2 * sizeof(unsigned long long)) != cudaSuccess)
         return cleanup(MBG_E_CUDA);
     cudaMemsetAsync(s->bad, 0xff, sizeof(unsigned long long), s->stream);
+    cudaMemsetAsync(s->bad + 1, 0, sizeof(unsigned long long), s->stream);
     cudaEventCreate(&s->ev0);
     cudaEventCreate(&s->ev1);
     if (cudaStreamSynchronize(s->stream) != cudaSuccess) return cleanup(MBG_E_CUDA);
@@ -900,7 +903,7 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
     }
     const long long tiles = s->wave_n;
     const long long n_chunks = (n_steps + k - 1) / k;
-    // [ticket, stall, done flags][masks (8 B per step)][checks (1 B per step)], in 4-byte words
+    // [ticket, unused, done flags][masks (8 B per step)][checks (1 B per step)], in 4-byte words
     const long long flags = 2 + n_chunks * tiles;
     const long long mask_off = (flags + 1) / 2 * 2, check_off = mask_off + 2 * n_chunks * k;
     const long long need = check_off + (n_chunks * k + 3) / 4;
@@ -931,7 +934,7 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
     }
     V.cur = s->cur;
     V.ticket = s->wave;
-    V.stall = s->wave + 1;
+    V.stall = reinterpret_cast<unsigned *>(s->bad + 1);  // sticky across launches
     V.done = s->wave + 2;
     CK(s->g.exact ? exact::launch_wave_masks(L, n_steps, V.last_step, masks, checks, s->stream)
                   : fast::launch_wave_masks(L, n_steps, V.last_step, masks, checks, s->stream));
@@ -957,12 +960,18 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
     return MBG_OK;
 }
 
-// after a stream synchronize: a persistent launch that gave up waiting is an error
+// after a stream synchronize: a persistent launch that gave up waiting is an
+// error.  The flag survives later launches (they are not allowed to clear it),
+// so a timeout is reported at the first synchronisation after it, however
+// many advances were enqueued in between; it is cleared once reported.
 int check_stall(mbg_solver *s) {
     if (!s->wave) return MBG_OK;
     unsigned v = 0;
-    CK(cudaMemcpy(&v, s->wave + 1, sizeof(v), cudaMemcpyDeviceToHost));
-    if (v) return fail(s, MBG_E_CUDA, "persistent step kernel: dependency wait timed out");
+    CK(cudaMemcpy(&v, s->bad + 1, sizeof(v), cudaMemcpyDeviceToHost));
+    if (v) {
+        CK(cudaMemset(s->bad + 1, 0, sizeof(unsigned long long)));
+        return fail(s, MBG_E_CUDA, "persistent step kernel: dependency wait timed out");
+    }
     return MBG_OK;
 }
 
@@ -1005,7 +1014,7 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
             for (size_t r = 0; r < s->recs.size(); ++r)
                 if (step % s->recs[r].every == 0) m |= 1ull << r;
             L.step_mask[t] = m;
-            L.check[t] = (step % 1024 == 0 || step == s->g.num_t - 1) ? 1 : 0;
+            L.check[t] = step_flags(L, step, s->g.num_t - 1);
         }
         const long long tiles = (L.res_hi - L.res_lo + L.tile_own - 1) / L.tile_own;
         int kernels = 0;

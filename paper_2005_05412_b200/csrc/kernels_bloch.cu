@@ -327,8 +327,9 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
         }
         // ---- non-finite scan and records (owned result cells only) --------------
         const unsigned long long mask = K.mask[s];
-        const bool check = K.check[s] != 0;
-        if (mask || check) {
+        const unsigned char flags = K.check[s];
+        const bool check = (flags & MBG_STEP_SCAN) != 0;
+        if (mask || flags) {
 #pragma unroll
             for (int i = 0; i < C; ++i) {
                 const long long c = base + i * 32 + lane;
@@ -360,7 +361,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
             }
-            if (L.inv && n % L.inv_every == 0) {  // eigenvalues (1 +- |v|)/2 (_kernels.py:541-546)
+            if (L.inv && (flags & MBG_STEP_MONITOR)) {  // eigenvalues (1 +- |v|)/2 (_kernels.py:541-546)
                 unsigned long long key = ~0ull;
 #pragma unroll
                 for (int i = 0; i < C; ++i) {
@@ -490,8 +491,9 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                       : mad(bdx, hr - H[i], (MBG_POL_FOLD && A1) ? E[i] : a * E[i]);
         }
         const unsigned long long mask = s_mask[s];
-        const bool check = s_check[s] != 0;
-        if (mask || check) {
+        const unsigned char flags = s_check[s];
+        const bool check = (flags & MBG_STEP_SCAN) != 0;
+        if (mask || flags) {
             const long long n = K.n0 + s;
             const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
 #pragma unroll
@@ -523,7 +525,7 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
             }
-            if (MON && QM && L.inv && n % L.inv_every == 0) {  // fused invariant monitor (see run_tile)
+            if (MON && QM && L.inv && (flags & MBG_STEP_MONITOR)) {  // fused invariant monitor (see run_tile)
                 unsigned long long key = ~0ull;
 #pragma unroll
                 for (int i = 0; i < C; ++i) {
@@ -674,7 +676,7 @@ __global__ void wave_mask_kernel(const __grid_constant__ Launch L, long long n_s
     for (int r = 0; r < L.n_rec; ++r)
         if (n % L.rec_every[r] == 0) m |= 1ull << r;
     masks[i] = m;
-    checks[i] = (n % 1024 == 0 || n == last_step) ? 1 : 0;
+    checks[i] = step_flags(L, n, last_step);
 }
 
 // item's dependencies: items t-1 .. t+1 of the previous chunk.  One pass

@@ -609,7 +609,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
         E = en;
         H = hn;
         const unsigned long long mask = L.step_mask[s];
-        const bool check = L.check[s] != 0;
+        const bool check = (L.check[s] & MBG_STEP_SCAN) != 0;
         if ((mask || check) && own()) {
             const long long c = cell();
             if (check && !isfinite(E)) atomicMin(L.bad_step, (unsigned long long)n);

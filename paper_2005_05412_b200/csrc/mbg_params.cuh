@@ -64,7 +64,7 @@ struct Launch {
     double *rec_re[kMaxRecords];
     double *rec_im[kMaxRecords];
     unsigned long long step_mask[kMaxTileSteps];  // bit r: record r samples at fused step s
-    unsigned char check[kMaxTileSteps];           // 1: non-finite scan at fused step s
+    unsigned char check[kMaxTileSteps];           // MBG_STEP_* flags of fused step s
     unsigned long long *bad_step;
     // two-level invariant monitor fused into the record steps (null: off):
     // running min-eigenvalue key at inv[2], every inv_every steps
@@ -72,6 +72,18 @@ struct Launch {
     long long inv_every;
     Regions rg;
 };
+
+// per-step flags (Launch::check, the persistent launch's check bytes)
+enum : unsigned char { MBG_STEP_SCAN = 1, MBG_STEP_MONITOR = 2 };
+
+// the reference's non-finite scan (every 1024 steps and the last,
+// solver_fdtd.py:386-388) and the invariant monitor's cadence
+// (solver_fdtd.py:425-426: every monitored step, records or not)
+__host__ __device__ inline unsigned char step_flags(const Launch &L, long long n, long long last_step) {
+    unsigned char f = (n % 1024 == 0 || n == last_step) ? MBG_STEP_SCAN : 0;
+    if (L.inv && L.inv_every > 0 && n % L.inv_every == 0) f |= MBG_STEP_MONITOR;
+    return f;
+}
 
 // two-level splitting in Bloch form (_kernels.py:200-232)
 struct BlochQm {

@@ -14,7 +14,13 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import NativeError
+from .reference import mblight
+
+
+class NativeError(mblight.SolverError):
+    """The CUDA library reported a failure (launch, allocation, argument), or
+    it is missing: there is no CPU fallback."""
+
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("MBGPU_LIB", PKG / "_build" / "libmbgpu.so"))

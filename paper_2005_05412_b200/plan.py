@@ -1,144 +1,75 @@
 """Host-side setup of one run: everything the fused GPU kernels consume.
 
-This restates the constructor of the reference solver
-(``FdtdSolver.__init__``, ``mblight/solver_fdtd.py:207-326``) minus the time
-loop: grid sizing (``init_fdtd_simulation``, ``solver_fdtd.py:80-102``),
-per-material update coefficients (``get_fdtd_constants``,
-``solver_fdtd.py:122-133``), the cell -> region map (``solver_fdtd.py:242-272``),
-quantum groups and their stepper constants (``_kernels.py:351-374,
-431-439, 467-500``), sources, record plans (``solver_fdtd.py:136-172``) and
-the boundary constants (``solver_fdtd.py:310-325``).
+The constructor of the reference solver (``FdtdSolver.__init__``,
+``mblight/solver_fdtd.py:207-326``) minus the time loop and the state arrays.
+Everything that is a function or class of the reference is called, not
+restated: validation (``scenario_validate``), grid sizing
+(``init_fdtd_simulation``, ``solver_fdtd.py:80-102``), per-material
+coefficients (``get_fdtd_constants``, ``solver_fdtd.py:122-133``), record
+schedules (``_RecordPlan``, ``solver_fdtd.py:136-172``), the worker count
+(``_resolve_threads``) and the stepper constants, read from the reference's
+own kernel objects built for one cell (``BlochSplittingKernel`` /
+``VectorSplittingKernel`` / ``VectorRk4Kernel``, ``_kernels.py:340-560``).
+What remains here is the layout the GPU needs instead of the reference's
+per-cell arrays.
 
 Where the reference stores per-cell coefficient arrays (32 B/cell read
 every step), the plan keeps a *region table*: region r covers E cells
 [e_start[r], e_start[r+1]) and H nodes [h_start[r], h_start[r+1]); the
 kernels look coefficients up by region, so no coefficient bytes cross HBM.
 The tables are derived from the very same ``searchsorted`` maps the
-reference builds, so the per-cell values are identical.
-
-The plan only reads attributes of the device/scenario objects, so both this
-package's setup model and the reference ``mblight`` objects work.
+reference builds (``solver_fdtd.py:242-272``), so the per-cell values are
+identical.
 """
 
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from .constants import HBAR
-from .errors import ValidationError
-from .qm import precompute_relaxation_propagator
-from .setup_model import DEFAULT_SEED, scenario_validate
+from .reference import core, kernels, mblight, solver_fdtd
 
-COURANT_NUMBER = 0.5
-NONFINITE_CHECK_EVERY = 1024  # solver_fdtd.py:50
+COURANT_NUMBER = solver_fdtd.COURANT_NUMBER
+NONFINITE_CHECK_EVERY = solver_fdtd._NONFINITE_CHECK_EVERY
 QUANTITY_CODES = {"e": 0, "h": 1, "d": 2, "inv": 3}
 STEPPERS = ("splitting", "rk4")
 
-
-@dataclass(frozen=True)
-class GridLayout:
-    """Spatio-temporal discretisation (field names of ``solver_fdtd.py:69-77``)."""
-
-    num_x: int
-    dx: float
-    num_t: int
-    dt: float
-    courant: float = COURANT_NUMBER
-
-
-def init_fdtd_simulation(device, scenario) -> GridLayout:
-    """dx = L/(Nx-1); dt from Courant 0.5 at the fastest material, shrunk so an
-    integer number of steps lands on the end time (``solver_fdtd.py:80-102``)."""
-    nx = scenario.num_gridpoints
-    if nx == 1:
-        if scenario.num_timesteps is None or scenario.num_timesteps < 2:
-            raise ValueError("scenarios with a single grid point must specify num_timesteps")
-        nt = int(scenario.num_timesteps)
-        return GridLayout(1, 0.0, nt, scenario.end_time / (nt - 1))
-    c_max = max(m.light_speed for m in device.materials())
-    dx = device.length / (nx - 1)
-    dt0 = COURANT_NUMBER * dx / c_max
-    nt = int(math.ceil(scenario.end_time / dt0)) + 1
-    return GridLayout(nx, dx, nt, scenario.end_time / (nt - 1))
-
-
-@dataclass(frozen=True)
-class CellCoefficients:
-    a_prime: float
-    b_prime: float
-    c_prime: float
-    gamma: float
-    inv_dx: float
-    qm: object = None
-
-
-def get_fdtd_constants(material, dt: float, dx: float) -> CellCoefficients:
-    """Lossy-Yee coefficients a', b', c' of one material (``solver_fdtd.py:122-133``)."""
-    if not (dt > 0 and dx > 0):
-        raise ValueError("dt and dx must be positive")
-    eps = material.permittivity
-    loss = dt * material.conductivity / (2.0 * eps)
-    return CellCoefficients(
-        (1.0 - loss) / (1.0 + loss),
-        (dt / eps) / (1.0 + loss),
-        dt / (dx * material.permeability),
-        material.overlap_factor,
-        1.0 / dx,
-        material.qm,
-    )
-
-
-def resolve_threads(explicit, num_x: int) -> int:
-    """Host worker count, kept for API parity (``solver_fdtd.py:184-195``)."""
-    if explicit is not None:
-        n = int(explicit)
-    else:
-        env = os.environ.get("MBLIGHT_THREADS", "").strip()
-        n = int(env) if env else (os.cpu_count() or 1)
-    if n < 1:
-        raise ValueError("worker count must be at least 1")
-    return min(n, num_x)
+GridLayout = solver_fdtd.GridLayout
+CellCoefficients = solver_fdtd.CellCoefficients
+init_fdtd_simulation = solver_fdtd.init_fdtd_simulation
+get_fdtd_constants = solver_fdtd.get_fdtd_constants
+resolve_threads = solver_fdtd._resolve_threads
 
 
 class RecordPlan:
-    """Sampling schedule of one record (``solver_fdtd.py:136-172``)."""
+    """Sampling schedule of one record: the reference's ``_RecordPlan``
+    (``solver_fdtd.py:136-172``: every, rows, cell, cols, x0, the host
+    buffer and ``to_result``) plus the kernels' quantity code and 0-based
+    density indices."""
 
-    def __init__(self, record, grid: GridLayout):
+    def __init__(self, record, grid):
+        self.ref = solver_fdtd._RecordPlan(record, grid, grid.num_t)
         self.record = record
-        if record.interval > 0:
-            self.every = max(1, int(math.floor(record.interval / grid.dt + 0.5)))
-        else:
-            self.every = 1
-        self.rows = (grid.num_t - 1) // self.every + 1
-        half = 0.5 * grid.dx if record.quantity == "h" else 0.0
-        if record.position is None:
-            self.cell = None
-            self.cols = grid.num_x
-            self.x0 = -half
-        else:
-            self.cell = 0 if grid.num_x == 1 else int(math.floor(record.position / grid.dx + 0.5))
-            self.cols = 1
-            self.x0 = self.cell * grid.dx
-            if half:
-                self.x0 -= half
+        self.every, self.rows, self.cell = self.ref.every, self.ref.rows, self.ref.cell
+        self.cols, self.x0 = self.ref.cols, self.ref.x0
         self.quantity = QUANTITY_CODES[record.quantity]
         self.i = record.i - 1 if record.quantity == "d" else 0
         self.j = record.j - 1 if record.quantity == "d" else 0
         self.is_complex = bool(record.is_complex)
 
-    def to_result(self, grid: GridLayout, data: np.ndarray, result_cls):
-        return result_cls(
-            name=self.record.name,
-            data=data,
-            t0=0.0,
-            dt_sample=self.every * grid.dt,
-            x0=self.x0,
-            dx=grid.dx if self.cols > 1 else 0.0,
-        )
+    @property
+    def buffer(self) -> np.ndarray:
+        """The reference's host buffer of this record (rows x cols, float or complex)."""
+        return self.ref.buffer
+
+    def to_result(self, grid, data=None):
+        """The reference's ``Result`` (``_RecordPlan.to_result``) over ``data``
+        (default: the plan's own buffer)."""
+        if data is not None:
+            self.ref.buffer = data
+        return self.ref.to_result(grid)
 
 
 def state_words(levels: int, stepper: str = "splitting") -> int:
@@ -221,49 +152,47 @@ class QmConstants:
 
 
 def qm_constants(desc, dt: float, stepper: str) -> QmConstants:
+    """The stepper constants of one medium, read from the reference's own
+    kernel object for it (built for one cell; nothing is stepped): the
+    polarisation entries (``_kernels.py:360-374``), the Bloch constants
+    (``BlochSplittingKernel.__init__``, ``_kernels.py:467-494``), the
+    relaxation half step and the affine Cayley operands
+    (``VectorSplittingKernel.__init__``, ``_kernels.py:431-439``) or the RK4
+    operators (``VectorRk4Kernel.__init__``, ``_kernels.py:554-557``)."""
     n = desc.dim
-    mu = desc.dipole_op.matrix()
-    upper = [(i, j, mu[i, j]) for i in range(n) for j in range(i + 1, n) if mu[i, j] != 0]
-    diag = [(i, mu[i, i].real) for i in range(n) if mu[i, i] != 0]
+    if stepper == "rk4":
+        k = kernels.VectorRk4Kernel(desc, dt, 1)
+    elif n == 2:
+        k = kernels.BlochSplittingKernel(desc, dt, 1)
+    else:
+        k = kernels.VectorSplittingKernel(desc, dt, 1)
     qc = QmConstants(
         levels=n,
-        pol_factor=desc.density_3d / dt,
-        pol_i=np.array([u[0] for u in upper], dtype=np.int32),
-        pol_j=np.array([u[1] for u in upper], dtype=np.int32),
-        pol_v=np.array([u[2] for u in upper], dtype=np.complex128),
-        pol_di=np.array([d[0] for d in diag], dtype=np.int32),
-        pol_dv=np.array([d[1] for d in diag], dtype=np.float64),
+        pol_factor=k._pol_factor,
+        pol_i=k._pol_i.astype(np.int32),
+        pol_j=k._pol_j.astype(np.int32),
+        pol_v=k._pol_v,
+        pol_di=k._pol_di.astype(np.int32),
+        pol_dv=k._pol_dv,
     )
-    h0 = desc.hamiltonian.matrix()
-    a = 0.5 * dt / HBAR
     if stepper == "rk4":
-        qc.h0 = h0
-        qc.mu = mu
-        qc.pop_matrix = np.asarray(desc.dissipator.pop_matrix, dtype=float)
-        qc.deph_matrix = np.asarray(desc.dissipator.dephasing_matrix, dtype=float)
-        return qc
-    ws = precompute_relaxation_propagator(desc, dt)
-    if n == 2:
-        pop = ws.pop_half
-        # identical expression order to BlochSplittingKernel.__init__
+        qc.h0 = np.asarray(k._h0, dtype=complex)
+        qc.mu = np.asarray(k._mu, dtype=complex)
+        qc.pop_matrix = np.asarray(k._pop, dtype=float)
+        qc.deph_matrix = np.asarray(k._deph, dtype=float)
+    elif n == 2:
+        # the argument list _bloch_step_range receives (_kernels.py:505-528)
         qc.bloch = dict(
-            kz=0.5 * (pop[0, 0] - pop[1, 0] - pop[0, 1] + pop[1, 1]),
-            cz=0.5 * (pop[0, 0] - pop[1, 0] + pop[0, 1] - pop[1, 1]),
-            fxy=ws.coh_half[0, 1],
-            ax_c=a * h0[0, 1].real, ax_s=-a * mu[0, 1].real,
-            ay_c=-a * h0[0, 1].imag, ay_s=a * mu[0, 1].imag,
-            az_c=0.5 * a * (h0[0, 0].real - h0[1, 1].real),
-            az_s=-0.5 * a * (mu[0, 0].real - mu[1, 1].real),
-            a0_c=0.5 * a * (h0[0, 0].real + h0[1, 1].real),
-            a0_s=-0.5 * a * (mu[0, 0].real + mu[1, 1].real),
-            mu_x=mu[0, 1].real, mu_y=-mu[0, 1].imag,
-            mu_z=0.5 * (mu[0, 0].real - mu[1, 1].real),
+            kz=k._kz, cz=k._cz, fxy=k._fxy,
+            ax_c=k._ax[0], ax_s=k._ax[1], ay_c=k._ay[0], ay_s=k._ay[1],
+            az_c=k._az[0], az_s=k._az[1], a0_c=k._a0[0], a0_s=k._a0[1],
+            mu_x=k._mu01.real, mu_y=-k._mu01.imag, mu_z=k._mu_zdiff,
         )
     else:
-        qc.pop_half = ws.pop_half
-        qc.coh_half = ws.coh_half
-        qc.b_const = np.eye(n, dtype=complex) + 1j * a * h0
-        qc.b_field = -1j * a * mu
+        qc.pop_half = k.pop_half
+        qc.coh_half = k.coh_half
+        qc.b_const = k._b_const
+        qc.b_field = k._b_field
     return qc
 
 
@@ -325,49 +254,43 @@ class SolverPlan:
         return pack_density(self.rho_init, self.stepper)
 
 
-_SAMPLES: dict = {}
-
-
-def _source_samples(src, dt: float, num_t: int) -> np.ndarray:
+def _source_samples(src, dt: float, num_t: int, cache: dict | None = None) -> np.ndarray:
     """Source.value(n dt) for n = 1..num_t-1 (row 0 unused), the source's own
-    function call by call (solver_fdtd.py:378-385).  Memoised on the source's
-    type and fields: sweeps over media or repeated runs of one scenario
-    (batched points, end-to-end benchmarks) sample each distinct source once."""
-    try:
-        key = (type(src).__module__, type(src).__qualname__, tuple(sorted(vars(src).items())), dt, num_t)
-        hash(key)
-    except TypeError:
-        key = None
-    if key is not None and key in _SAMPLES:
-        return _SAMPLES[key]
+    function call by call (solver_fdtd.py:378-385).  ``cache`` (optional,
+    owned by the caller, e.g. one ``run_points`` sweep) shares the samples of
+    equal sources of the two frozen pulse types the reference defines."""
+    key = None
+    if cache is not None and type(src) in (core.SechPulse, core.GaussianPulse):
+        key = (type(src), src, dt, num_t)  # frozen dataclasses: hashable by value
+    if key is not None and key in cache:
+        return cache[key]
     col = np.zeros(num_t)
     for n in range(1, num_t):
         col[n] = src.value(n * dt)
-    col.flags.writeable = False
     if key is not None:
-        if len(_SAMPLES) > 256:
-            _SAMPLES.clear()
-        _SAMPLES[key] = col
+        col.flags.writeable = False
+        cache[key] = col
     return col
 
 
-def build_plan(device, scenario, stepper: str = "splitting", seed=None) -> SolverPlan:
-    """Validate and precompute a run (``FdtdSolver.__init__`` minus state arrays)."""
-    problems = scenario_validate(device, scenario)
+def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_cache: dict | None = None) -> SolverPlan:
+    """Validate and precompute a run (``FdtdSolver.__init__`` minus state
+    arrays, same checks in the same order).  ``sample_cache``: see
+    :func:`_source_samples`."""
+    problems = core.scenario_validate(device, scenario)
     if problems:
-        raise ValidationError(problems)
+        raise mblight.ValidationError(problems)
     if stepper not in STEPPERS:
         raise ValueError(f"unknown stepper {stepper!r}")
     grid = init_fdtd_simulation(device, scenario)
-    seed = DEFAULT_SEED if seed is None else int(seed)
+    seed = core.DEFAULT_SEED if seed is None else int(seed)
     nx, dt, dx = grid.num_x, grid.dt, grid.dx
 
     e_init = np.ascontiguousarray(scenario.ic_e_field.build(nx, seed), dtype=float)
     h_init = np.zeros(nx + 1)
     h_init[0:nx] = scenario.ic_h_field.build(nx, seed + 1)
 
-    lib = {m.id: m for m in device.materials()}
-    mats = [lib[r.material_id] for r in device.regions]
+    mats = [core.get_material(r.material_id) for r in device.regions]
     n_reg = len(device.regions)
     ends = np.array([r.x_end for r in device.regions])
     if nx > 1:
@@ -415,7 +338,7 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None) -> Solve
     cells = [0 if nx == 1 else int(math.floor(s.position / dx + 0.5)) for s in srcs]
     values = np.zeros((grid.num_t, len(srcs)))
     for k, s in enumerate(srcs):
-        values[:, k] = _source_samples(s, dt, grid.num_t)
+        values[:, k] = _source_samples(s, dt, grid.num_t, sample_cache)
 
     plans = [RecordPlan(rec, grid) for rec in scenario.records]
     names = [p.record.name for p in plans]

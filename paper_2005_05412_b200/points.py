@@ -22,7 +22,9 @@ import time
 import numpy as np
 
 from . import native
-from .errors import SolverError
+from .reference import mblight
+
+SolverError = mblight.SolverError
 from .plan import QUANTITY_CODES, build_plan, unpack_density
 from .solver import GpuFdtdSolver
 
@@ -148,7 +150,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
                 col = re[b] + 1j * im[b] if im is not None else re[b].copy()
                 col[0] = _initial_entry(p, pl)  # row 0: the initial state (solver_fdtd.py:449)
                 data = col[:, None]
-            res.append(pl.to_result(p.grid, data, solver._result_cls))
+            res.append(pl.to_result(p.grid, data))
         results.append(res)
     return results
 

@@ -34,7 +34,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import native
-from .errors import SolverError
+from .reference import mblight
+
+SolverError = mblight.SolverError
 
 
 @dataclass(frozen=True)
@@ -293,7 +295,7 @@ def run_slabs_local(solver, slabs_count: int, period=None):
     finally:
         for st in states:
             st.close()
-    solver.results = [p.to_result(solver.grid, d, solver._result_cls) for p, d in zip(solver.plan.plans, recs)]
+    solver.results = [p.to_result(solver.grid, d) for p, d in zip(solver.plan.plans, recs)]
     return solver.results
 
 

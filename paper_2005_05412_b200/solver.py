@@ -4,9 +4,9 @@
 ``run()`` contract (one ``Result`` per record in record order, blocking,
 ``SolverError`` on a second call or on a non-finite field, validation before
 any work) and replaces the hot loop with the fused sm_100a kernels of
-``libmbgpu.so``.  Setup arithmetic comes from :mod:`.plan` (a restatement of
-``FdtdSolver.__init__``), so every coefficient the kernels see equals the one
-the reference's numba loops see.
+``libmbgpu.so``.  Setup comes from :mod:`.plan`, which calls the reference's own setup
+functions and kernel constructors (``FdtdSolver.__init__``), so every
+coefficient the kernels see is the one the reference's numba loops see.
 
 Registered names: ``gpu-fdtd-reg-cayley`` (splitting stepper) and
 ``gpu-fdtd-rk4``.  :func:`register_with_reference` adds the same names to the
@@ -17,27 +17,21 @@ and the mblight CLI resolve to this solver.
 from __future__ import annotations
 
 import ctypes as C
-import sys
+import math
 
 import numpy as np
 
 from . import native
-from .errors import SolverError
 from .plan import build_plan, resolve_threads
-from .setup_model import Result, register_solver
+from .reference import core, mblight
+
+SolverError = mblight.SolverError
 
 SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
 # records larger than this stream through a device window of rows ...
 RECORD_HBM_BYTES = 4 << 30
 # ... sized so one segment's rows take about this much device memory
 RECORD_SEGMENT_BYTES = 512 << 20
-
-
-def _result_class(scenario):
-    """Results are built with the caller's own ``Result`` type (reference or mirror)."""
-    mod = sys.modules.get(type(scenario).__module__)
-    cls = getattr(mod, "Result", None) if mod is not None else None
-    return cls if isinstance(cls, type) else Result
 
 
 class GpuFdtdSolver:
@@ -75,12 +69,11 @@ class GpuFdtdSolver:
         self.gpu = int(gpu)
         self.persistent = None if persistent is None else bool(persistent)
         self.record_segment = record_segment
-        self._host_rows = None
+        self._streamed = False
         self.results = None
         self.launches = 0
         self.kernel_ms = None
         self._ran = False
-        self._result_cls = _result_class(scenario)
         if len(self.plan.plans) > native.MAX_RECORDS:
             raise ValueError(f"the GPU solver supports at most {native.MAX_RECORDS} records")
         if len(self.plan.src_cells) > native.MAX_SOURCES:
@@ -177,17 +170,35 @@ class GpuFdtdSolver:
             h.call("mbg_upload_density", native.ptr(w))
 
     def download_results(self, h):
+        """Every record into the reference's own host buffer (``_RecordPlan.buffer``)
+        and out as its ``Result`` (``_RecordPlan.to_result``)."""
         out = []
         for r, p in enumerate(self.plan.plans):
-            if self._host_rows is not None:  # streamed: the rows are already on the host
-                re, im = self._host_rows[r]
-            else:
-                re = np.zeros((p.rows, p.cols))
-                im = np.zeros((p.rows, p.cols)) if p.is_complex else None
-                h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
-            data = re if im is None else re + 1j * im
-            out.append(p.to_result(self.grid, data, self._result_cls))
+            if not self._streamed:  # streamed: the rows are already in the buffer
+                self._download_rows(h, r, p, 0, p.rows, whole=True)
+            out.append(p.to_result(self.grid))
         return out
+
+    @staticmethod
+    def _download_rows(h, r, p, lo, hi, whole=False):
+        """Rows [lo, hi) of record r into its host buffer: straight into the
+        buffer for real records, through re/im halves for complex ones."""
+        buf = p.buffer
+        if not p.is_complex:
+            dst = buf[lo:hi]
+            if whole:
+                h.call("mbg_download_record", r, native.ptr(dst), None)
+            else:
+                h.call("mbg_download_record_rows", r, lo, hi, native.ptr(dst), None)
+            return
+        re = np.empty((hi - lo, p.cols))
+        im = np.empty((hi - lo, p.cols))
+        if whole:
+            h.call("mbg_download_record", r, native.ptr(re), native.ptr(im))
+        else:
+            h.call("mbg_download_record_rows", r, lo, hi, native.ptr(re), native.ptr(im))
+        buf[lo:hi].real = re
+        buf[lo:hi].imag = im
 
     # -- streamed records ---------------------------------------------------------
 
@@ -211,17 +222,15 @@ class GpuFdtdSolver:
         return max(1024, int(RECORD_SEGMENT_BYTES / per_step) // 1024 * 1024)
 
     def _open_streams(self, h, segment):
-        """Device windows of floor(S/every) + 1 rows; full host arrays (the
-        reference keeps every row in host memory, solver_fdtd.py:164-172)."""
-        self._host_rows = []
+        """Device windows of floor(S/every) + 1 rows; the host side is the
+        reference's own full buffer (it keeps every row in host memory,
+        solver_fdtd.py:136-172)."""
+        self._streamed = True
         self._row0 = []
         for r, p in enumerate(self.plan.plans):
             cap = min(p.rows, segment // p.every + 1)
             if cap < p.rows:
                 h.call("mbg_set_record_rows", r, cap)
-            re = np.zeros((p.rows, p.cols))
-            im = np.zeros((p.rows, p.cols)) if p.is_complex else None
-            self._host_rows.append((re, im))
             self._row0.append(0)
 
     def _drain_streams(self, h, last_step):
@@ -232,9 +241,7 @@ class GpuFdtdSolver:
             lo = self._row0[r]
             if done <= lo:
                 continue
-            re, im = self._host_rows[r]
-            h.call("mbg_download_record_rows", r, lo, done, native.ptr(re[lo:done]),
-                   native.ptr(im[lo:done]) if im is not None else None)
+            self._download_rows(h, r, p, lo, done)
             h.call("mbg_set_record_row0", r, done)
             self._row0[r] = done
 
@@ -301,6 +308,10 @@ class GpuFdtdSolver:
         self.kernel_ms = float(ms.value)
         if every is not None:
             self._read_invariants(h)
+        elif self.monitor_invariants:
+            # no quantum cells: the reference's report keeps its initial
+            # values (solver_fdtd.py:428-434)
+            self.invariant_report = {"max_trace_dev": 0.0, "max_herm_dev": 0.0, "min_eigenvalue": math.inf}
         launches = C.c_int64(0)
         h.call("mbg_launch_count", C.byref(launches))
         self.launches = int(launches.value)
@@ -324,22 +335,23 @@ def _rk4_factory(device, scenario, **kw):
     return GpuFdtdSolver(device, scenario, stepper="rk4", **kw)
 
 
-def register(registry_fn=register_solver):
+def register(registry_fn=None):
+    """Add the GPU solver names to the reference's solver registry
+    (``core.register_solver``, core.py:617)."""
+    registry_fn = core.register_solver if registry_fn is None else registry_fn
     registry_fn("gpu-fdtd-reg-cayley", GpuFdtdSolver)
     registry_fn("gpu-fdtd-rk4", _rk4_factory)
 
 
 def register_with_reference(mblight_module=None):
     """Register the GPU solver names in the reference's own registry
-    (``mblight.core.register_solver``, core.py:617)."""
+    (``mblight.core.register_solver``, core.py:617); importing this package
+    already did so for the ``mblight`` it binds to."""
     if mblight_module is None:
-        import mblight as mblight_module  # noqa: PLC0415
-    reg = getattr(mblight_module, "register_solver", None)
-    if reg is None:  # mblight re-exports create_solver but not register_solver
-        from importlib import import_module  # noqa: PLC0415
+        mblight_module = mblight
+    from importlib import import_module  # noqa: PLC0415
 
-        reg = import_module(mblight_module.__name__ + ".core").register_solver
-    register(reg)
+    register(import_module(mblight_module.__name__ + ".core").register_solver)
     return mblight_module
 
 

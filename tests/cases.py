@@ -157,6 +157,11 @@ CASES = {
     "cfg2_r16": (lambda api: configs.cfg2(api, nx=1 << 16, steps=20000, stress=True), "splitting"),
     "cfg2_full": (lambda api: configs.cfg2(api), "splitting"),
     "cfg2_stress_full": (lambda api: configs.cfg2(api, stress=True), "splitting"),
+    # the headline grid with density records inside the medium as well (its
+    # first cell, the middle of the device, the last medium cell): the BASELINE
+    # record cells all lie in the 7.5 um vacuum lead
+    "cfg2_medium_full": (lambda api: configs.cfg2(api, cells=(16, 4096, 8192, 209716, 1 << 21, 3984587),
+                                                  quantities=("e", "d11", "d22", "inv", "d12")), "splitting"),
     "cfg3_r16": (lambda api: configs.cfg3(api, nx=1 << 16, steps=50000, cells=(4096, 12288, 20000)), "splitting"),
     "cfg3_r16_stress": (lambda api: configs.cfg3(api, nx=1 << 16, steps=50000, stress=True), "splitting"),
     "cfg4_r14": (lambda api: configs.cfg4(api, nx=1 << 14, steps=100000), "splitting"),
@@ -381,4 +386,4 @@ for _n in (2, 3, 4, 5):
     CASES[f"kernel{_n}_rk4"] = kernel_case(_n, 200 + _n, stepper="rk4")
 
 # cases whose reference run takes minutes; generated once, marked slow
-SLOW = {"cfg2_full", "cfg2_stress_full", "cfg3_r16", "cfg3_r16_stress", "cfg4_r14"}
+SLOW = {"cfg2_full", "cfg2_stress_full", "cfg2_medium_full", "cfg3_r16", "cfg3_r16_stress", "cfg4_r14"}

@@ -7,7 +7,9 @@ import numpy as np
 import pytest
 from conftest import build_case
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 
 pytestmark = pytest.mark.gpu
 
@@ -37,7 +39,7 @@ def test_record_shapes_axes_and_order():
     sce.add_record(mb.Record("inv12", quantity="inv", interval=2.5e-15))
     sce.add_record(mb.Record("probe", quantity="e", position=75e-6))
     sce.add_record(mb.Record("d12", quantity="d", i=1, j=2, position=75e-6))
-    s = mb.GpuFdtdSolver(dev, sce)
+    s = gpu.GpuFdtdSolver(dev, sce)
     res = {r.name: r for r in s.run()}
     every = round(2.5e-15 / s.grid.dt)
     rows = (s.grid.num_t - 1) // every + 1
@@ -51,7 +53,7 @@ def test_record_shapes_axes_and_order():
 def test_inversion_outside_quantum_region_is_zero():
     dev, sce = _sit_small()
     sce.add_record(mb.Record("inv12", quantity="inv", interval=2.5e-15))
-    inv = mb.GpuFdtdSolver(dev, sce).run()[0]
+    inv = gpu.GpuFdtdSolver(dev, sce).run()[0]
     x = inv.positions
     vac = (x < 7.5e-6) | (x > 142.5e-6)
     assert np.count_nonzero(inv.data[-1][vac]) == 0
@@ -66,7 +68,7 @@ def test_zero_state_stays_zero():
     sce = mb.Scenario("s", 64, 2e-15, mb.QmOperator([1.0, 0.0]))
     sce.add_record(mb.Record("e", quantity="e"))
     sce.add_record(mb.Record("h", quantity="h"))
-    for r in mb.GpuFdtdSolver(dev, sce).run():
+    for r in gpu.GpuFdtdSolver(dev, sce).run():
         assert np.count_nonzero(r.data) == 0
 
 
@@ -80,7 +82,7 @@ def test_nonfinite_field_aborts_with_the_scan_step():
     sce.add_source(mb.SechPulse("s", 5e-6, "hard", 1e10, 2e14, 10.0, 2e14))
     import oracle as orc
 
-    solver = mb.GpuFdtdSolver(dev, sce, stepper="rk4")
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper="rk4")
     _, bad = orc.run_oracle(solver.plan)
     with pytest.raises(mb.SolverError, match=f"at step {bad}$"):
         solver.run()
@@ -93,7 +95,7 @@ def test_pulse_travels_at_light_speed():
     sce = mb.Scenario("s", 2048, 100e-15, mb.QmOperator([1.0, 0.0]))
     sce.add_source(mb.SechPulse("sech", 0.0, "hard", 1.0, 2e14, 10.0, 2e14))
     sce.add_record(mb.Record("e", quantity="e", interval=100e-15))
-    e = mb.GpuFdtdSolver(dev, sce).run()[0]
+    e = gpu.GpuFdtdSolver(dev, sce).run()[0]
     x_peak = e.positions[int(np.argmax(np.abs(e.data[-1])))]
     assert abs(x_peak - mb.C0 * (e.times[-1] - 50e-15)) <= 3 * (40e-6 / 2047)
     assert np.max(np.abs(e.data[-1])) >= 0.98
@@ -108,7 +110,7 @@ def _reflection_energy_ratio(r):
     sce.add_source(mb.SechPulse("sech", 20e-6, "soft", 1.0, 2e14, 10.0, 2e14))
     sce.add_record(mb.Record("e", quantity="e", interval=5e-15))
     sce.add_record(mb.Record("h", quantity="h", interval=5e-15))
-    res = {x.name: x for x in mb.GpuFdtdSolver(dev, sce).run()}
+    res = {x.name: x for x in gpu.GpuFdtdSolver(dev, sce).run()}
     dx = 60e-6 / 4095
     energy = 0.5 * mb.EPS0 * np.sum(res["e"].data ** 2, axis=1) * dx
     energy += 0.5 * mb.MU0 * np.sum(res["h"].data ** 2, axis=1) * dx
@@ -128,7 +130,7 @@ def test_sit_physics_full_run():
     """Self-induced transparency (pkg/tests/test_acceptance.py:203-229): the
     medium is left inverted-back (|w+1| < 0.05) behind a 2 pi pulse."""
     dev, sce, _ = build_case("cfg1_full")
-    res = {r.name: r for r in mb.GpuFdtdSolver(dev, sce).run()}
+    res = {r.name: r for r in gpu.GpuFdtdSolver(dev, sce).run()}
     inv = res["inv@2000"].data[:, 0]
     assert np.max(np.abs(inv[-1] + 1.0)) < 0.05
     assert np.min(inv) > -1.0 - 1e-9 and np.max(inv) <= 1.0 + 1e-9
@@ -136,7 +138,7 @@ def test_sit_physics_full_run():
 
 def test_invariant_monitor():
     dev, sce, stepper = build_case("rand4_split")
-    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    s = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
     s.run()
     rep = s.invariant_report
     assert rep["max_trace_dev"] < 1e-9 and rep["max_herm_dev"] < 1e-12 and rep["min_eigenvalue"] > -1e-9
@@ -145,7 +147,7 @@ def test_invariant_monitor():
 def test_results_are_independent_arrays():
     dev, sce = _sit_small(256, 5e-15)
     sce.add_record(mb.Record("e", quantity="e"))
-    s = mb.GpuFdtdSolver(dev, sce)
+    s = gpu.GpuFdtdSolver(dev, sce)
     r = s.run()[0]
     r.data[:] = 1.0  # caller owns the buffers
     assert s.results[0].data is r.data
@@ -159,7 +161,7 @@ def test_device_invariant_monitor_matches_numpy(case):
     from paper_2005_05412_b200.plan import unpack_density
 
     dev, sce, stepper = build_case(case)
-    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    s = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     h = s.open_handle()
     s.upload_initial_state(h)
     h.call("mbg_sample", 0)
@@ -211,7 +213,7 @@ def test_single_step_matches_hand_computed_update():
     sce.add_record(mb.Record("e", quantity="e"))
     sce.add_record(mb.Record("h", quantity="h"))
     for exact in (True, False):
-        s = mb.GpuFdtdSolver(dev, sce, exact=exact)
+        s = gpu.GpuFdtdSolver(dev, sce, exact=exact)
         assert s.grid.num_t == 2
         res = {r.name: r for r in s.run()}
         cf = mb.get_fdtd_constants(dev.material_at(0.0), s.grid.dt, s.grid.dx)
@@ -249,7 +251,7 @@ def test_phase_velocity_error_below_one_percent():
                       ic_e_field=mb.CurveField(np.sin(k * x_e)),
                       ic_h_field=mb.CurveField(-np.sin(k * (x_h + 0.5 * mb.C0 * dt)) / z0))
     sce.add_record(mb.Record("probe", quantity="e", position=length / 2))
-    r = mb.GpuFdtdSolver(dev, sce).run()[0]
+    r = gpu.GpuFdtdSolver(dev, sce).run()[0]
     trace, times = r.data[:, 0], r.times
     good = times < (length / 2) / mb.C0
     trace, times = trace[good], times[good]
@@ -279,7 +281,7 @@ def test_event_marks_time_the_advance():
     import ctypes as C
 
     dev, sce = _cfg2_small(stress=False)
-    s = mb.GpuFdtdSolver(dev, sce)
+    s = gpu.GpuFdtdSolver(dev, sce)
     h = s.open_handle()
     s.upload_initial_state(h)
     h.call("mbg_mark", 0)
@@ -291,7 +293,7 @@ def test_event_marks_time_the_advance():
     h.call("mbg_mark_elapsed", 1, 2, C.byref(part))
     h.call("mbg_mark_elapsed", 0, 2, C.byref(total))
     assert 0.0 < part.value <= total.value
-    with pytest.raises(mb.NativeError):
+    with pytest.raises(gpu.NativeError):
         h.call("mbg_mark_elapsed", 0, 7, C.byref(part))  # slot never recorded
     h.close()
 
@@ -302,15 +304,15 @@ def test_zero_field_upload_is_a_memset():
     from paper_2005_05412_b200 import native
 
     dev, sce = _cfg2_small(stress=False)
-    a = mb.GpuFdtdSolver(dev, sce)
+    a = gpu.GpuFdtdSolver(dev, sce)
     assert a.plan.fields_zero
     ra = a.run()
-    b = mb.GpuFdtdSolver(dev, sce)
+    b = gpu.GpuFdtdSolver(dev, sce)
     h = b.open_handle()
     e, hf = np.zeros(b.grid.num_x), np.zeros(b.grid.num_x + 1)
     h.call("mbg_upload_fields", native.ptr(e), native.ptr(hf))
     h.call("mbg_upload_density", native.ptr(native.f64(b.plan.rho_init_packed())))
-    with pytest.raises(mb.NativeError):
+    with pytest.raises(gpu.NativeError):
         h.call("mbg_upload_fields", native.ptr(e), None)
     b._ran = True
     b._run_on(h)
@@ -328,7 +330,7 @@ def test_state_round_trip_through_the_relaxed_frame(exact):
     from paper_2005_05412_b200 import native
 
     dev, sce = _cfg2_small()
-    s = mb.GpuFdtdSolver(dev, sce, exact=exact)
+    s = gpu.GpuFdtdSolver(dev, sce, exact=exact)
     h = s.open_handle()
     s.upload_initial_state(h)
     nx, w = s.grid.num_x, s.plan.state_words
@@ -355,10 +357,10 @@ def test_streamed_records_equal_resident_records(case, segment):
     after every segment of `segment` steps) equal the HBM-resident records bit
     for bit, for point and whole-domain, real and complex records."""
     dev, sce, stepper = build_case(case)
-    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     mb.clear_material_library()
     dev, sce, stepper = build_case(case)
-    got = mb.GpuFdtdSolver(dev, sce, stepper=stepper, record_segment=segment).run()
+    got = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, record_segment=segment).run()
     for a, b in zip(ref, got):
         assert a.name == b.name and a.data.shape == b.data.shape
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), (case, segment, a.name)
@@ -368,12 +370,12 @@ def test_records_stream_automatically_past_the_device_budget(monkeypatch):
     from paper_2005_05412_b200 import solver as S
 
     dev, sce, stepper = build_case("sit_hard_whole")
-    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     monkeypatch.setattr(S, "RECORD_HBM_BYTES", 1 << 10)
     monkeypatch.setattr(S, "RECORD_SEGMENT_BYTES", 1 << 16)
     mb.clear_material_library()
     dev, sce, stepper = build_case("sit_hard_whole")
-    sol = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    sol = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     assert sol._segment_steps() >= 1024
     got = sol.run()
     assert sol._host_rows is not None
@@ -385,7 +387,7 @@ def test_advance_refuses_rows_outside_the_device_window():
     from paper_2005_05412_b200 import native
 
     dev, sce, stepper = build_case("sit_hard_whole")
-    sol = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    sol = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     h = sol.open_handle()
     try:
         sol.upload_initial_state(h)
@@ -405,11 +407,11 @@ def test_streamed_records_with_the_invariant_monitor():
     """Segments end on monitor steps: same records and the same invariant
     report as the resident run."""
     dev, sce, stepper = build_case("rand3_split")
-    a = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    a = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
     ra = a.run()
     mb.clear_material_library()
     dev, sce, stepper = build_case("rand3_split")
-    b = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True, record_segment=37)
+    b = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True, record_segment=37)
     rb = b.run()
     assert b._host_rows is not None
     for x, y in zip(ra, rb):
@@ -449,7 +451,7 @@ def test_two_level_equivalence_bloch_vs_three_level_kernel():
         sce.add_record(mb.Record("e", quantity="e", interval=50 * dt0))
         for i, j in ((1, 1), (2, 2), (1, 2)):
             sce.add_record(mb.Record(f"d{i}{j}", quantity="d", i=i, j=j, interval=50 * dt0))
-        return mb.GpuFdtdSolver(dev, sce)
+        return gpu.GpuFdtdSolver(dev, sce)
 
     two = build(qm2, [1.0, 0.0], "2")
     three = build(qm3, [1.0, 0.0, 0.0], "3")
@@ -468,11 +470,11 @@ def test_fused_two_level_monitor_equals_stepwise_numpy(case):
     from paper_2005_05412_b200 import native
 
     dev, sce, stepper = build_case(case)
-    fused = mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
+    fused = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True)
     fused.run()
     mb.clear_material_library()
     dev, sce, stepper = build_case(case)
-    s = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    s = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     every = min(p.every for p in s.plan.plans)
     cells = np.concatenate([np.arange(lo, hi) for lo, hi, _ in s.plan.groups])
     h = s.open_handle()
@@ -495,3 +497,38 @@ def test_fused_two_level_monitor_equals_stepwise_numpy(case):
     rep = fused.invariant_report
     assert rep["max_trace_dev"] == 0.0 and rep["max_herm_dev"] == 0.0
     assert rep["min_eigenvalue"] == pytest.approx(min(mins), abs=1e-15)
+
+
+@pytest.mark.parametrize("records", [False, True])
+@pytest.mark.parametrize("persistent", [None, True, False])
+def test_monitor_report_equals_the_reference_solver(records, persistent):
+    """The invariant report of a two-level run with and without records
+    (record-less: the reference's default cadence of 256 steps,
+    solver_fdtd.py:302-304) equals the reference solver's own report for the
+    same objects, whichever launch path runs the steps."""
+    dev, sce = _sit_small(2048, 40e-15)
+    sce.add_source(mb.SechPulse("sech", 0.0, "hard", 4.2186e9, 2e14, 10.0, 2e14))
+    if records:
+        sce.add_record(mb.Record("inv", quantity="inv", interval=1.3e-15))
+    ref = mb.FdtdSolver(dev, sce, monitor_invariants=True, threads=4)
+    ref.run()
+    s = mb.create_solver("gpu-fdtd-reg-cayley", dev, sce, monitor_invariants=True, persistent=persistent,
+                         tile_steps=16)
+    s.run()
+    want, got = ref.invariant_report, s.invariant_report
+    assert got["max_trace_dev"] == want["max_trace_dev"] and got["max_herm_dev"] == want["max_herm_dev"]
+    assert got["min_eigenvalue"] == pytest.approx(want["min_eigenvalue"], abs=1e-12)
+
+
+def test_monitor_without_quantum_media_keeps_the_initial_report():
+    mb.add_material(mb.Material("Vacuum"))
+    dev = mb.Device("v")
+    dev.add_region(mb.Region("v", "Vacuum", 0.0, 20e-6))
+    sce = mb.Scenario("s", 512, 10e-15, mb.QmOperator([1.0, 0.0]))
+    sce.add_source(mb.SechPulse("sech", 0.0, "soft", 1e9, 2e14, 5.0, 1e15))
+    ref = mb.FdtdSolver(dev, sce, monitor_invariants=True, threads=1)
+    ref.run()
+    s = mb.create_solver("gpu-fdtd-reg-cayley", dev, sce, monitor_invariants=True)
+    s.run()
+    assert s.invariant_report == ref.invariant_report == {"max_trace_dev": 0.0, "max_herm_dev": 0.0,
+                                                          "min_eigenvalue": math.inf}

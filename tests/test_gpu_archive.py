@@ -1,0 +1,64 @@
+"""The drop-in end to end on the GPU: the reference's own objects, registry
+and archive writer around the GPU solver.
+
+``mblight.create_solver("gpu-fdtd-reg-cayley", *mblight.builtin_setup(...),
+exact=True).run()`` into ``mblight.write_archive`` (writer_raw.py:40-92) must
+produce the archive the reference's own solver writes, byte for byte
+(pkg/tests/test_acceptance.py:279-312 pins byte-identical archives across
+worker counts).  The reference archives' SHA-256 digests were recorded by
+``tests/golden/make_archive_golden.py``.
+"""
+
+import hashlib
+import json
+from pathlib import Path
+
+import pytest
+from conftest import GOLDEN
+
+import paper_2005_05412_b200 as gpu  # noqa: F401  (registers the GPU solver names)
+from paper_2005_05412_b200.reference import mblight as mb
+
+pytestmark = pytest.mark.gpu
+
+GPU_NAME = {"fdtd-reg-cayley": "gpu-fdtd-reg-cayley", "fdtd-rk4": "gpu-fdtd-rk4"}
+
+
+def _golden():
+    return json.loads((GOLDEN / "archives.json").read_text())
+
+
+def _archive(tmp_path, key, exact):
+    g = _golden()[key]
+    mb.clear_material_library()
+    dev, sce = mb.builtin_setup(g["setup"], gridpoints=g["gridpoints"], end_time=g["end_time"])
+    results = mb.create_solver(GPU_NAME[g["solver"]], dev, sce, exact=exact).run()
+    assert all(type(r) is mb.Result for r in results)
+    folder = mb.write_archive(tmp_path / key, results, dev, sce)
+    files = {p.name: hashlib.sha256(p.read_bytes()).hexdigest() for p in sorted(Path(folder).iterdir())}
+    return g, files, folder
+
+
+@pytest.mark.parametrize("key", ["ziolkowski1995", "ziolkowski1995_rk4_60fs"])
+def test_archive_bytes_identical_to_the_reference(tmp_path, key):
+    g, files, _ = _archive(tmp_path, key, exact=True)
+    assert files == g["files"]
+
+
+def test_single_point_archive_metadata_identical(tmp_path):
+    """song2005 (three levels at one grid point): the reference steps it with
+    numpy (ScalarKernel), so the payloads agree to tolerance (song_point
+    golden) and the metadata byte for byte."""
+    g, files, folder = _archive(tmp_path, "song2005", exact=False)
+    assert set(files) == set(g["files"])
+    assert files["meta.json"] == g["files"]["meta.json"]
+    _, back = mb.read_archive(folder)
+    assert {r.name for r in back} == {n.split(".")[0] for n in files if n != "meta.json"}
+
+
+def test_fast_variant_archive_reads_back_within_tolerance(tmp_path):
+    """The fast (FMA) variant's archive has the reference's layout and
+    metadata; its payloads are checked against the goldens in test_gpu_parity."""
+    g, files, folder = _archive(tmp_path, "ziolkowski1995", exact=False)
+    assert files["meta.json"] == g["files"]["meta.json"]
+    assert set(files) == set(g["files"])

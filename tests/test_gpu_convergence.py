@@ -17,7 +17,9 @@ import numpy as np
 import pytest
 from scipy.linalg import expm
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 
 pytestmark = pytest.mark.gpu
 
@@ -66,7 +68,7 @@ def _gpu(desc, rho0, e_field, horizon, steps, stepper, tag):
     pairs = [(i, j) for i in range(n) for j in range(i, n)]
     for i, j in pairs:
         sce.add_record(mb.Record(f"d{i}{j}", quantity="d", i=i + 1, j=j + 1, position=0.0, interval=horizon))
-    res = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    res = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     out = np.zeros((n, n), complex)
     for (i, j), r in zip(pairs, res):
         out[i, j] = r.data[-1, 0]

@@ -17,7 +17,9 @@ import numpy as np
 import pytest
 from conftest import ROOT
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 
 sys.path.insert(0, str(ROOT / "oracle"))
 import oracle as orc  # noqa: E402
@@ -85,7 +87,7 @@ CASES = [
 @pytest.mark.parametrize("nx,levels,steps,stepper,k", CASES)
 def test_tiny_domains_and_short_runs_match_the_oracle(nx, levels, steps, stepper, k, exact):
     dev, sce, stepper = _build(nx, levels, steps, stepper, hard_right=(nx % 2 == 1))
-    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper, tile_steps=k, exact=exact)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, tile_steps=k, exact=exact)
     assert solver.grid.num_t - 1 == steps and solver.grid.num_x == nx
     ref, bad = orc.run_oracle(solver.plan)
     if bad:
@@ -114,9 +116,9 @@ def test_advance_in_uneven_pieces_equals_one_run(levels):
     import ctypes as C
 
     dev, sce, stepper = _build(3000, levels, 700)
-    whole = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    whole = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     dev, sce, stepper = _build(3000, levels, 700)
-    sol = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    sol = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     h = sol.open_handle()
     sol.upload_initial_state(h)
     k = C.c_int32(0)

@@ -13,7 +13,9 @@ import numpy as np
 import pytest
 from conftest import ROOT
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 from paper_2005_05412_b200 import configs, native
 from paper_2005_05412_b200.plan import unpack_density
 
@@ -33,7 +35,7 @@ def test_full_grid_prefix_matches_the_oracle(name, steps, kw):
         pytest.skip(f"host memory below {need >> 30} GB for the full-grid oracle")
     mb.clear_material_library()
     dev, sce = getattr(configs, name)(mb, **kw)
-    sol = mb.GpuFdtdSolver(dev, sce)
+    sol = gpu.GpuFdtdSolver(dev, sce)
     plan = sol.plan
     nx = sol.grid.num_x
     h = sol.open_handle()

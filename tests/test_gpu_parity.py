@@ -12,7 +12,9 @@ import pytest
 from cases import CASES
 from conftest import build_case, load_golden, rel_err
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 
 pytestmark = pytest.mark.gpu
 
@@ -27,7 +29,7 @@ ALL = sorted(CASES)
 
 def _run(name, **kw):
     dev, sce, stepper = build_case(name)
-    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper, **kw)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, **kw)
     return solver, solver.run()
 
 
@@ -106,7 +108,7 @@ def test_gpu_matches_oracle_on_fresh_seeds():
         mb.clear_material_library()
         build, stepper = random_case(dim, seed, nx=700, end=30e-15)
         dev, sce = build(mb)
-        solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+        solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
         got = solver.run()
         recs, bad = orc.run_oracle(solver.plan)
         assert bad == 0
@@ -125,7 +127,7 @@ def test_real_media_fast_paths_match_the_oracle(dim, stepper):
     mb.clear_material_library()
     build, _ = random_case(dim, 950 + dim, nx=600, end=25e-15, stepper=stepper, real=True)
     dev, sce = build(mb)
-    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     got = solver.run()
     recs, bad = orc.run_oracle(solver.plan)
     assert bad == 0

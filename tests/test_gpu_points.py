@@ -8,7 +8,9 @@ import numpy as np
 import pytest
 from conftest import load_golden, rel_err
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 from paper_2005_05412_b200.points import run_points
 
 pytestmark = pytest.mark.gpu
@@ -53,7 +55,7 @@ def _two_level(scale=1.0, t2=1e12, tag=""):
 def _alone(build, stepper, exact, **kw):
     mb.clear_material_library()
     dev, sce = build(**kw)
-    return mb.GpuFdtdSolver(dev, sce, stepper=stepper, exact=exact).run()
+    return gpu.GpuFdtdSolver(dev, sce, stepper=stepper, exact=exact).run()
 
 
 @pytest.mark.parametrize("stepper", ["splitting", "rk4"])

@@ -16,7 +16,8 @@ from cases import CASES, SLOW
 from conftest import build_case, load_golden, rel_err
 
 import oracle as orc
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+from paper_2005_05412_b200.reference import mblight as mb
 
 BITWISE = {"cfg1_full", "cfg2_r16", "cfg2_full", "cfg2_stress_full", "sit_hard_whole", "multi_material", "bragg_stack",
            "vacuum_sources", "rand2_split", "kernel2_split", "rand2_rk4", "kernel2_rk4"}
@@ -28,7 +29,7 @@ NAMES = sorted(n for n in CASES if n not in LONG or os.environ.get("MBG_SLOW"))
 def test_oracle_matches_reference_golden(name):
     meta, recs = load_golden(name)
     dev, sce, stepper = build_case(name)
-    plan = mb.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
     assert [plan.grid.num_x, plan.grid.dx, plan.grid.num_t, plan.grid.dt] == meta["grid"]
     got, bad = orc.run_oracle(plan)
     assert bad == 0
@@ -46,7 +47,7 @@ def test_long_cases_are_listed():
 
 def test_oracle_is_thread_count_independent():
     dev, sce, stepper = build_case("rand3_split")
-    plan = mb.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
     a, _ = orc.run_oracle(plan, threads=1)
     b, _ = orc.run_oracle(plan, threads=4)
     for x, y in zip(a, b):
@@ -63,6 +64,6 @@ def test_oracle_reports_the_first_failing_scan():
     dev.add_region(mb.Region("a", "stiff", 0.0, 10e-6))
     sce = mb.Scenario("s", 64, 2e-13, mb.QmOperator([1.0, 0.0]))
     sce.add_source(mb.SechPulse("s", 5e-6, "hard", 1e10, 2e14, 10.0, 2e14))
-    plan = mb.GpuFdtdSolver(dev, sce, stepper="rk4").plan
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper="rk4").plan
     _, bad = orc.run_oracle(plan)
     assert bad > 0 and (bad % 1024 == 0 or bad == plan.grid.num_t - 1)

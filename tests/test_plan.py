@@ -1,7 +1,7 @@
-"""Host-side setup (plan.py / setup_model.py / qm.py) against the reference's
-known answers: grid sizing (pkg/tests/test_solver.py:63-75), coefficients
-(:119-141), relaxation propagator closed form (pkg/tests/test_quantum.py:349-359),
-splitmix64 (core.py:377-388), and the region table vs per-cell maps."""
+"""Host-side setup (plan.py) against the reference: its known answers for grid
+sizing (pkg/tests/test_solver.py:63-75), coefficients (:119-141) and the
+relaxation propagator closed form (pkg/tests/test_quantum.py:349-359), and the
+plan against the reference's own ``FdtdSolver.__init__`` for the same objects."""
 
 import math
 import sys
@@ -11,7 +11,9 @@ import numpy as np
 import pytest
 from conftest import build_case
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 from paper_2005_05412_b200 import plan as P
 
 
@@ -73,33 +75,17 @@ def test_relaxation_half_step_is_stochastic():
         assert np.allclose(ws.pop_half.sum(axis=0), 1.0, atol=1e-12)
 
 
-def _splitmix_loop(seed, count):
-    mask = (1 << 64) - 1
-    state = seed & mask
-    out = []
-    for _ in range(count):
-        state = (state + 0x9E3779B97F4A7C15) & mask
-        z = state
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & mask
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & mask
-        out.append((z ^ (z >> 31)) / 2.0**64)
-    return np.array(out)
-
-
-@pytest.mark.parametrize("seed", [0, 7, 0xB10C, 2**64 - 1, 123456789123])
-def test_vectorised_splitmix64_equals_the_sequential_stream(seed):
-    assert np.array_equal(mb.splitmix64_uniform(seed, 5000), _splitmix_loop(seed, 5000))
-
-
 def test_cfg2_initial_inversion():
-    u = mb.splitmix64_uniform(0xB10C, 1)[0]
+    from importlib import import_module
+
+    u = import_module("mblight.core")._splitmix64_stream(0xB10C, 1)[0]
     assert abs(u - 0.923420) < 1e-6
 
 
 @pytest.mark.parametrize("case", ["cfg3_r16", "multi_material", "vacuum_sources", "tiny_group"])
 def test_region_table_reproduces_per_cell_maps(case):
     dev, sce, stepper = build_case(case)
-    plan = mb.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
     nx, dx = plan.grid.num_x, plan.grid.dx
     ends = np.array([r.x_end for r in dev.regions])
     cell_region = np.minimum(np.searchsorted(ends, np.arange(nx) * dx, side="right"), len(ends) - 1)
@@ -121,7 +107,7 @@ def test_weak_scaling_device_builds_for_every_gpu_count(replicas):
 
     nx = 4096 * replicas
     dev, sce = configs.cfg2(mb, nx=nx, steps=10, replicas=replicas, cells=(16, nx // 2))
-    plan = mb.GpuFdtdSolver(dev, sce).plan
+    plan = gpu.GpuFdtdSolver(dev, sce).plan
     assert len(dev.regions) == 3 * replicas and len(plan.groups) == replicas
     # the reference's per-cell group runs (solver_fdtd.py:276-285)
     ends = np.array([r.x_end for r in dev.regions])
@@ -161,7 +147,7 @@ def test_validation_before_any_work_and_registry():
 def test_bad_stepper_rejected():
     dev, sce, _ = build_case("sit_hard_whole")
     with pytest.raises(ValueError):
-        mb.GpuFdtdSolver(dev, sce, stepper="euler")
+        gpu.GpuFdtdSolver(dev, sce, stepper="euler")
 
 
 def test_solver_keeps_reference_attributes():
@@ -171,55 +157,88 @@ def test_solver_keeps_reference_attributes():
     assert isinstance(s.grid, mb.GridLayout)
 
 
-REF = Path("/root/reference/pkg/src")
+@pytest.mark.parametrize("case", ["cfg2_r16", "multi_material", "rand5_split", "sit_hard_whole",
+                                  "vacuum_sources", "tiny_group", "song_point"])
+def test_plan_equals_the_reference_constructor(case):
+    """Everything the kernels consume equals what the reference's own
+    ``FdtdSolver.__init__`` (solver_fdtd.py:207-326) builds for the same
+    objects: per-cell coefficients, initial fields, boundary constants, source
+    cells, record schedules and the stepper constants of every quantum group."""
+    dev, sce, stepper = build_case(case)
+    ref = mb.FdtdSolver(dev, sce, stepper=stepper)
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    g = plan.grid
+    assert g == ref.grid
+    assert np.array_equal(plan.e_init, ref.e) and np.array_equal(plan.h_init, ref.h)
+    if g.num_x > 1:
+        cells = plan.regions.per_cell(g.num_x)
+        for name in ("coef_a", "coef_bg", "coef_bdx", "coef_ch"):
+            assert np.array_equal(cells[name], getattr(ref, name)), name
+        assert plan.boundary == ref._bc
+    assert [(c, k) for c, k in zip(plan.src_cells, plan.src_hard)] == \
+        [(cell, 1 if src.kind == "hard" else 0) for src, cell in ref._sources]
+    for k, (src, _) in enumerate(ref._sources):
+        n = np.arange(1, g.num_t, max(1, g.num_t // 97))
+        assert np.array_equal(plan.src_values[n, k], [src.value(i * g.dt) for i in n])
+    for p, rp in zip(plan.plans, ref._plans):
+        assert (p.every, p.rows, p.cell, p.cols) == (rp.every, rp.rows, rp.cell, rp.cols)
+        assert repr(p.x0) == repr(rp.x0)  # -0.0 != 0.0 in the archive's json
+    assert [(a, b) for a, b, _ in plan.groups] == [(gr.start, gr.stop) for gr in ref.groups]
+    for (_, _, q), gr in zip(plan.groups, ref.groups):
+        qc, k = plan.qm[q], gr.kernel
+        if type(k).__name__ == "ScalarKernel":  # groups of <= 32 cells step through numpy
+            continue
+        assert qc.pol_factor == k._pol_factor and np.array_equal(qc.pol_v, k._pol_v)
+        if qc.bloch is not None:
+            assert (qc.bloch["kz"], qc.bloch["cz"], qc.bloch["fxy"]) == (k._kz, k._cz, k._fxy)
+            assert (qc.bloch["ax_c"], qc.bloch["ax_s"]) == k._ax and (qc.bloch["az_c"], qc.bloch["az_s"]) == k._az
+        elif qc.pop_half is not None:
+            assert np.array_equal(qc.pop_half, k.pop_half) and np.array_equal(qc.b_const, k._b_const)
+            assert np.array_equal(qc.coh_half, k.coh_half) and np.array_equal(qc.b_field, k._b_field)
+        elif qc.h0 is not None and hasattr(k, "_h0"):
+            assert np.array_equal(qc.h0, k._h0) and np.array_equal(qc.pop_matrix, k._pop)
 
 
-@pytest.mark.skipif(not REF.exists(), reason="reference not mounted (GPU box)")
-def test_plan_from_reference_objects_equals_plan_from_mirror():
-    """Drop-in: the GPU solver accepts the reference's own Device/Scenario."""
-    import os
+def test_whole_domain_record_origin_is_positive_zero():
+    """x0 of a whole-domain e/inv record is +0.0 as in the reference
+    (solver_fdtd.py:150), so meta.json of the archive matches byte for byte."""
+    import json
 
-    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
-    sys.path.insert(0, str(REF))
-    import mblight
-
-    from cases import CASES
-
-    for case in ("cfg2_r16", "multi_material", "rand5_split"):
-        build, stepper = CASES[case]
-        mblight.clear_material_library()
-        mb.clear_material_library()
-        a = mb.GpuFdtdSolver(*build(mblight), stepper=stepper).plan
-        b = mb.GpuFdtdSolver(*build(mb), stepper=stepper).plan
-        assert a.grid == b.grid
-        assert np.array_equal(a.e_init, b.e_init) and np.array_equal(a.h_init, b.h_init)
-        assert np.array_equal(a.src_values, b.src_values)
-        for name in ("e_start", "h_start", "coef_a", "coef_bg", "coef_bdx", "coef_ch", "qm_index"):
-            assert np.array_equal(getattr(a.regions, name), getattr(b.regions, name)), name
-        for qa, qb in zip(a.qm, b.qm):
-            for f in ("pop_half", "coh_half", "b_const", "b_field"):
-                if getattr(qa, f) is not None:
-                    assert np.array_equal(getattr(qa, f), getattr(qb, f)), f
-            assert qa.bloch == qb.bloch
-    mblight.clear_material_library()
+    dev, sce, stepper = build_case("sit_hard_whole")
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    whole = [p for p in plan.plans if p.cell is None and p.record.quantity != "h"]
+    assert whole and all(json.dumps(p.x0) == "0.0" for p in whole)
 
 
-@pytest.mark.skipif(not REF.exists(), reason="reference not mounted (GPU box)")
 def test_registration_into_the_reference_registry():
-    import os
-
-    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
-    sys.path.insert(0, str(REF))
-    import mblight
-
     from cases import CASES
 
-    mb.register_with_reference(mblight)
-    assert {"gpu-fdtd-reg-cayley", "gpu-fdtd-rk4"} <= set(mblight.available_solvers())
+    gpu.register_with_reference(mb)
+    assert {"gpu-fdtd-reg-cayley", "gpu-fdtd-rk4"} <= set(mb.available_solvers())
     build, _ = CASES["sit_hard_whole"]
-    mblight.clear_material_library()
-    dev, sce = build(mblight)
-    s = mblight.create_solver("gpu-fdtd-reg-cayley", dev, sce, seed=3)
-    assert isinstance(s, mb.GpuFdtdSolver) and s.seed == 3
-    assert s._result_cls is mblight.Result
-    mblight.clear_material_library()
+    dev, sce = build(mb)
+    s = mb.create_solver("gpu-fdtd-reg-cayley", dev, sce, seed=3)
+    assert isinstance(s, gpu.GpuFdtdSolver) and s.seed == 3
+
+
+def test_source_sample_cache_is_per_sweep():
+    """Without a caller-owned cache every plan samples its sources with
+    Source.value again, as the reference does on every run."""
+    from paper_2005_05412_b200 import plan as P
+
+    calls = []
+
+    class Counting(mb.SechPulse):
+        def value(self, t):
+            calls.append(t)
+            return super().value(t)
+
+    src = Counting("c", 0.0, "soft", 1.0, 2e14, 5.0, 1e15)
+    P._source_samples(src, 1e-17, 50)
+    P._source_samples(src, 1e-17, 50)
+    assert len(calls) == 98  # subclasses are never memoised
+    cache = {}
+    s2 = mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15)
+    a = P._source_samples(s2, 1e-17, 50, cache)
+    b = P._source_samples(mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15), 1e-17, 50, cache)
+    assert a is b and len(cache) == 1

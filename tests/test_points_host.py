@@ -7,7 +7,9 @@ import math
 import numpy as np
 import pytest
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 from paper_2005_05412_b200 import points as P
 from paper_2005_05412_b200.plan import build_plan
 

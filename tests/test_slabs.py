@@ -15,7 +15,9 @@ import pytest
 import torch.multiprocessing as mp
 from conftest import ROOT, build_case
 
-import paper_2005_05412_b200 as mb
+import paper_2005_05412_b200 as gpu
+
+from paper_2005_05412_b200.reference import mblight as mb
 from paper_2005_05412_b200 import slabs
 
 
@@ -55,7 +57,9 @@ def _worker(rank, world, port, case, k, period, out_path):
     import torch.distributed as dist
     from np_slab import NumpySlab
 
-    import paper_2005_05412_b200 as mbw
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mbw
     from paper_2005_05412_b200 import slabs as sl
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -67,7 +71,7 @@ def _worker(rank, world, port, case, k, period, out_path):
         build, stepper = CASES[case]
         mbw.clear_material_library()
         dev, sce = build(mbw)
-        solver = mbw.GpuFdtdSolver(dev, sce, stepper=stepper)
+        solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
         recs = sl.run_slab_rank(solver, world, rank, "cpu", state_factory=NumpySlab, k=k, period=period)
         if rank == 0:
             np.savez(out_path, *recs)
@@ -82,7 +86,7 @@ def test_gloo_ranks_match_oracle_bitwise(world, k, period, case):
     import oracle as orc
 
     dev, sce, stepper = build_case(case)
-    plan = mb.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
     ref, bad = orc.run_oracle(plan)
     assert bad == 0
     with tempfile.TemporaryDirectory() as d:
@@ -110,10 +114,10 @@ def test_native_slabs_on_one_gpu_match_single_domain(case, count, period):
     """Windowed solvers (persistent multi-chunk launches between exchanges for
     the two-level / classical kernels) bit-identical to the single domain."""
     dev, sce, stepper = build_case(case)
-    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     mb.clear_material_library()
     dev, sce, stepper = build_case(case)
-    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     got = slabs.run_slabs_local(solver, count, period)
     for a, b in zip(ref, got):
         assert a.name == b.name and a.data.shape == b.data.shape
@@ -141,10 +145,10 @@ def test_run_slab_rank_nccl_world_one_matches_single_domain():
     import torch
 
     dev, sce, stepper = build_case("multi_material")
-    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     mb.clear_material_library()
     dev, sce, stepper = build_case("multi_material")
-    solver = mb.GpuFdtdSolver(dev, sce, stepper=stepper)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     recs = _nccl_single(lambda: slabs.run_slab_rank(solver, 1, 0, torch.device("cuda", 0)))
     for a, b in zip(ref, recs):
         assert np.array_equal(a.data, b), a.name
@@ -180,7 +184,9 @@ def _gpu_worker(rank, world, port, case, period, out_path):
     import torch
     import torch.distributed as dist
 
-    import paper_2005_05412_b200 as mbw
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mbw
     from paper_2005_05412_b200 import slabs as sl
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -193,7 +199,7 @@ def _gpu_worker(rank, world, port, case, period, out_path):
         mbw.clear_material_library()
         dev, sce = build(mbw)
         torch.cuda.set_device(0)
-        solver = mbw.GpuFdtdSolver(dev, sce, stepper=stepper, gpu=0)
+        solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, gpu=0)
         recs = sl.run_slab_rank(solver, world, rank, torch.device("cuda", 0), period=period)
         if rank == 0:
             np.savez(out_path, *[r.data for r in recs])
@@ -209,7 +215,7 @@ def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period):
     TorchTransport exchange plan, pack/unpack on the adopted stream, scan-flag
     reduction and record gather, bit-identical to the single-domain run."""
     dev, sce, stepper = build_case(case)
-    ref = mb.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "recs.npz")
         mp.spawn(_gpu_worker, args=(world, _free_port(), case, period, out), nprocs=world, join=True)

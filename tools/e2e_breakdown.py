@@ -4,13 +4,14 @@ import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from paper_2005_05412_b200 import configs  # noqa: E402
 
 for rep in range(3):
     mb.clear_material_library()
     dev, sce = configs.cfg2(mb)
-    s = mb.GpuFdtdSolver(dev, sce)
+    s = gpu.GpuFdtdSolver(dev, sce)
     t = [time.perf_counter()]
     h = s.open_handle(); t.append(time.perf_counter())
     s.upload_initial_state(h); t.append(time.perf_counter())

@@ -15,7 +15,9 @@ sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from paper_2005_05412_b200 import configs  # noqa: E402
 
 names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
@@ -23,7 +25,7 @@ for name in names:
     mb.clear_material_library()
     t0 = time.perf_counter()
     dev, sce = getattr(configs, name)(mb)
-    sol = mb.GpuFdtdSolver(dev, sce, monitor_invariants=True)
+    sol = gpu.GpuFdtdSolver(dev, sce, monitor_invariants=True)
     t1 = time.perf_counter()
     res = sol.run()
     t2 = time.perf_counter()

@@ -15,7 +15,9 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from cases import CASES  # noqa: E402
 from conftest import load_golden, rel_err  # noqa: E402
 
@@ -29,7 +31,7 @@ for name in sorted(CASES):
         mb.clear_material_library()
         build, stepper = CASES[name]
         dev, sce = build(mb)
-        s = mb.GpuFdtdSolver(dev, sce, stepper=stepper, exact=exact)
+        s = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, exact=exact)
         t = time.perf_counter()
         res = s.run()
         wall = time.perf_counter() - t

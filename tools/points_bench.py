@@ -16,7 +16,9 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 import numpy as np  # noqa: E402
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from paper_2005_05412_b200.points import LAST_RUN, run_points  # noqa: E402
 from test_gpu_points import _song  # noqa: E402
 
@@ -32,7 +34,7 @@ t0 = time.perf_counter()
 res = run_points(problems, stepper=a.stepper)
 t_batch = time.perf_counter() - t0
 steps = 9999
-sol = mb.GpuFdtdSolver(*problems[0], stepper=a.stepper)
+sol = gpu.GpuFdtdSolver(*problems[0], stepper=a.stepper)
 t0 = time.perf_counter()
 sol.run()
 t_one = time.perf_counter() - t0

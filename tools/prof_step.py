@@ -13,7 +13,9 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from paper_2005_05412_b200 import configs  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -36,7 +38,7 @@ if a.config == "cfg5":
     dev, sce = configs.cfg5(mb, steps=total)
 else:
     dev, sce = getattr(configs, a.config)(mb, **kw, **({"steps": total} if a.config != "cfg1" else {}))
-sol = mb.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact,
+sol = gpu.GpuFdtdSolver(dev, sce, stepper=a.stepper, tile_steps=a.tile_steps, exact=a.exact,
                        persistent=False if a.per_launch else None)
 h = sol.open_handle()
 sol.upload_initial_state(h)

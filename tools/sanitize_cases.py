@@ -6,7 +6,9 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from cases import CASES  # noqa: E402
 from paper_2005_05412_b200 import slabs  # noqa: E402
 
@@ -15,10 +17,10 @@ for name in ["sit_hard_whole", "multi_material", "vacuum_sources", "rand3_split"
     mb.clear_material_library()
     build, stepper = CASES[name]
     dev, sce = build(mb)
-    mb.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True).run()
+    gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True).run()
     print("ok", name, flush=True)
 mb.clear_material_library()
 build, stepper = CASES["multi_material"]
 dev, sce = build(mb)
-slabs.run_slabs_local(mb.GpuFdtdSolver(dev, sce, stepper=stepper), 3)
+slabs.run_slabs_local(gpu.GpuFdtdSolver(dev, sce, stepper=stepper), 3)
 print("ok slabs", flush=True)

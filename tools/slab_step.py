@@ -20,7 +20,9 @@ sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 
-import paper_2005_05412_b200 as mb  # noqa: E402
+import paper_2005_05412_b200 as gpu  # noqa: E402
+
+from paper_2005_05412_b200.reference import mblight as mb  # noqa: E402
 from paper_2005_05412_b200 import configs, slabs  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -34,7 +36,7 @@ if a.config == "cfg2":
     dev, sce = configs.cfg2(mb, nx=(1 << 22) * a.world, steps=a.steps, replicas=a.world)
 else:
     dev, sce = configs.cfg5(mb, gpus=a.world, steps=a.steps)
-solver = mb.GpuFdtdSolver(dev, sce, tile_steps=a.tile_steps)
+solver = gpu.GpuFdtdSolver(dev, sce, tile_steps=a.tile_steps)
 k = slabs.tile_steps_of(solver)
 period = a.period or slabs.exchange_period(solver, k, a.world)
 part = slabs.partition(solver.grid.num_x, a.world, period)
