@@ -11,10 +11,17 @@ initial state (device-to-device), sample row 0, run every fused launch.
 
 ``value`` is device time (CUDA events on the launch stream, max over ranks)
 with the state resident in HBM; ``e2e`` times the public API call
-(``GpuFdtdSolver.run``) which uploads the initial fields from the host and
-downloads the records every step.  ``--impl reference`` times the CPU
-restatement of the reference algorithm (oracle/, a port: the reference is
-Python+numba and cannot be shipped to the GPU box) on all host cores.
+(``mblight.create_solver("gpu-fdtd-reg-cayley", ...).run()``: plan build with
+the sources sampled by Source.value, initial-state upload, the run, record
+download) every step.  ``--impl reference`` times the CPU restatement of the
+reference loop (oracle/, OpenMP C port) on all host cores; both lines also
+carry ``cpu_baseline_stock``: the reference's own numba solver
+(``mblight.FdtdSolver``, installed unmodified in baseline/_ref) on the same
+cores with all threads and with one, on bounded step samples.
+Extra keys: ``roofline`` (sustained FP64 denominator, algorithmic and executed
+fractions), ``n_level`` (BASELINE configs[2] / [3] samples), and
+``scaling_samples`` (cfg4 strong scaling and the cfg5 exchange-period sweep
+with efficiencies against one GPU; see scaling_samples()).
 """
 
 from __future__ import annotations
@@ -192,6 +199,7 @@ def run_reference(args, world, rank):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} of {plan.grid.num_t - 1} time steps at full Nx={nx} per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline_stock": None if args.no_cpu_baseline else stock_reference(args.gpus),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -224,8 +232,11 @@ def run_mine(args, world, rank, local):
     dev, sce = build_workload(mb, args.gpus)
     if world > 1:
         from paper_2005_05412_b200 import slabs
+        backend, _ = slabs.slab_backend(local)
+        samples = None if args.no_scaling_samples else (
+            lambda w, r, d: scaling_samples(w, r, d, backend=backend))
         return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT, clock_sampler=ClockSampler,
-                                rebuild=lambda: build_workload(mb, args.gpus))
+                                rebuild=lambda: build_workload(mb, args.gpus), samples=samples)
 
     solver = gpu.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
     plan = solver.plan
@@ -281,9 +292,13 @@ def run_mine(args, world, rank, local):
     # roofline of the dominant kernel: one persistent launch per run (two-level
     # medium, one GPU) working through ceil((Nt-1)/k) fused chunks
     b, f, fq = algorithmic_per_cell(plan)
-    peak_fp64 = C.c_double(0)
-    native.load().mbg_fp64_peak(local, C.byref(peak_fp64))
-    peak_fp64 = peak_fp64.value
+    burst = C.c_double(0)
+    native.load().mbg_fp64_peak(local, C.byref(burst))
+    sustained = C.c_double(0)
+    native.load().mbg_fp64_peak_sustained(local, 2.0, C.byref(sustained))
+    # the step kernel runs inside ~1 s of back-to-back runs: the sustained
+    # DFMA figure (>= 2 s train, same clocks) is its denominator
+    peak_fp64 = sustained.value
     bw, bw_src = measured_hbm_gbs()
     persistent = plan.levels <= 2 and solver.stepper == "splitting" and num_t - 1 > k
     chunks = (num_t - 1 + k - 1) // k
@@ -307,12 +322,13 @@ def run_mine(args, world, rank, local):
     if nc.get("mix_per_cell_step"):
         mix = nc["mix_per_cell_step"]
         executed = 2 * mix.get("DFMA", 0.0) + mix.get("DMUL", 0.0) + mix.get("DADD", 0.0)
+        roof["executed_frac"] = executed * cells_per_launch / (per_launch_ms * 1e-3) / 1e12 / peak_fp64
         roof["executed"] = {
             "source": f"profiles/ncu_summary.json[{ncu_key}] (ncu --set full of the same launch)",
             "fp64_instr_per_cell_step": nc.get("fp64_instr_per_cell_step"),
             "fp64_flops_per_cell_step": round(executed, 1),
             "fp64_pipe_pct": nc.get("fp64_pipe_pct"),
-            "achieved_tflops": executed * value / 1e12,
+            "achieved_tflops": executed * cells_per_launch / (per_launch_ms * 1e-3) / 1e12,
             "note": ("frac counts SURVEY 8(d)'s algorithmic flops (the reference's 82-flop Bloch step); the fast "
                      "kernel evaluates the same step in fewer FP64 operations (Rodrigues-form rotation, fused "
                      "relaxations), so frac can exceed 1 -- the executed figures and the FP64 pipe share "
@@ -328,7 +344,9 @@ def run_mine(args, world, rank, local):
         "launch_ms_avg": per_launch_ms, "launch_share_of_step": sum(adv_ms) / (ms * len(adv_ms) / args.steps),
         "hbm_achieved_gbs": bytes_launch / (per_launch_ms * 1e-3) / 1e9,
         "hbm_peak_gbs": bw, "hbm_peak_source": bw_src, "fp64_peak_tflops": peak_fp64,
-        "fp64_peak_source": "measured in-run (mbg_fp64_peak: DFMA chains on all SMs)",
+        "fp64_peak_burst_tflops": burst.value,
+        "fp64_peak_source": ("measured in-run: mbg_fp64_peak_sustained (independent DFMA chains on every SM, "
+                             "back to back for >= 2 s); burst = best single 1 ms launch (mbg_fp64_peak)"),
         "roofline_cell_updates_per_s": min(bw * 1e9 * k / b, peak_fp64 * 1e12 / f),
     })
 
@@ -338,8 +356,12 @@ def run_mine(args, world, rank, local):
     for it in range(args.warmup + args.steps):
         mb.clear_material_library()
         d2, s2 = build_workload(mb, 1)
-        sol = gpu.GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
         t0 = time.perf_counter()
+        # the call a user makes: create_solver(...) builds the plan (the sources
+        # sampled by Source.value, as the reference's run() does per step) and
+        # run() uploads, steps, downloads the records
+        sol = mb.create_solver("gpu-fdtd-reg-cayley", d2, s2, tile_steps=args.tile_steps, exact=args.exact,
+                               gpu=local)
         res = sol.run()
         dt_run = time.perf_counter() - t0
         if it >= args.warmup:
@@ -351,8 +373,14 @@ def run_mine(args, world, rank, local):
             h2d = 8 * (fields + p.state_words + p.src_values.size)
             d2h = sum(r.data.size * (16 if r.is_complex else 8) for r in res) + 8 * max(1, (num_t - 1) // (1 << 14))
     e2e_value = cell_updates / sum(e2e_times)
+    e2e_note = ("wall clock around mblight.create_solver('gpu-fdtd-reg-cayley', device, scenario).run(): plan "
+                "build (sources sampled with Source.value), initial-state upload, the run, record download")
 
-    n_level = None if args.no_n_level else n_level_samples(local)
+    n_level = None if args.no_n_level else n_level_samples(local, peak_fp64)
+    import torch
+
+    samples = None if args.no_scaling_samples else scaling_samples(1, 0, torch.device("cuda", local))
+    stock = None if args.no_cpu_baseline else stock_reference(1)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -363,19 +391,24 @@ def run_mine(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(plan, args, k),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "note": e2e_note},
         "gpu_launches": int(launches),  # persistent step + step-mask + row-0 sample kernels (library count)
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
+        # the reference's own numba solver on the same host cores (the cpu_baseline is the C port)
+        "cpu_baseline_stock": stock,
         # BASELINE configs[2], [3] (N = 3, N = 6) on one GPU, bounded samples beside the headline
         "n_level": n_level,
+        # cfg4 strong / cfg5 exchange-period samples (at N = 1: the single-GPU rates they scale from)
+        "scaling_samples": samples,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def n_level_samples(local, chunks=16):
+def n_level_samples(local, peak_tflops, chunks=16):
     """BASELINE configs[2] / [3] on one GPU (N = 3 on 2^23 cells, N = 6 on 2^24
     cells): device time of `chunks` fused launches from the initial state
     (bounded samples of the 50000- / 100000-step runs; reported beside the
@@ -387,8 +420,6 @@ def n_level_samples(local, chunks=16):
     from paper_2005_05412_b200.reference import mblight as mb
     from paper_2005_05412_b200 import configs, native
 
-    peak = C.c_double(0)
-    native.load().mbg_fp64_peak(local, C.byref(peak))
     out = {}
     for name, n in (("cfg3", 3), ("cfg4", 6)):
         mb.clear_material_library()
@@ -413,7 +444,7 @@ def n_level_samples(local, chunks=16):
         out[name] = {"levels": n, "num_x": sol.grid.num_x, "tile_steps": k.value, "sampled_steps": steps,
                      "of_steps": sol.grid.num_t - 1, "value": rate, "unit": UNIT,
                      "algorithmic_flops_per_cell_update": f, "achieved_tflops": rate * f / 1e12,
-                     "fp64_peak_tflops": peak.value, "frac": rate * f / 1e12 / peak.value,
+                     "fp64_peak_tflops": peak_tflops, "frac": rate * f / 1e12 / peak_tflops,
                      "launches": chunks}
     return out
 
@@ -435,6 +466,103 @@ def cpu_baseline(plan, steps):
                       f"Nx={plan.grid.num_x} ({t:.1f} s, OpenMP C restatement, oracle/mb_oracle.c)"}
 
 
+def stock_reference(gpus, steps_all=200, steps_one=40):
+    """The reference's own solver, unmodified (``mblight.FdtdSolver``, numba,
+    solver_fdtd.py:444-498, installed in baseline/_ref), on this box's host
+    cores: threads = cpu_count and threads = 1, each on a bounded sample --
+    the workload's grid and medium with the end time cut to a few steps (its
+    run() has no step limit).  A first tiny run compiles the numba loops."""
+    from paper_2005_05412_b200 import configs
+    from paper_2005_05412_b200.reference import mblight as mb
+
+    def sample(steps):
+        mb.clear_material_library()
+        if gpus == 1:
+            return configs.cfg2(mb, steps=steps)
+        return configs.cfg2(mb, nx=(1 << 22) * gpus, steps=steps, replicas=gpus)
+
+    dev, sce = configs.cfg2(mb, nx=4096, steps=4, cells=(16, 2000))
+    mb.FdtdSolver(dev, sce, threads=2).run()  # numba compile (cached in NUMBA_CACHE_DIR)
+    out = {"kind": "reference", "impl": "mblight.FdtdSolver (numba, unmodified)"}
+    for label, threads, steps in (("threads_all", os.cpu_count() or 1, steps_all), ("threads_1", 1, steps_one)):
+        dev, sce = sample(steps)
+        solver = mb.FdtdSolver(dev, sce, threads=threads)
+        t0 = time.perf_counter()
+        solver.run()
+        t = time.perf_counter() - t0
+        g = solver.grid
+        out[label] = {"value": g.num_x * (g.num_t - 1) / t, "unit": UNIT, "cores": solver.threads,
+                      "sample": f"cfg2 grid (Nx={g.num_x}) cut to {g.num_t - 1} time steps, {t:.1f} s "
+                                f"including its per-step Source.value and record sampling"}
+    return out
+
+
+SAMPLE_STEPS = 128
+
+
+def scaling_samples(world, rank, device, backend=None, reps=3):
+    """north_star's multi-GPU targets as bounded samples:
+
+    * ``cfg4_strong``: BASELINE configs[3] (six levels, 2^24 cells) split over
+      the ranks, SAMPLE_STEPS steps per run with the halo exchange every
+      period; efficiency = rate_N / (N * rate_1), rate_1 timed on rank 0
+      alone on the whole grid;
+    * ``cfg5_weak``: BASELINE configs[4] (cfg4's medium, 2^22 cells per rank)
+      for exchange periods P in {1, 4, 16, 64} steps (tile depth k = min(P, 4));
+      efficiency = per-rank rate / the single-domain rate of 2^22 cells at the
+      same k (rank 0 alone).
+    Device time, max over ranks; one warm-up run each."""
+    import torch.distributed as dist
+
+    import paper_2005_05412_b200 as gpu
+    from paper_2005_05412_b200 import configs, slabs
+    from paper_2005_05412_b200.reference import mblight as mb
+
+    def timed(build, w, tile_steps=None, period=None):
+        mb.clear_material_library()
+        dev, sce = build()
+        sol = gpu.GpuFdtdSolver(dev, sce, gpu=device.index, tile_steps=tile_steps)
+        overlap = w > 1 and slabs.overlaps_by_default(sol, backend or "nccl")
+        t = slabs.SlabTimer(sol, w, rank if w > 1 else 0, device, steps=SAMPLE_STEPS, period=period,
+                            overlap=overlap)
+        try:
+            ms = t.time(reps)
+        finally:
+            t.close()
+        return sol.grid.num_x * SAMPLE_STEPS * reps / (ms * 1e-3), t.k, t.period, overlap
+
+    def single(build, tile_steps=None):
+        """rank 0 alone: the 1-GPU rate of the same sample (broadcast)."""
+        val = None
+        if world == 1:
+            return None
+        if rank == 0:
+            val = timed(build, 1, tile_steps)[0]
+        box = [val]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    out = {"steps_per_run": SAMPLE_STEPS, "runs": reps}
+    rate, k, period, overlap = timed(lambda: configs.cfg4(mb), world)
+    one = single(lambda: configs.cfg4(mb))
+    out["cfg4_strong"] = {"num_x": 1 << 24, "levels": 6, "ranks": world, "tile_steps": k,
+                          "exchange_period": period if world > 1 else None, "overlap": overlap,
+                          "value": rate, "unit": UNIT, "single_gpu_value": one if world > 1 else rate,
+                          "efficiency": rate / (world * one) if one else 1.0}
+    sweep = []
+    for p in (1, 4, 16, 64):
+        kk = min(p, 4)
+        rate, k, period, overlap = timed(lambda: configs.cfg5(mb, gpus=world), world, tile_steps=kk,
+                                         period=p if world > 1 else None)
+        one = single(lambda: configs.cfg5(mb, gpus=1), tile_steps=kk)
+        per_rank = rate / world
+        sweep.append({"exchange_period": p, "tile_steps": k, "overlap": overlap, "value": rate,
+                      "per_rank_value": per_rank, "single_domain_value": one if world > 1 else per_rank,
+                      "efficiency": per_rank / one if one else 1.0})
+    out["cfg5_weak"] = {"num_x_per_rank": 1 << 22, "levels": 6, "ranks": world, "unit": UNIT, "sweep": sweep}
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -446,6 +574,7 @@ def main(argv=None):
     ap.add_argument("--cpu-steps", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-n-level", action="store_true", help="skip the N = 3 / N = 6 samples")
+    ap.add_argument("--no-scaling-samples", action="store_true", help="skip the cfg4 / cfg5 multi-GPU samples")
     args = ap.parse_args(argv)
     world, rank, local = dist_env()
     if args.gpus != world:

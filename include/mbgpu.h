@@ -194,6 +194,9 @@ int mbg_checkpoint_restore(mbg_solver *s);
 /* measured FP64 FMA throughput of the device (TFLOP/s), the FP64 roofline
  * denominator: independent DFMA chains on every SM, timed with CUDA events */
 int mbg_fp64_peak(int device, double *tflops);
+/* the same DFMA chains back to back for at least `seconds` (sustained clocks
+ * and power): the denominator for kernels timed inside a long run */
+int mbg_fp64_peak_sustained(int device, double seconds, double *tflops);
 
 /* timing helpers for bench.py: device time of the launches issued by
  * mbg_advance between mark_begin/mark_end (CUDA events on the solver stream) */

@@ -1328,6 +1328,16 @@ int mbg_checkpoint_restore(mbg_solver *s) {
     return MBG_OK;
 }
 
+int mbg_fp64_peak_sustained(int device, double seconds, double *tflops) {
+    mbg_solver *s = nullptr;
+    if (!tflops || !(seconds > 0)) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    double ms = 0.0, flops = 0.0;
+    CK(measure_fp64_sustained(seconds, &ms, &flops));
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return MBG_OK;
+}
+
 int mbg_fp64_peak(int device, double *tflops) {
     mbg_solver *s = nullptr;
     if (!tflops) return MBG_E_ARG;

@@ -318,6 +318,41 @@ cudaError_t measure_fp64_peak(double *ms, double *flops) {
     return err;
 }
 
+// the same DFMA chains back to back for at least `seconds` (one event pair
+// around the whole train): the throughput a kernel that runs for seconds
+// sees under the clocks and power of sustained FP64 load
+cudaError_t measure_fp64_sustained(double seconds, double *ms, double *flops) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double *out = nullptr;
+    cudaError_t err = cudaMalloc(&out, sizeof(double));
+    if (err != cudaSuccess) return err;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    fp64_fma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);  // warm
+    cudaEventRecord(a);
+    cudaEventSynchronize(a);
+    long long launches = 0;
+    float t = 0.f;
+    while (t < 1e3 * seconds) {  // batches of 64 launches (~80 ms), timed as one train
+        for (int i = 0; i < 64; ++i) fp64_fma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        launches += 64;
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&t, a, b);
+    }
+    err = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *ms = t;
+    *flops = 2.0 * 16.0 * iters * (double)blocks * threads * (double)launches;
+    return err;
+}
+
 cudaError_t launch_frame(bool to_frame, double *s, long long plane, long long win_n, const Regions &rg,
                          long long win_lo, const BlochFrame &F, double *out, cudaStream_t st) {
     if (win_n <= 0) return cudaSuccess;

@@ -116,5 +116,6 @@ cudaError_t launch_invariants(const Launch &L, int levels, int bloch, const Bloc
 
 // FP64 roofline denominator: best-of-5 DFMA throughput (ms of the best launch, flops per launch)
 cudaError_t measure_fp64_peak(double *ms, double *flops);
+cudaError_t measure_fp64_sustained(double seconds, double *ms, double *flops);
 
 }  // namespace mbg

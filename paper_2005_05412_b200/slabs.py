@@ -90,10 +90,11 @@ def exchange_plan(slab: Slab):
 class SlabState:
     """One slab on one device: the native handle plus its geometry."""
 
-    def __init__(self, solver, slab: Slab, stream: int = 0):
+    def __init__(self, solver, slab: Slab, stream: int = 0, records: bool = True):
         self.solver = solver
         self.slab = slab
-        self.h = solver.open_handle(win=(slab.win_lo, slab.win_hi), own=(slab.own_lo, slab.own_hi))
+        self.h = solver.open_handle(win=(slab.win_lo, slab.win_hi), own=(slab.own_lo, slab.own_hi),
+                                    records=records)
         if stream:
             self.h.call("mbg_set_stream", stream)
         solver.upload_initial_state(self.h, win=(slab.win_lo, slab.win_hi))
@@ -141,6 +142,79 @@ class SlabState:
         self.h.close()
 
 
+class EdgeStrips:
+    """The cells a slab sends its neighbours, computed ahead of the slab itself
+    so the halo exchange overlaps the slab's own advance.
+
+    Per interface, the g cells a neighbour needs after one exchange period of
+    P = g steps depend only on the 3g cells around them at the period's start
+    (the dependency cone widens one cell per side per step).  A strip solver
+    -- a second handle of the same solver with window [own_lo - g, own_lo + 2g)
+    on the left (mirrored on the right), owned part the g sent cells, no
+    records -- receives those 3g cells by a device copy, advances the period
+    on a side stream and packs the g cells into the send buffer; the exchange
+    then runs while the slab advances its whole window on the main stream.
+    Every cell executes the same instruction sequence in the strip as in the
+    slab, so the sent cells are bit-identical to the slab's own after the
+    period, and the ghosts the slab unpacks are those of the serial path.
+
+    Pays off for the N-level / RK4 kernels (launches of k steps that leave
+    SM slots free between CTAs, short periods); the two-level persistent
+    launch occupies every SM for its whole period, so its strips could not
+    run beside it (and its 2048-step period already amortises the exchange).
+    """
+
+    def __init__(self, main: "SlabState", period: int, stream):
+        import torch
+
+        self.main, self.g, self.stream = main, period, stream
+        sl = main.slab
+        g = period
+        if (sl.ghost_left or sl.ghost_right) and (sl.own_hi - sl.own_lo) < 2 * g:
+            raise ValueError("edge strips need slabs of at least two exchange periods")
+        self.sides = {}
+        solver = main.solver
+        for side in ("left", "right"):
+            if side == "left" and sl.ghost_left:
+                win, own = (sl.win_lo, sl.own_lo + 2 * g), (sl.own_lo, sl.own_lo + g)
+            elif side == "right" and sl.ghost_right:
+                win, own = (sl.own_hi - 2 * g, sl.win_hi), (sl.own_hi - g, sl.own_hi)
+            else:
+                continue
+            h = solver.open_handle(win=win, own=own, records=False)
+            h.call("mbg_set_stream", stream.cuda_stream)
+            scratch = torch.empty(main.words * (win[1] - win[0]), dtype=torch.float64, device=stream.device)
+            self.sides[side] = (h, win, own, scratch)
+        # the strips' state is copied from the slab every period (opaque halo
+        # words, already in the slab's storage frame): settle the handle's own
+        # frame on an uploaded initial state first (mbg_sample without records
+        # does only that), so no later call maps the copied words again
+        for h, win, _, _ in self.sides.values():
+            solver.upload_initial_state(h, win=win)
+            h.call("mbg_sample", 0)
+
+    def run(self, first: int, count: int, main_stream, send: dict):
+        """Enqueue one period: copy the strips' 3g cells from the slab (main
+        stream), then on the side stream advance them ``count`` steps and pack
+        the sent cells into ``send[side]`` (device tensors)."""
+        import torch
+
+        for h, win, own, scratch in self.sides.values():
+            self.main.pack(win[0], win[1] - win[0], scratch.data_ptr())
+        ready = torch.cuda.Event()
+        ready.record(main_stream)
+        self.stream.wait_event(ready)
+        for side, (h, win, own, scratch) in self.sides.items():
+            h.call("mbg_unpack_halo", win[0], win[1] - win[0], scratch.data_ptr())
+            h.call("mbg_advance", first, count)
+            h.call("mbg_pack_halo", own[0], own[1] - own[0], send[side].data_ptr())
+
+    def close(self):
+        for h, *_ in self.sides.values():
+            h.close()
+        self.sides = {}
+
+
 def assemble(plan, slabs, per_slab_records):
     """Merge slab records into full records (point records from their owner)."""
     out = []
@@ -182,16 +256,36 @@ class LocalTransport:
         for st in self.states:
             st.h.call("mbg_synchronize")
 
+    def exchange_from(self, sends):
+        """Ghosts from the neighbours' edge-strip send buffers (``sends[i]``:
+        side -> device tensor of slab i's strips)."""
+        for i, st in enumerate(self.states):
+            _, rl, _, rr = exchange_plan(st.slab)
+            if rl is not None:
+                st.unpack(rl[0], rl[1], sends[i - 1]["right"].data_ptr())
+            if rr is not None:
+                st.unpack(rr[0], rr[1], sends[i + 1]["left"].data_ptr())
+        for st in self.states:
+            st.h.call("mbg_synchronize")
+
 
 class TorchTransport:
-    """One slab per process; neighbours exchange with batched isend/irecv."""
+    """One slab per process; neighbours exchange with batched isend/irecv.
 
-    def __init__(self, state: SlabState, device):
+    ``exchange()`` = ``start()`` + ``finish()``: pack the slab's edge cells,
+    send/receive, unpack the ghosts.  With edge strips (:class:`EdgeStrips`)
+    the sent cells are packed by the strips on their side stream and
+    ``start(packed=True)`` issues the transfer there; the slab's own advance
+    is enqueued before ``finish()``, whose wait makes the main stream (not
+    the host) wait for the transfer."""
+
+    def __init__(self, state: SlabState, device, side_stream=None):
         import torch
         import torch.distributed as dist
 
         self.torch, self.dist = torch, dist
         self.state = state
+        self.side_stream = side_stream
         sl, rl, sr, rr = exchange_plan(state.slab)
         self.plan = (sl, rl, sr, rr)
         w = state.words
@@ -210,33 +304,54 @@ class TorchTransport:
 
             self.h_send_l, self.h_recv_l = host(self.send_l), host(self.recv_l)
             self.h_send_r, self.h_recv_r = host(self.send_r), host(self.recv_r)
+        self._reqs = []
 
-    def exchange(self):
+    @property
+    def send(self) -> dict:
+        """Device send buffers by side (what EdgeStrips.run packs into)."""
+        return {k: v for k, v in (("left", self.send_l), ("right", self.send_r)) if v is not None}
+
+    def start(self, packed: bool = False):
         sl, rl, sr, rr = self.plan
         st, dist = self.state, self.dist
         rank = st.slab.rank
-        ops = []
+        if not packed:
+            if sl is not None:
+                st.pack_into(sl[0], sl[1], self.send_l)
+            if sr is not None:
+                st.pack_into(sr[0], sr[1], self.send_r)
         if self.stage:
+            if packed and self.side_stream is not None:
+                self.side_stream.synchronize()  # the strips packed on the side stream
+            for d, h in ((self.send_l, self.h_send_l), (self.send_r, self.h_send_r)):
+                if d is not None:
+                    h.copy_(d)  # synchronous: the pack kernel has run
             send_l, recv_l, send_r, recv_r = self.h_send_l, self.h_recv_l, self.h_send_r, self.h_recv_r
         else:
             send_l, recv_l, send_r, recv_r = self.send_l, self.recv_l, self.send_r, self.recv_r
+        ops = []
         if sl is not None:
-            st.pack_into(sl[0], sl[1], self.send_l)
             ops.append(dist.P2POp(dist.isend, send_l, rank - 1))
             ops.append(dist.P2POp(dist.irecv, recv_l, rank - 1))
         if sr is not None:
-            st.pack_into(sr[0], sr[1], self.send_r)
             ops.append(dist.P2POp(dist.isend, send_r, rank + 1))
             ops.append(dist.P2POp(dist.irecv, recv_r, rank + 1))
+        if not ops:
+            self._reqs = []
+            return
+        ctx = self.torch.cuda.stream(self.side_stream) if (packed and self.side_stream is not None
+                                                          and not self.stage) else _nullcontext()
+        with ctx:  # NCCL's stream waits for the stream current here
+            self._reqs = dist.batch_isend_irecv(ops)
+
+    def finish(self):
+        sl, rl, sr, rr = self.plan
+        st = self.state
+        for req in self._reqs:
+            req.wait()  # NCCL: the current (main) stream waits; gloo: the host waits
+        self._reqs = []
         if self.stage:
-            for d, h in ((self.send_l, send_l), (self.send_r, send_r)):
-                if d is not None:
-                    h.copy_(d)  # synchronous: the pack kernel has run
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-        if self.stage:
-            for d, h in ((self.recv_l, recv_l), (self.recv_r, recv_r)):
+            for d, h in ((self.recv_l, self.h_recv_l), (self.recv_r, self.h_recv_r)):
                 if d is not None:
                     d.copy_(h)
         if rl is not None:
@@ -244,16 +359,22 @@ class TorchTransport:
         if rr is not None:
             st.unpack_from(rr[0], rr[1], self.recv_r)
 
+    def exchange(self):
+        self.start()
+        self.finish()
+
 
 # ---------------------------------------------------------------- drivers --
 
-def _step_loop(grid, k, advance, exchange, poll, poll_every=1 << 14):
+def _step_loop(grid, period, step_period, poll, poll_every=1 << 14):
+    """Steps 1..num_t-1 in exchange periods: ``step_period(n, cnt)`` advances
+    steps n..n+cnt-1 and refreshes the ghosts; the non-finite flag is polled
+    every ``poll_every`` steps and at the end."""
     n = 1
     since = 0
     while n < grid.num_t:
-        cnt = min(k, grid.num_t - n)
-        advance(n, cnt)
-        exchange()
+        cnt = min(period, grid.num_t - n)
+        step_period(n, cnt)
         n += cnt
         since += cnt
         if since >= poll_every or n >= grid.num_t:
@@ -263,11 +384,20 @@ def _step_loop(grid, k, advance, exchange, poll, poll_every=1 << 14):
                 raise SolverError(f"non-finite electric field at step {bad}")
 
 
-def run_slabs_local(solver, slabs_count: int, period=None):
+def _check_monitor(solver):
+    if solver.monitor_invariants:
+        raise NotImplementedError("the slab drivers do not run the invariant monitor; "
+                                  "use GpuFdtdSolver.run() for a monitored run")
+
+
+def run_slabs_local(solver, slabs_count: int, period=None, overlap: bool = False):
     """Run ``solver``'s scenario as ``slabs_count`` slabs on one device (tests);
-    ``period`` = steps between exchanges (default exchange_period)."""
+    ``period`` = steps between exchanges (default exchange_period);
+    ``overlap``: the sent cells come from edge strips (EdgeStrips) on a side
+    stream instead of the slabs themselves."""
     if solver._ran:
         raise SolverError("run() may only be called once per solver instance")
+    _check_monitor(solver)
     solver._ran = True
     import torch
 
@@ -275,24 +405,43 @@ def run_slabs_local(solver, slabs_count: int, period=None):
     period = period or exchange_period(solver, k, slabs_count)
     slabs = partition(solver.grid.num_x, slabs_count, period)
     # one shared stream: every pack, unpack and launch runs in issue order
-    stream = torch.cuda.Stream(device=f"cuda:{solver.gpu}")
+    device = torch.device("cuda", solver.gpu)
+    stream = torch.cuda.Stream(device=device)
     states = [SlabState(solver, s, stream=stream.cuda_stream) for s in slabs]
+    strips, sends = [], []
     try:
         tr = LocalTransport(states)
+        if overlap:
+            side = torch.cuda.Stream(device=device, priority=-1)
+            strips = [EdgeStrips(st, period, side) for st in states]
+            sends = [{k2: torch.empty(st.words * period, dtype=torch.float64, device=device) for k2 in sp.sides}
+                     for st, sp in zip(states, strips)]
         for st in states:
             st.sample(0)
 
-        def advance(n, cnt):
+        def step_period(n, cnt):
+            if overlap:
+                for sp, snd in zip(strips, sends):
+                    sp.run(n, cnt, stream, snd)
             for st in states:
                 st.advance(n, cnt)
+            if overlap:
+                done = torch.cuda.Event()
+                done.record(side)
+                stream.wait_event(done)
+                tr.exchange_from(sends)
+            else:
+                tr.exchange()
 
         def poll():
             bads = [b for b in (st.poll() for st in states) if b >= 0]
             return min(bads) if bads else -1
 
-        _step_loop(solver.grid, period, advance, tr.exchange, poll)
+        _step_loop(solver.grid, period, step_period, poll)
         recs = assemble(solver.plan, slabs, [st.records() for st in states])
     finally:
+        for sp in strips:
+            sp.close()
         for st in states:
             st.close()
     solver.results = [p.to_result(solver.grid, d) for p, d in zip(solver.plan.plans, recs)]
@@ -361,40 +510,69 @@ def slab_backend(local: int):
     return backend, local
 
 
-def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None):
+def overlaps_by_default(solver, backend: str) -> bool:
+    """Edge strips for the N-level / RK4 kernels under NCCL (see EdgeStrips)."""
+    dense = solver.plan.levels > 2 or (solver.plan.levels == 2 and solver.stepper == "rk4")
+    return dense and backend == "nccl"
+
+
+def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None, overlap=None):
     """This process's slab of a ``world``-way run (torch.distributed initialised).
     Returns the assembled records on rank 0 and None elsewhere.
 
     ``state_factory(solver, slab)`` replaces the native slab (tests drive the
-    same host logic with a CPU slab stepper under gloo)."""
+    same host logic with a CPU slab stepper under gloo).  ``overlap``: send
+    the edge strips' cells while the slab advances (default: N-level / RK4
+    under NCCL, see :func:`overlaps_by_default`)."""
     import torch
     import torch.distributed as dist
 
+    _check_monitor(solver)
     if k is None:
         k = tile_steps_of(solver)
     period = period or exchange_period(solver, k, world)
     slabs = partition(solver.grid.num_x, world, period)
+    if overlap is None:
+        overlap = state_factory is None and overlaps_by_default(solver, dist.get_backend())
+    if overlap and state_factory is not None:
+        raise ValueError("edge strips need native slabs")
     # the native launches, the pack/unpack kernels and torch's NCCL ops must
     # be ordered on one stream: a dedicated torch stream, made current, that
     # the native handle adopts (the legacy default stream cannot be adopted)
     stream = torch.cuda.Stream(device) if state_factory is None else None
+    side = torch.cuda.Stream(device, priority=-1) if overlap else None
     if state_factory is None:
         st = SlabState(solver, slabs[rank], stream=stream.cuda_stream)
     else:
         st = state_factory(solver, slabs[rank])
+    strips = None
     try:
         with torch.cuda.stream(stream) if stream is not None else _nullcontext():
-            tr = TorchTransport(st, device)
+            tr = TorchTransport(st, device, side_stream=side)
+            if overlap:
+                strips = EdgeStrips(st, period, side)
             st.sample(0)
+
+            def step_period(n, cnt):
+                if strips is not None:
+                    strips.run(n, cnt, stream, tr.send)
+                    tr.start(packed=True)
+                    st.advance(n, cnt)
+                    tr.finish()
+                else:
+                    st.advance(n, cnt)
+                    tr.exchange()
 
             def poll():
                 b = st.poll()
                 v = int(_reduce_scalar(b if b >= 0 else 2**62, dist.ReduceOp.MIN, device, torch.int64))
                 return -1 if v == 2**62 else v
 
-            _step_loop(solver.grid, period, st.advance, tr.exchange, poll)
+            _step_loop(solver.grid, period, step_period, poll)
         mine = st.records()
     finally:
+        if strips is not None:
+            strips.close()
         st.close()
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(mine, gathered, dst=0)
@@ -403,15 +581,117 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     return assemble(solver.plan, slabs, gathered)
 
 
-def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=None, rebuild=None):
+class SlabTimer:
+    """Bounded, repeatable slab runs for the benchmark: this rank's slab (and
+    edge strips) stay resident, every run restores the initial state from a
+    device checkpoint and advances ``steps`` steps with an exchange every
+    period.  ``time(reps)`` returns device milliseconds of ``reps`` runs
+    (CUDA events on the launch stream), max over ranks.  World size 1 is a
+    single slab without ghosts (no transport): the single-domain run."""
+
+    def __init__(self, solver, world: int, rank: int, device, steps: int, period=None, k=None,
+                 overlap: bool = False):
+        import torch
+
+        self.torch = torch
+        self.world, self.rank, self.device = world, rank, device
+        self.k = tile_steps_of(solver) if k is None else k
+        self.period = period or (exchange_period(solver, self.k, world) if world > 1 else max(1, steps))
+        self.steps = steps
+        self.slabs = partition(solver.grid.num_x, world, self.period if world > 1 else 0)
+        self.stream = torch.cuda.Stream(device)
+        self.side = torch.cuda.Stream(device, priority=-1) if overlap else None
+        self.st = SlabState(solver, self.slabs[rank], stream=self.stream.cuda_stream)
+        self.tr = None
+        self.strips = None
+        with torch.cuda.stream(self.stream):
+            if world > 1:
+                self.tr = TorchTransport(self.st, device, side_stream=self.side)
+                if overlap:
+                    self.strips = EdgeStrips(self.st, self.period, self.side)
+        self.st.h.call("mbg_checkpoint_save")
+        self.grid = solver.grid
+
+    def _period(self, n, cnt):
+        st, tr = self.st, self.tr
+        if tr is None:
+            st.advance(n, cnt)
+        elif self.strips is not None:
+            self.strips.run(n, cnt, self.stream, tr.send)
+            tr.start(packed=True)
+            st.advance(n, cnt)
+            tr.finish()
+        else:
+            st.advance(n, cnt)
+            tr.exchange()
+
+    def one_run(self):
+        self.st.h.call("mbg_checkpoint_restore")
+        self.st.sample(0)
+        n = 1
+        end = 1 + self.steps
+        while n < end:
+            cnt = min(self.period, end - n)
+            self._period(n, cnt)
+            n += cnt
+
+    def launches(self) -> int:
+        v = C.c_int64(0)
+        self.st.h.call("mbg_launch_count", C.byref(v))
+        return int(v.value)
+
+    def time(self, reps: int, warmup: int = 1, sampler=None) -> float:
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):
+                self.one_run()
+            torch.cuda.synchronize(self.device)
+            self._barrier()
+            l0 = self.launches()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            with sampler if sampler is not None else _nullcontext():
+                t0.record(self.stream)
+                for _ in range(reps):
+                    self.one_run()
+                t1.record(self.stream)
+                torch.cuda.synchronize(self.device)
+            self._barrier()
+        self.timed_launches = self.launches() - l0
+        ms = t0.elapsed_time(t1)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            ms = _reduce_scalar(ms, dist.ReduceOp.MAX, self.device)
+        bad = self.st.poll()
+        if bad >= 0:
+            raise SolverError(f"non-finite electric field at step {bad}")
+        return float(ms)
+
+    def _barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def close(self):
+        if self.strips is not None:
+            self.strips.close()
+        self.st.close()
+
+
+def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=None, rebuild=None,
+               samples=None):
     """bench.py --gpus N under torchrun: weak-scaled cfg2, one slab per GPU,
     device time of K full runs, max over ranks.
 
     ``clock_sampler(gpu)``: context manager sampling clocks during the timed
     region (bench.py's ClockSampler); ``rebuild()``: fresh (device, scenario)
     for the end-to-end runs through run_slab_rank (the public multi-GPU call:
-    window upload, exchanges, record download and gather), wall-clocked with
-    barriers, max over ranks."""
+    plan build, window upload, exchanges, record download and gather),
+    wall-clocked with barriers, max over ranks; ``samples(world, rank,
+    device)``: extra bounded multi-GPU workloads (bench.py: cfg4 strong
+    scaling, cfg5 exchange-period sweep), reported under ``scaling_samples``."""
     import json
     import os
     import time
@@ -427,64 +707,24 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
     if not dist.is_initialized():
         dist.init_process_group(backend, device_id=device if backend == "nccl" else None)
     solver = GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
-    k = tile_steps_of(solver)
-    period = exchange_period(solver, k, world)
-    slabs = partition(solver.grid.num_x, world, period)
-    # one stream for the native launches, the halo pack/unpack and NCCL (see run_slab_rank)
-    stream = torch.cuda.Stream(device)
-    st = SlabState(solver, slabs[rank], stream=stream.cuda_stream)
-    ctx = torch.cuda.stream(stream)
-    ctx.__enter__()
-    tr = TorchTransport(st, device)
-    st.h.call("mbg_checkpoint_save")
     grid = solver.grid
-
-    def one_run():
-        st.h.call("mbg_checkpoint_restore")
-        st.sample(0)
-        n = 1
-        while n < grid.num_t:
-            cnt = min(period, grid.num_t - n)
-            st.advance(n, cnt)
-            tr.exchange()
-            n += cnt
-
-    for _ in range(args.warmup):
-        one_run()
-    torch.cuda.synchronize(device)
-    dist.barrier()
-    l0 = C.c_int64(0)
-    st.h.call("mbg_launch_count", C.byref(l0))
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    sampler = clock_sampler(local) if clock_sampler is not None else _nullcontext()
-    with sampler:
-        t0.record(stream)
-        for _ in range(args.steps):
-            one_run()
-        t1.record(stream)
-        torch.cuda.synchronize(device)
-    dist.barrier()
-    ms = _reduce_scalar(t0.elapsed_time(t1), dist.ReduceOp.MAX, device)
-    l1 = C.c_int64(0)
-    st.h.call("mbg_launch_count", C.byref(l1))
-    bad = st.poll()
-    st.close()
-    ctx.__exit__(None, None, None)
-    if bad >= 0:
-        raise SolverError(f"non-finite electric field at step {bad}")
-    ms = float(ms)
+    timer = SlabTimer(solver, world, rank, device, steps=grid.num_t - 1)
+    k, period, slabs = timer.k, timer.period, timer.slabs
+    sampler = clock_sampler(local) if clock_sampler is not None else None
+    ms = timer.time(args.steps, warmup=args.warmup, sampler=sampler)
+    launches = timer.timed_launches
+    timer.close()
     cells = grid.num_x * (grid.num_t - 1) * args.steps
 
     e2e = None
     if rebuild is not None:
         walls = []
         for it in range(args.warmup + args.steps):
-            d2, s2 = rebuild()
-            sol = GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
             torch.cuda.synchronize(device)
             dist.barrier()
             w0 = time.perf_counter()
+            d2, s2 = rebuild()
+            sol = GpuFdtdSolver(d2, s2, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
             run_slab_rank(sol, world, rank, device)
             torch.cuda.synchronize(device)
             w = _reduce_scalar(time.perf_counter() - w0, dist.ReduceOp.MAX, device)
@@ -498,10 +738,11 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
                "d2h_bytes_per_step": int(sum(p.rows * (mine.own_hi - mine.own_lo if p.cell is None else 1) *
                                              (16 if p.is_complex else 8) for p in plan.plans
                                              if p.cell is None or mine.own_lo <= p.cell < mine.own_hi)),
-               "note": "rank 0's bytes; wall clock around run_slab_rank (window upload, exchanges, record "
-                       "download + gather), max over ranks"}
+               "note": "rank 0's bytes; wall clock around the public multi-GPU call (plan build with the "
+                       "sources sampled by Source.value, window upload, exchanges, record download + "
+                       "gather), max over ranks"}
+    extra = samples(world, rank, device) if samples is not None else None
     if rank == 0:
-        launches = l1.value - l0.value
         line = {
             "metric": metric, "value": cells / (ms * 1e-3), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -517,12 +758,13 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
             "e2e": e2e,
             # this rank's kernels (step, step-mask, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),
+            "scaling_samples": extra,
         }
         if backend != "nccl" or local != int(os.environ.get("LOCAL_RANK", local)):
             line["config"]["shared_gpu"] = (f"all {world} ranks on GPU {local}, {backend} exchanges staged "
                                             f"through the host: a functional run of the multi-rank path, "
                                             f"not a scaling measurement")
-        if clock_sampler is not None:
+        if sampler is not None:
             line["clocks"] = sampler.summary()
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -99,8 +99,10 @@ class GpuFdtdSolver:
         s.own_lo, s.own_hi = own if own is not None else (s.win_lo, s.win_hi)
         return s
 
-    def open_handle(self, win=None, own=None) -> native.Handle:
-        """Create the device solver and upload everything but the initial state."""
+    def open_handle(self, win=None, own=None, records=True) -> native.Handle:
+        """Create the device solver and upload everything but the initial state
+        (``records=False``: a handle that never samples, e.g. the edge-strip
+        solvers of a slab)."""
         plan = self.plan
         h = native.Handle(self._grid_struct(win, own))
         rt = plan.regions
@@ -117,7 +119,7 @@ class GpuFdtdSolver:
         cells, hard, vals = native.i64(plan.src_cells), native.i32(plan.src_hard), native.f64(plan.src_values)
         h.call("mbg_set_sources", len(cells), native.ptr(cells, native._i64p), native.ptr(hard, native._i32p),
                native.ptr(vals))
-        ps = plan.plans
+        ps = plan.plans if records else []
         q = native.i32([p.quantity for p in ps])
         cell = native.i64([-1 if p.cell is None else p.cell for p in ps])
         ii, jj = native.i32([p.i for p in ps]), native.i32([p.j for p in ps])

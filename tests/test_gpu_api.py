@@ -378,7 +378,7 @@ def test_records_stream_automatically_past_the_device_budget(monkeypatch):
     sol = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
     assert sol._segment_steps() >= 1024
     got = sol.run()
-    assert sol._host_rows is not None
+    assert sol._streamed
     for a, b in zip(ref, got):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
 
@@ -413,7 +413,7 @@ def test_streamed_records_with_the_invariant_monitor():
     dev, sce, stepper = build_case("rand3_split")
     b = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True, record_segment=37)
     rb = b.run()
-    assert b._host_rows is not None
+    assert b._streamed
     for x, y in zip(ra, rb):
         assert np.array_equal(x.data, y.data), x.name
     assert a.invariant_report == b.invariant_report
