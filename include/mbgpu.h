@@ -16,6 +16,7 @@
  *   mbg_set_qm_rk4        VectorRk4Kernel constants                _kernels.py:552-557
  *   mbg_set_boundary      boundary precompute                      solver_fdtd.py:310-325
  *   mbg_set_sources       Source.value(n dt) per step              solver_fdtd.py:379-385
+ *   mbg_set_source_rows   (same samples, streamed per run segment)  solver_fdtd.py:379-385
  *   mbg_set_records       _RecordPlan list                         solver_fdtd.py:136-172,300-305
  *   mbg_upload_fields     initial E / H                            solver_fdtd.py:237-239
  *   mbg_upload_density    DensityKernel.init_state                 _kernels.py:376-377, 496-500
@@ -113,9 +114,15 @@ int mbg_set_qm_rk4(mbg_solver *s, int32_t qm, const double *h0, const double *mu
                    int32_t ndpol, const int32_t *pol_di, const double *pol_dv, double pol_factor);
 /* w = 1 - sqrt(R), c = v dt / dx, z = sqrt(mu / eps) of the edge materials */
 int mbg_set_boundary(mbg_solver *s, double wl, double cl, double zl, double wr, double cr, double zr);
-/* values: [num_t][n] samples Source.value(n dt) (row 0 unused) */
+/* values: [num_t][n] samples Source.value(n dt) (row 0 unused); NULL: the
+ * table starts zero and its rows come through mbg_set_source_rows */
 int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t *hard,
                     const double *values);
+/* rows [lo, hi) of the sample table (rows: (hi - lo) x n doubles), copied
+ * stream-ordered through pinned staging: the run samples its sources segment
+ * by segment while the device steps (Source.value inside the reference's
+ * loop, solver_fdtd.py:379-385) */
+int mbg_set_source_rows(mbg_solver *s, int64_t lo, int64_t hi, const double *rows);
 /* quantity MBG_Q_*, cell -1 = whole domain, i/j 0-based, every >= 1; complex for d with i != j */
 int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *quantity, const int64_t *cell,
                     const int32_t *i, const int32_t *j, const int64_t *every);

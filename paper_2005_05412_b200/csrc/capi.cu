@@ -67,6 +67,7 @@ struct mbg_solver {
     long long src_cell[kMaxSources] = {};
     int src_hard[kMaxSources] = {};
     double *src_values = nullptr;
+    double *src_host = nullptr;  // pinned staging of the sample table (rows uploaded as they are sampled)
     std::vector<Rec> recs;
     unsigned long long *bad = nullptr;
     unsigned long long *inv = nullptr;  // running invariant keys (mbg_invariants_accumulate)
@@ -507,6 +508,7 @@ void mbg_destroy(mbg_solver *s) {
         dfree(st, r.im);
     }
     if (st) cudaStreamSynchronize(st);
+    if (s->src_host) cudaFreeHost(s->src_host);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     for (cudaEvent_t e : s->marks)
@@ -652,6 +654,11 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
     if (!s || n < 0) return MBG_E_ARG;
     if (n > kMaxSources) return fail(s, MBG_E_UNSUPPORTED, "too many sources (max 32)");
     cudaSetDevice(s->g.device);
+    if (s->src_host) {
+        CK(cudaStreamSynchronize(s->stream));  // no copy out of the old staging in flight
+        cudaFreeHost(s->src_host);
+        s->src_host = nullptr;
+    }
     dfree(s->stream, s->src_values);
     s->src_values = nullptr;
     s->n_src = n;
@@ -663,9 +670,30 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
     if (n > 0) {
         const size_t bytes = sizeof(double) * (size_t)n * s->g.num_t;
         CK(dalloc(s->stream, &s->src_values, bytes));
-        CK(cudaMemcpyAsync(s->src_values, values, bytes, cudaMemcpyHostToDevice, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
+        if (values) {
+            CK(cudaMemcpyAsync(s->src_values, values, bytes, cudaMemcpyHostToDevice, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+        } else {
+            // rows arrive later (mbg_set_source_rows) through a pinned staging copy
+            CK(cudaMemsetAsync(s->src_values, 0, bytes, s->stream));
+            CK(cudaMallocHost(reinterpret_cast<void **>(&s->src_host), bytes));
+        }
     }
+    return MBG_OK;
+}
+
+int mbg_set_source_rows(mbg_solver *s, int64_t lo, int64_t hi, const double *rows) {
+    if (!s || lo < 0 || hi < lo || hi > s->g.num_t) return MBG_E_ARG;
+    if (s->n_src == 0 || hi == lo) return MBG_OK;
+    if (!s->src_host) return fail(s, MBG_E_STATE, "mbg_set_source_rows needs mbg_set_sources(..., values = NULL)");
+    if (!rows) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    const size_t off = (size_t)lo * s->n_src, cnt = (size_t)(hi - lo) * s->n_src;
+    // stream order: these rows reach the device before any later launch
+    // reads them; the staging rows of earlier calls are never rewritten
+    std::memcpy(s->src_host + off, rows, sizeof(double) * cnt);
+    CK(cudaMemcpyAsync(s->src_values + off, s->src_host + off, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                       s->stream));
     return MBG_OK;
 }
 

@@ -228,21 +228,31 @@ class SolverPlan:
     seed: int
     stepper: str
     levels: int  # N of the quantum materials, 0 if none
-    e_init: np.ndarray
-    h_init: np.ndarray  # num_x + 1 entries, last is 0
     regions: RegionTable
     qm: list
     groups: list  # (start, stop, qm_index)
     rho_init: np.ndarray  # complex N x N (or None)
     src_cells: np.ndarray
     src_hard: np.ndarray
-    src_values: np.ndarray  # [num_t, n_src], row n = value at t = n dt
     plans: list
     boundary: tuple  # ((w, c dt/dx, Z) left, (...) right) or None
     materials: list = field(default_factory=list)
     # the initial fields are identically zero (the scenario's default
     # ConstantField(0)): the upload is a device memset instead of a copy
     fields_zero: bool = False
+    sources: list = field(default_factory=list)
+    # initial fields: built by the scenario's own IC objects; a ConstantField
+    # (which cannot fail) is built only when first read
+    ic_fields: tuple = (None, None)
+    _e_init: np.ndarray | None = None
+    _h_init: np.ndarray | None = None
+    # source samples [num_t, n_src] (row n = Source.value(n dt)), filled on
+    # demand: the GPU run samples them segment by segment while the device
+    # steps the previous segment (the reference calls Source.value inside its
+    # time loop, solver_fdtd.py:379-385); sampled_to = rows [0, sampled_to) done
+    _src_values: np.ndarray | None = None
+    sampled_to: int = 1
+    sample_cache: dict | None = None
 
     @property
     def state_words(self) -> int:
@@ -253,30 +263,101 @@ class SolverPlan:
             return np.zeros(0)
         return pack_density(self.rho_init, self.stepper)
 
+    @property
+    def e_init(self) -> np.ndarray:
+        if self._e_init is None:
+            self._e_init = np.ascontiguousarray(self.ic_fields[0].build(self.grid.num_x, self.seed), dtype=float)
+        return self._e_init
 
-def _source_samples(src, dt: float, num_t: int, cache: dict | None = None) -> np.ndarray:
-    """Source.value(n dt) for n = 1..num_t-1 (row 0 unused), the source's own
-    function call by call (solver_fdtd.py:378-385).  ``cache`` (optional,
-    owned by the caller, e.g. one ``run_points`` sweep) shares the samples of
-    equal sources of the two frozen pulse types the reference defines."""
-    key = None
-    if cache is not None and type(src) in (core.SechPulse, core.GaussianPulse):
-        key = (type(src), src, dt, num_t)  # frozen dataclasses: hashable by value
-    if key is not None and key in cache:
-        return cache[key]
-    col = np.zeros(num_t)
-    for n in range(1, num_t):
-        col[n] = src.value(n * dt)
-    if key is not None:
+    @property
+    def h_init(self) -> np.ndarray:
+        """num_x + 1 entries, the last one 0 (solver_fdtd.py:238-239)."""
+        if self._h_init is None:
+            nx = self.grid.num_x
+            h = np.zeros(nx + 1)
+            h[0:nx] = self.ic_fields[1].build(nx, self.seed + 1)
+            self._h_init = h
+        return self._h_init
+
+    @property
+    def src_buffer(self) -> np.ndarray:
+        """The [num_t, n_src] sample table (rows past ``sampled_to`` not filled yet)."""
+        if self._src_values is None:
+            self._src_values = np.zeros((self.grid.num_t, len(self.sources)))
+        return self._src_values
+
+    def sample_sources(self, hi: int) -> tuple[int, int]:
+        """Fill sample rows up to ``hi`` (exclusive) with each source's own
+        ``value(n dt)``; returns the rows [lo, hi) filled by this call."""
+        buf = self.src_buffer
+        lo = self.sampled_to
+        hi = min(int(hi), self.grid.num_t)
+        if hi <= lo:
+            return lo, lo
+        dt = self.grid.dt
+        for k, s in enumerate(self.sources):
+            full = _cached_samples(s, dt, self.grid.num_t, self.sample_cache)
+            if full is not None:
+                buf[lo:hi, k] = full[lo:hi]
+                continue
+            col = buf[:, k]
+            for n in range(lo, hi):
+                col[n] = s.value(n * dt)
+        self.sampled_to = hi
+        return lo, hi
+
+    @property
+    def src_values(self) -> np.ndarray:
+        """Every source sample (solver_fdtd.py:378-385), rows 1..num_t-1 (row 0 unused)."""
+        self.sample_sources(self.grid.num_t)
+        return self.src_buffer
+
+
+def _cached_samples(src, dt: float, num_t: int, cache: dict | None):
+    """Shared samples of equal sources across the plans of one sweep
+    (``cache`` owned by the caller, e.g. one ``run_points`` call), for the two
+    frozen pulse types the reference defines; None when not cacheable."""
+    if cache is None or type(src) not in (core.SechPulse, core.GaussianPulse):
+        return None
+    key = (type(src), src, dt, num_t)  # frozen dataclasses: hashable by value
+    col = cache.get(key)
+    if col is None:
+        col = np.zeros(num_t)
+        for n in range(1, num_t):
+            col[n] = src.value(n * dt)
         col.flags.writeable = False
         cache[key] = col
     return col
 
 
+def _first_at_or_after(end: float, dx: float, lo: int, hi: int, offset: float = 0.0) -> int:
+    """Smallest m in [lo, hi] with fl((m - offset) * dx) >= end (hi if none):
+    the count of grid positions (np.arange(..) - offset) * dx below ``end``,
+    which is what ``searchsorted(region_ends, x, side='right')`` compares
+    (solver_fdtd.py:245-266).  The positions are monotone in m, so a guess
+    from the division is corrected by exact comparisons of the same products."""
+    def x(m):
+        return (float(m) - offset) * dx
+
+    if not end > x(lo):
+        return lo
+    m = min(max(int(math.ceil(end / dx + offset)), lo), hi)
+    while m > lo and x(m - 1) >= end:
+        m -= 1
+    while m < hi and x(m) < end:
+        m += 1
+    return m
+
+
 def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_cache: dict | None = None) -> SolverPlan:
     """Validate and precompute a run (``FdtdSolver.__init__`` minus state
     arrays, same checks in the same order).  ``sample_cache``: see
-    :func:`_source_samples`."""
+    :func:`_cached_samples`.
+
+    Nothing here is O(Nx) for the default zero initial fields: the region
+    table comes from the region ends by exact comparisons of the reference's
+    own grid positions (no per-cell map), and the source samples are taken
+    when the run needs them."""
     problems = core.scenario_validate(device, scenario)
     if problems:
         raise mblight.ValidationError(problems)
@@ -286,22 +367,42 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
     seed = core.DEFAULT_SEED if seed is None else int(seed)
     nx, dt, dx = grid.num_x, grid.dt, grid.dx
 
-    e_init = np.ascontiguousarray(scenario.ic_e_field.build(nx, seed), dtype=float)
-    h_init = np.zeros(nx + 1)
-    h_init[0:nx] = scenario.ic_h_field.build(nx, seed + 1)
+    # initial fields (solver_fdtd.py:235-239): the IC objects' own build(),
+    # called here -- so a failing IC raises before any work -- except for the
+    # constant IC, whose array is only made when it is read
+    ic_e, ic_h = scenario.ic_e_field, scenario.ic_h_field
+    consts = [type(ic) is core.ConstantField for ic in (ic_e, ic_h)]
+    e_init = None if consts[0] else np.ascontiguousarray(ic_e.build(nx, seed), dtype=float)
+    h_init = None
+    if not consts[1]:
+        h_init = np.zeros(nx + 1)
+        h_init[0:nx] = ic_h.build(nx, seed + 1)
+    fields_zero = ((ic_e.value == 0.0) if consts[0] else not e_init.any()) and \
+                  ((ic_h.value == 0.0) if consts[1] else not h_init.any())
 
     mats = [core.get_material(r.material_id) for r in device.regions]
     n_reg = len(device.regions)
-    ends = np.array([r.x_end for r in device.regions])
+    ends = [float(r.x_end) for r in device.regions]
     if nx > 1:
-        cell_region = np.minimum(np.searchsorted(ends, np.arange(nx) * dx, side="right"), n_reg - 1)
-        x_h = (np.arange(1, nx) - 0.5) * dx
-        h_region = np.minimum(np.searchsorted(ends, x_h, side="right"), n_reg - 1)
         coeffs = [get_fdtd_constants(m, dt, dx) for m in mats]
+        # cell m is in region min(#{ends <= m dx}, n_reg - 1), H node m in
+        # min(#{ends <= (m - 1/2) dx}, n_reg - 1) (searchsorted side='right',
+        # solver_fdtd.py:245-266): region r >= 1 starts at the first position
+        # not below ends[r - 1]
+        e_start = [0] + [_first_at_or_after(ends[r - 1], dx, 0, nx) for r in range(1, n_reg)]
+        h_start = [1] + [_first_at_or_after(ends[r - 1], dx, 1, nx, 0.5) for r in range(1, n_reg)]
+        h_start = [min(v, nx) for v in h_start]
     else:
-        cell_region = np.zeros(1, dtype=np.int64)
-        h_region = np.zeros(0, dtype=np.int64)
         coeffs = [CellCoefficients(1.0, 0.0, 0.0, m.overlap_factor, 0.0, m.qm) for m in mats]
+        e_start = [0] + [nx] * (n_reg - 1)
+        h_start = [1] + [1] * (n_reg - 1)
+
+    def region_of_cell(m):
+        r = 0
+        for q in range(1, n_reg):
+            if e_start[q] <= m:
+                r = q
+        return r
 
     # quantum materials (one constant set per distinct qm material)
     qm_ids: list[str] = []
@@ -317,8 +418,8 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
     levels = qm_list[0].levels if qm_list else 0
 
     regions = RegionTable(
-        e_start=np.searchsorted(cell_region, np.arange(n_reg), side="left").astype(np.int64),
-        h_start=(np.searchsorted(h_region, np.arange(n_reg), side="left") + 1).astype(np.int64),
+        e_start=np.array(e_start, dtype=np.int64),
+        h_start=np.array(h_start, dtype=np.int64),
         coef_a=np.array([c.a_prime for c in coeffs]),
         coef_bg=np.array([c.b_prime * c.gamma for c in coeffs]),
         coef_bdx=np.array([c.b_prime * c.inv_dx for c in coeffs]),
@@ -326,19 +427,17 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
         qm_index=qm_index,
     )
 
-    # maximal runs of cells in one region (solver_fdtd.py:276-285), vectorised
-    cuts = (np.flatnonzero(cell_region[1:] != cell_region[:-1]) + 1).tolist()
+    # maximal runs of cells in one region (solver_fdtd.py:276-285): the
+    # non-empty regions, in order
     groups = []
-    for start, stop in zip([0] + cuts, cuts + [nx]):
-        r = int(cell_region[start])
-        if qm_index[r] >= 0:
+    bounds = e_start + [nx]
+    for r in range(n_reg):
+        start, stop = bounds[r], bounds[r + 1]
+        if stop > start and qm_index[r] >= 0:
             groups.append((start, stop, int(qm_index[r])))
 
     srcs = list(scenario.sources)
     cells = [0 if nx == 1 else int(math.floor(s.position / dx + 0.5)) for s in srcs]
-    values = np.zeros((grid.num_t, len(srcs)))
-    for k, s in enumerate(srcs):
-        values[:, k] = _source_samples(s, dt, grid.num_t, sample_cache)
 
     plans = [RecordPlan(rec, grid) for rec in scenario.records]
     names = [p.record.name for p in plans]
@@ -347,7 +446,7 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
 
     boundary = None
     if nx > 1:
-        left, right = mats[int(cell_region[0])], mats[int(cell_region[-1])]
+        left, right = mats[region_of_cell(0)], mats[region_of_cell(nx - 1)]
         boundary = (
             (1.0 - math.sqrt(device.bc_left.reflectivity), left.light_speed * dt / dx,
              math.sqrt(left.permeability / left.permittivity)),
@@ -357,10 +456,10 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
 
     rho0 = np.asarray(scenario.rho_init.matrix(), dtype=complex) if levels else None
     return SolverPlan(
-        grid=grid, seed=seed, stepper=stepper, levels=levels, e_init=e_init, h_init=h_init,
+        grid=grid, seed=seed, stepper=stepper, levels=levels,
         regions=regions, qm=qm_list, groups=groups, rho_init=rho0,
         src_cells=np.array(cells, dtype=np.int64),
         src_hard=np.array([1 if s.kind == "hard" else 0 for s in srcs], dtype=np.int32),
-        src_values=values, plans=plans, boundary=boundary, materials=mats,
-        fields_zero=not (e_init.any() or h_init.any()),
+        plans=plans, boundary=boundary, materials=mats, fields_zero=bool(fields_zero),
+        sources=srcs, ic_fields=(ic_e, ic_h), _e_init=e_init, _h_init=h_init, sample_cache=sample_cache,
     )

@@ -32,6 +32,8 @@ SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
 RECORD_HBM_BYTES = 4 << 30
 # ... sized so one segment's rows take about this much device memory
 RECORD_SEGMENT_BYTES = 512 << 20
+# first run segment when the sources are sampled during the run (see _run_on)
+FIRST_FEED = 1024
 
 
 class GpuFdtdSolver:
@@ -70,6 +72,7 @@ class GpuFdtdSolver:
         self.persistent = None if persistent is None else bool(persistent)
         self.record_segment = record_segment
         self._streamed = False
+        self._fed = 0
         self.results = None
         self.launches = 0
         self.kernel_ms = None
@@ -99,10 +102,11 @@ class GpuFdtdSolver:
         s.own_lo, s.own_hi = own if own is not None else (s.win_lo, s.win_hi)
         return s
 
-    def open_handle(self, win=None, own=None, records=True) -> native.Handle:
+    def open_handle(self, win=None, own=None, records=True, stream_sources=False) -> native.Handle:
         """Create the device solver and upload everything but the initial state
         (``records=False``: a handle that never samples, e.g. the edge-strip
-        solvers of a slab)."""
+        solvers of a slab; ``stream_sources``: the source samples not taken
+        yet are uploaded by the run as it samples them, see _run_on)."""
         plan = self.plan
         h = native.Handle(self._grid_struct(win, own))
         rt = plan.regions
@@ -116,9 +120,19 @@ class GpuFdtdSolver:
         if plan.boundary is not None:
             (wl, cl, zl), (wr, cr, zr) = plan.boundary
             h.call("mbg_set_boundary", wl, cl, zl, wr, cr, zr)
-        cells, hard, vals = native.i64(plan.src_cells), native.i32(plan.src_hard), native.f64(plan.src_values)
-        h.call("mbg_set_sources", len(cells), native.ptr(cells, native._i64p), native.ptr(hard, native._i32p),
-               native.ptr(vals))
+        cells, hard = native.i64(plan.src_cells), native.i32(plan.src_hard)
+        if stream_sources and len(cells) and plan.sampled_to < self.grid.num_t:
+            h.call("mbg_set_sources", len(cells), native.ptr(cells, native._i64p), native.ptr(hard, native._i32p),
+                   None)
+            if plan.sampled_to > 1:  # rows sampled before the run
+                buf = plan.src_buffer
+                h.call("mbg_set_source_rows", 1, plan.sampled_to, native.ptr(buf[1:plan.sampled_to]))
+            self._fed = plan.sampled_to
+        else:
+            vals = native.f64(plan.src_values)
+            h.call("mbg_set_sources", len(cells), native.ptr(cells, native._i64p), native.ptr(hard, native._i32p),
+                   native.ptr(vals))
+            self._fed = self.grid.num_t
         ps = plan.plans if records else []
         q = native.i32([p.quantity for p in ps])
         cell = native.i64([-1 if p.cell is None else p.cell for p in ps])
@@ -254,7 +268,7 @@ class GpuFdtdSolver:
         if self._ran:
             raise SolverError("run() may only be called once per solver instance")
         self._ran = True
-        h = self.open_handle()
+        h = self.open_handle(stream_sources=True)
         try:
             self.upload_initial_state(h)
             self._run_on(h)
@@ -287,14 +301,23 @@ class GpuFdtdSolver:
         chunk = poll_every if split is None else max(1, split)
         if segment:
             chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
+        # sources not sampled yet: sampled (Source.value, as the reference's
+        # loop calls it per step) for the next segment while the device steps
+        # the current one; segments grow from FIRST_FEED steps by 4x
+        feed = self._fed < num_t
+        cap = FIRST_FEED if feed and split is None else chunk
         n = 1
         since = 0
         h.call("mbg_event_begin")
         while n < num_t:
-            cnt = min(chunk, num_t - n)
+            cnt = min(chunk, cap, num_t - n)
+            self._feed_sources(h, n + cnt)
             h.call("mbg_advance", n, cnt)
             n += cnt
             since += cnt
+            if feed and n < num_t:
+                cap = min(4 * cap, chunk)
+                self._feed_sources(h, n + min(chunk, cap, num_t - n))
             if split is not None and (n - 1) % split == 0:
                 h.call("mbg_invariants_accumulate")
             if segment:
@@ -317,6 +340,16 @@ class GpuFdtdSolver:
         launches = C.c_int64(0)
         h.call("mbg_launch_count", C.byref(launches))
         self.launches = int(launches.value)
+
+    def _feed_sources(self, h, hi):
+        """Sample the sources up to row ``hi`` (exclusive) and queue those rows
+        for the device (stream-ordered before the next launch)."""
+        if hi <= self._fed:
+            return
+        lo, hi = self.plan.sample_sources(hi)
+        if hi > lo:
+            h.call("mbg_set_source_rows", lo, hi, native.ptr(self.plan.src_buffer[lo:hi]))
+        self._fed = hi
 
     # -- invariant monitor (solver_fdtd.py:306-308, 425-440) ---------------------
 

@@ -223,7 +223,8 @@ def test_registration_into_the_reference_registry():
 
 def test_source_sample_cache_is_per_sweep():
     """Without a caller-owned cache every plan samples its sources with
-    Source.value again, as the reference does on every run."""
+    Source.value again, as the reference does on every run; subclasses are
+    never shared."""
     from paper_2005_05412_b200 import plan as P
 
     calls = []
@@ -234,11 +235,53 @@ def test_source_sample_cache_is_per_sweep():
             return super().value(t)
 
     src = Counting("c", 0.0, "soft", 1.0, 2e14, 5.0, 1e15)
-    P._source_samples(src, 1e-17, 50)
-    P._source_samples(src, 1e-17, 50)
-    assert len(calls) == 98  # subclasses are never memoised
+    assert P._cached_samples(src, 1e-17, 50, {}) is None
+    assert P._cached_samples(mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15), 1e-17, 50, None) is None
     cache = {}
     s2 = mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15)
-    a = P._source_samples(s2, 1e-17, 50, cache)
-    b = P._source_samples(mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15), 1e-17, 50, cache)
+    a = P._cached_samples(s2, 1e-17, 50, cache)
+    b = P._cached_samples(mb.SechPulse("s", 0.0, "soft", 1.0, 2e14, 5.0, 1e15), 1e-17, 50, cache)
     assert a is b and len(cache) == 1
+    assert np.array_equal(a[1:], [s2.value(n * 1e-17) for n in range(1, 50)])
+
+
+def test_sources_sampled_in_segments_equal_one_pass():
+    """The run samples its sources segment by segment (plan.sample_sources);
+    any split gives the table a single pass of Source.value gives."""
+    dev, sce, stepper = build_case("vacuum_sources")
+    full = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan.src_values.copy()
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    assert plan.sampled_to == 1
+    n = plan.grid.num_t
+    for hi in (2, 7, 7, n // 3, n // 2 + 1, n + 5):
+        lo, got_hi = plan.sample_sources(hi)
+        assert got_hi == min(hi, n) and plan.sampled_to == got_hi
+    assert np.array_equal(plan.src_buffer, full)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_region_starts_equal_searchsorted_maps(seed):
+    """The region table is derived from the region ends alone; it equals the
+    first-cell-of-each-region of the reference's per-cell maps
+    (searchsorted(ends, m dx, 'right') and (m - 1/2) dx for H nodes,
+    solver_fdtd.py:245-266), also for ends that fall exactly on a cell or
+    node position and for empty regions."""
+    from paper_2005_05412_b200 import plan as P
+
+    rng = np.random.default_rng(seed)
+    nx = int(rng.integers(2, 3000))
+    dx = float(rng.uniform(1e-11, 1e-8))
+    n_reg = int(rng.integers(1, 9))
+    cuts = []
+    for _ in range(n_reg - 1):
+        m = int(rng.integers(0, nx + 2))
+        kind = rng.integers(0, 3)
+        cuts.append(m * dx if kind == 0 else (m - 0.5) * dx if kind == 1 else float(rng.uniform(0, nx * dx)))
+    ends = sorted(cuts) + [(nx - 1) * dx]
+    cell_region = np.minimum(np.searchsorted(ends, np.arange(nx) * dx, side="right"), n_reg - 1)
+    h_region = np.minimum(np.searchsorted(ends, (np.arange(1, nx) - 0.5) * dx, side="right"), n_reg - 1)
+    want_e = np.searchsorted(cell_region, np.arange(n_reg), side="left")
+    want_h = np.searchsorted(h_region, np.arange(n_reg), side="left") + 1
+    got_e = [0] + [P._first_at_or_after(ends[r - 1], dx, 0, nx) for r in range(1, n_reg)]
+    got_h = [1] + [P._first_at_or_after(ends[r - 1], dx, 1, nx, 0.5) for r in range(1, n_reg)]
+    assert list(want_e) == got_e and list(want_h) == got_h

@@ -19,6 +19,14 @@ for name in ["sit_hard_whole", "multi_material", "vacuum_sources", "rand3_split"
     dev, sce = build(mb)
     gpu.GpuFdtdSolver(dev, sce, stepper=stepper, monitor_invariants=True).run()
     print("ok", name, flush=True)
+# the persistent wavefront kernel (cross-CTA acquire/release tickets): forced
+# on small two-level runs, with and without records inside the wave
+from paper_2005_05412_b200 import configs  # noqa: E402
+for exact in (False, True):
+    mb.clear_material_library()
+    dev, sce = configs.cfg1(mb, nx=4096, steps=600, cells=(100, 2000, 4000))
+    gpu.GpuFdtdSolver(dev, sce, persistent=True, tile_steps=16, exact=exact, monitor_invariants=True).run()
+    print("ok persistent", "exact" if exact else "fast", flush=True)
 mb.clear_material_library()
 build, stepper = CASES["multi_material"]
 dev, sce = build(mb)
