@@ -156,18 +156,22 @@ __device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const 
     // of a x (a x v1) is -|a|^2 y1, and the x and z components share one factor:
     //   x2 = x1 - 2az s,  z2 = z1 + 2ax s,  s = (nh y1 + cy) / D,
     //   y2 = ((nh^2 - |a|^2) y1 + 2 nh cy) / D,  cy = az x1 - ax z1.
-    // 23 FP64 operations (30 in the g / dot-product grouping), tolerance-level
+    // With D = nh^2 + |a|^2 the y row simplifies to y2 = 2 nh s - y1:
+    //   2 nh (nh y1 + cy)/D - y1 = ((nh^2 - |a|^2) y1 + 2 nh cy)/D,
+    // so with t = 2 s (exact doubling) all three rows are one FMA each:
+    //   x2 = x1 - az t,  z2 = z1 + ax t,  y2 = nh t - y1.
+    // 20 FP64 operations (30 in the g / dot-product grouping), tolerance-level
     // against the reference (not bitwise).
-    const double ax = q.ax_s * e, ax2 = r.axs2 * e, az = q.az_c;
+    const double ax = q.ax_s * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
     const double nh = fma(-0.5, qq, r.c1h);
     const double iD = rcp_ge1(fma(nh, nh, qq));
-    const double nm = fma(nh, nh, -qq);  // D cos
     const double cy = fma(az, x1, -(ax * z1));
     const double in = iD * fma(nh, y1, cy);
-    x = fma(-r.az2x, in, x1);
-    y = iD * fma(nm, y1, (nh + nh) * cy);
-    z = fma(ax2, in, z1);
+    const double t = in + in;
+    x = fma(-az, t, x1);
+    y = fma(nh, t, -y1);
+    z = fma(ax, t, z1);
     return x - x0;
 }
 #define MBG_BLOCH_REAL bloch_cell_real_frame

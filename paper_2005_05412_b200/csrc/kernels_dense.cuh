@@ -122,6 +122,16 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             B[wre(N, i, j)] = A[wre(N, i, j)] * q.coh[i * N + j];
             B[wim(N, i, j)] = A[wim(N, i, j)] * q.coh[i * N + j];
         }
+#ifndef MBG_SPLIT_FENCE
+#define MBG_SPLIT_FENCE 1
+#endif
+    // compiler fences (bit 0 here, bit 1 per congruence row): the state words
+    // are re-read from shared memory where used again instead of being held
+    // (spilled) across the inversion.  Measured on cfg4: none 4.77e9, bit 0
+    // 4.92e9 (1588 -> 324 spill bytes), bits 0+1 4.54e9 (120 spill bytes),
+    // bit 1 alone 4.54e9 -- the per-row fence costs more schedule freedom than
+    // the spills it removes
+    if constexpr ((MBG_SPLIT_FENCE & 1) != 0) asm volatile("" ::: "memory");
     if constexpr (RA) {
         // Real Hamiltonian and dipole (fast variant): A real symmetric, so
         // U = (I + iA)^-1 (I - iA) = (2P - I) - 2iAP with P = (I + A^2)^-1 real
@@ -232,6 +242,7 @@ __device__ __forceinline__ double congruence(const DenseQm<N> &q, VA &A, VB &B, 
     double acc_p = 0.0;  // raw[i]: row i's diagonal before the second half relaxation
 #pragma unroll
     for (int i = 0; i < N; ++i) {
+        if constexpr ((MBG_SPLIT_FENCE & 2) != 0) asm volatile("" ::: "memory");  // per row
         double tr[N], ti[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -334,51 +345,53 @@ __device__ __forceinline__ void master_rhs(const Rk4Qm<N> &q, const double *hr, 
         }
 }
 
-// Same derivative for N >= 4 with H = h0 - E mu formed row by row on the fly
-// (a full H would hold 2N^2 doubles in registers).  The empty asm on the
-// field value keeps the compiler from caching H rows across (i, j) pairs.
-// The source is the stage state A + c K (c = 0: A alone), formed while it is
-// read into registers, so no stage buffer is kept in shared memory; dst may
-// be K itself (every source word is read before the first write).
+// Same derivative for N >= 4 from H = h0 - E mu held packed (Hermitian: N
+// real diagonal words, re/im of the upper pairs; RH: the imaginary words are
+// zero and never read), formed once per cell step for the four stages.  The
+// stage source A + c K is formed while it is read into registers, so no stage
+// buffer is kept in shared memory; dst may be K itself (every source word is
+// read before the first write).  The fence keeps the compiler from holding
+// shared-memory words in registers across stages (N = 6: 4456 -> 0 spill bytes).
+template <int N, bool RH, class VH>
+__device__ __forceinline__ void herm_h(VH &hp, int i, int j, double &re, double &im) {
+    if constexpr (RH) {
+        re = i == j ? hp[i] : (i < j ? hp[wre(N, i, j)] : hp[wre(N, j, i)]);
+        im = 0.0;
+    } else {
+        herm<N>(hp, i, j, re, im);
+    }
+}
+
 template <int N, bool RH, class VA, class VK, class VD>
-__device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA &a0, VK &k0, double c, VD &dst) {
+__device__ __forceinline__ void master_rhs_packed(const Rk4Qm<N> &q, RegVec<N * N> &hp, VA &a0, VK &k0, double c,
+                                                  VD &dst) {
     constexpr double kInvHbar = 1.0 / 1.054571817e-34;
-    // one pass over the shared-memory state into registers: every entry is used 2N times
+    asm volatile("" ::: "memory");
     RegVec<N * N> src;
 #pragma unroll
     for (int w = 0; w < N * N; ++w) src[w] = c == 0.0 ? a0[w] : mad(c, k0[w], a0[w]);  // c is a literal per call
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        double ei = e;
-        asm volatile("" : "+d"(ei));
-        double ar[N], ai[N];  // row i of H
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            ar[k] = mad(-ei, q.mu_re[i * N + k], q.h0_re[i * N + k]);
-            ai[k] = RH ? 0.0 : mad(-ei, q.mu_im[i * N + k], q.h0_im[i * N + k]);
-        }
+    for (int i = 0; i < N; ++i)
 #pragma unroll
         for (int j = i; j < N; ++j) {
-            double ej = ei;
-            asm volatile("" : "+d"(ej));
+            // [H, S]_ij = sum_k H_ik S_kj - S_ik H_kj
             double cr = 0.0, ci = 0.0;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                double sr, si, tr, ti;
+                double sr, si, tr, ti, ar, ai, br, bi;
                 herm<N>(src, k, j, sr, si);
                 herm<N>(src, i, k, tr, ti);
-                // H_kj = conj(H_jk) (H is exactly Hermitian)
-                const double br = mad(-ej, q.mu_re[j * N + k], q.h0_re[j * N + k]);
+                herm_h<N, RH>(hp, i, k, ar, ai);
+                herm_h<N, RH>(hp, k, j, br, bi);
                 if constexpr (RH) {
-                    cr += mad(ar[k], sr, -(tr * br));
-                    ci += mad(ar[k], si, -(ti * br));
+                    cr += mad(ar, sr, -(tr * br));
+                    ci += mad(ar, si, -(ti * br));
                 } else {
-                    const double bi = -mad(-ej, q.mu_im[j * N + k], q.h0_im[j * N + k]);
-                    cr += mad(ar[k], sr, -(ai[k] * si)) - mad(tr, br, -(ti * bi));
-                    ci += mad(ar[k], si, ai[k] * sr) - mad(tr, bi, ti * br);
+                    cr += mad(ar, sr, -(ai * si)) - mad(tr, br, -(ti * bi));
+                    ci += mad(ar, si, ai * sr) - mad(tr, bi, ti * br);
                 }
             }
-            double dr = ci * kInvHbar, di = -cr * kInvHbar;
+            const double dr = ci * kInvHbar, di = -cr * kInvHbar;
             if (i == j) {
                 double acc = q.popm[i * N] * src[0];
 #pragma unroll
@@ -390,7 +403,6 @@ __device__ __forceinline__ void master_rhs_rows(const Rk4Qm<N> &q, double e, VA 
                 dst[wim(N, i, j)] = mad(-g, src[wim(N, i, j)], di);
             }
         }
-    }
 }
 
 // Classical RK4 on the packed state.  Registers (N <= 3): explicit stage
@@ -410,16 +422,27 @@ __device__ __forceinline__ double rk4_cell(const Rk4Qm<N> &q, double e, VA &A, V
     }
     const double dt = q.dt;
     if constexpr (N >= 4) {
-        master_rhs_rows<N, RH>(q, e, A, K, 0.0, K);  // k1
+        RegVec<NW> hp;  // H = h0 - E mu, packed (_kernels.py:270-272)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            hp[i] = mad(-e, q.mu_re[i * N + i], q.h0_re[i * N + i]);
+#pragma unroll
+            for (int j = i + 1; j < N; ++j) {
+                hp[wre(N, i, j)] = mad(-e, q.mu_re[i * N + j], q.h0_re[i * N + j]);
+                hp[wim(N, i, j)] = RH ? 0.0 : mad(-e, q.mu_im[i * N + j], q.h0_im[i * N + j]);
+            }
+        }
+        master_rhs_packed<N, RH>(q, hp, A, K, 0.0, K);  // k1
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = K[w];
-        master_rhs_rows<N, RH>(q, e, A, K, 0.5 * dt, K);  // k2
+        master_rhs_packed<N, RH>(q, hp, A, K, 0.5 * dt, K);  // k2
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
-        master_rhs_rows<N, RH>(q, e, A, K, 0.5 * dt, K);  // k3
+        master_rhs_packed<N, RH>(q, hp, A, K, 0.5 * dt, K);  // k3
 #pragma unroll
         for (int w = 0; w < NW; ++w) Acc[w] = mad(2.0, K[w], Acc[w]);
-        master_rhs_rows<N, RH>(q, e, A, K, dt, K);  // k4
+        master_rhs_packed<N, RH>(q, hp, A, K, dt, K);  // k4
+        asm volatile("" ::: "memory");
     } else {
         master_rhs<N, RH>(q, hr, hi, A, K);  // k1
 #pragma unroll

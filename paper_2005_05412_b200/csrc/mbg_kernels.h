@@ -41,6 +41,9 @@ constexpr int kBlochCtaTile = kBlochWarpsPerBlock * kBlochTile;
 // (six-level RK4: 96-cell tiles, so two CTAs of three shared-memory state
 // buffers fit an SM)
 __host__ __device__ constexpr int dense_tile_width(int n, bool rk4) {
+#ifdef MBG_DENSE_TW
+    if (n >= 5 && !rk4) return MBG_DENSE_TW;  // tuning builds
+#endif
     return n <= 3 ? 256 : (rk4 && n == 6 ? 96 : (n <= 6 ? 128 : 64));
 }
 __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <= 3 ? 2 : 1; }
