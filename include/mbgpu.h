@@ -57,6 +57,8 @@ extern "C" {
 
 #define MBG_MAX_REGIONS 128
 #define MBG_MAX_QM 4
+/* distinct quantum materials of one mbg_batch_points call (constant sets in device memory) */
+#define MBG_MAX_BATCH_QM 65536
 #define MBG_MAX_SOURCES 32
 #define MBG_MAX_RECORDS 64
 #define MBG_MAX_LEVELS 8

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/mbgpu.h"
@@ -263,9 +264,10 @@ cudaError_t launch_dense_n(const mbg_solver *s, const Launch &L, long long tiles
 // real-operator choice as the step kernels)
 template <int N>
 cudaError_t batch_dense_n(const mbg_solver *s, int B, const BatchRecs &R, const double *e_seq, double *state,
-                          const int *medium) {
+                          const int *medium, std::vector<void *> &dev_bufs) {
     const bool rk4 = s->g.stepper == MBG_STEPPER_RK4;
     auto go = [&](auto *P, auto fill, auto real) {
+        using Q = std::remove_cv_t<std::remove_pointer_t<decltype(P->qm)>>;
         P->B = B;
         P->num_t = s->g.num_t;
         P->e_seq = e_seq;
@@ -274,12 +276,23 @@ cudaError_t batch_dense_n(const mbg_solver *s, int B, const BatchRecs &R, const 
         P->R = R;
         P->n_qm = (int)s->qm.size();
         P->real_a = P->n_qm > 0 && !disable_real_a();
+        std::vector<Q> host(P->n_qm);
         for (int q = 0; q < P->n_qm; ++q) {
-            fill(P->qm[q], s->qm[q]);
+            fill(host[q], s->qm[q]);
             P->real_a &= real(s->qm[q]) ? 1 : 0;
         }
-        cudaError_t e = s->g.exact ? exact::launch_batch_dense(N, rk4, P, B, s->stream)
-                                   : fast::launch_batch_dense(N, rk4, P, B, s->stream);
+        Q *dq = nullptr;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&dq), sizeof(Q) * host.size(), s->stream);
+        if (e == cudaSuccess) {
+            dev_bufs.push_back(dq);
+            e = cudaMemcpyAsync(dq, host.data(), sizeof(Q) * host.size(), cudaMemcpyHostToDevice, s->stream);
+            // the pageable source must stay valid until the copy is staged
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+        }
+        P->qm = dq;
+        if (e == cudaSuccess)
+            e = s->g.exact ? exact::launch_batch_dense(N, rk4, P, B, s->stream)
+                           : fast::launch_batch_dense(N, rk4, P, B, s->stream);
         delete P;
         return e;
     };
@@ -573,7 +586,7 @@ static QmHost &qm_slot(mbg_solver *s, int q) {
 }
 
 int mbg_set_qm_bloch(mbg_solver *s, int32_t q, const double *c) {
-    if (!s || q < 0 || q >= kMaxQm || !c) return fail(s, MBG_E_ARG, "bad qm index");
+    if (!s || q < 0 || q >= MBG_MAX_BATCH_QM || !c) return fail(s, MBG_E_ARG, "bad qm index");
     if (!s->bloch) return fail(s, MBG_E_STATE, "solver is not a two-level splitting solver");
     QmHost &h = qm_slot(s, q);
     h.n = 2;
@@ -608,7 +621,7 @@ static bool pol_ok(int n, int npol, const int32_t *pi, const int32_t *pj, int nd
 int mbg_set_qm_dense(mbg_solver *s, int32_t q, const double *pop, const double *coh, const double *bc,
                      const double *bf, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
                      int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
-    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support at most MBG_MAX_QM quantum materials");
+    if (!s || q < 0 || q >= MBG_MAX_BATCH_QM) return fail(s, MBG_E_UNSUPPORTED, "qm index beyond MBG_MAX_BATCH_QM");
     const int n = s->g.levels;
     if (s->bloch || s->g.stepper != MBG_STEPPER_SPLITTING || n < 3)
         return fail(s, MBG_E_STATE, "solver is not an N>=3 splitting solver");
@@ -627,7 +640,7 @@ int mbg_set_qm_dense(mbg_solver *s, int32_t q, const double *pop, const double *
 int mbg_set_qm_rk4(mbg_solver *s, int32_t q, const double *h0, const double *mu, const double *popm,
                    const double *deph, int32_t npol, const int32_t *pi, const int32_t *pj, const double *pv,
                    int32_t ndpol, const int32_t *pdi, const double *pdv, double pol_factor) {
-    if (!s || q < 0 || q >= kMaxDenseQm) return fail(s, MBG_E_UNSUPPORTED, "dense kernels support at most MBG_MAX_QM quantum materials");
+    if (!s || q < 0 || q >= MBG_MAX_BATCH_QM) return fail(s, MBG_E_UNSUPPORTED, "qm index beyond MBG_MAX_BATCH_QM");
     const int n = s->g.levels;
     if (s->g.stepper != MBG_STEPPER_RK4 || n < 2) return fail(s, MBG_E_STATE, "solver is not an RK4 solver");
     if (!pol_ok(n, npol, pi, pj, ndpol, pdi)) return fail(s, MBG_E_ARG, "bad dipole index list");
@@ -1233,11 +1246,13 @@ int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const doub
     double *d_e = nullptr, *d_s = nullptr;
     int *d_m = nullptr;
     std::vector<double *> bufs;
+    std::vector<void *> qbufs;  // device constant sets of the media
     auto release = [&]() {
         dfree(s->stream, d_e);
         dfree(s->stream, d_s);
         dfree(s->stream, d_m);
         for (double *p : bufs) dfree(s->stream, p);
+        for (void *p : qbufs) dfree(s->stream, p);
         cudaStreamSynchronize(s->stream);
     };
     auto step = [&](cudaError_t e, const char *what) {
@@ -1275,21 +1290,40 @@ int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const doub
             P.R = R;
             P.n_qm = nq;
             P.real_dipole = 1;
+            std::vector<BlochQm> hq(nq);
+            std::vector<BlochReal> hr(nq);
             for (int q = 0; q < nq; ++q) {
-                std::memcpy(&P.qm[q], s->qm[q].bloch, sizeof(BlochQm));
-                P.rq[q] = bloch_real(P.qm[q]);
-                P.real_dipole &= real_dipole(P.qm[q]) ? 1 : 0;
+                std::memcpy(&hq[q], s->qm[q].bloch, sizeof(BlochQm));
+                hr[q] = bloch_real(hq[q]);
+                P.real_dipole &= real_dipole(hq[q]) ? 1 : 0;
             }
-            e = s->g.exact ? exact::launch_batch_bloch(P, s->stream) : fast::launch_batch_bloch(P, s->stream);
+            BlochQm *dq = nullptr;
+            BlochReal *dr = nullptr;
+            e = cudaMallocAsync(reinterpret_cast<void **>(&dq), sizeof(BlochQm) * nq, s->stream);
+            if (e == cudaSuccess) {
+                qbufs.push_back(dq);
+                e = cudaMallocAsync(reinterpret_cast<void **>(&dr), sizeof(BlochReal) * nq, s->stream);
+            }
+            if (e == cudaSuccess) {
+                qbufs.push_back(dr);
+                e = cudaMemcpyAsync(dq, hq.data(), sizeof(BlochQm) * nq, cudaMemcpyHostToDevice, s->stream);
+            }
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(dr, hr.data(), sizeof(BlochReal) * nq, cudaMemcpyHostToDevice, s->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);  // host vectors die at scope end
+            P.qm = dq;
+            P.rq = dr;
+            if (e == cudaSuccess)
+                e = s->g.exact ? exact::launch_batch_bloch(P, s->stream) : fast::launch_batch_bloch(P, s->stream);
         } else {
             switch (N) {
-                case 2: e = batch_dense_n<2>(s, B, R, d_e, d_s, d_m); break;
-                case 3: e = batch_dense_n<3>(s, B, R, d_e, d_s, d_m); break;
-                case 4: e = batch_dense_n<4>(s, B, R, d_e, d_s, d_m); break;
-                case 5: e = batch_dense_n<5>(s, B, R, d_e, d_s, d_m); break;
-                case 6: e = batch_dense_n<6>(s, B, R, d_e, d_s, d_m); break;
-                case 7: e = batch_dense_n<7>(s, B, R, d_e, d_s, d_m); break;
-                case 8: e = batch_dense_n<8>(s, B, R, d_e, d_s, d_m); break;
+                case 2: e = batch_dense_n<2>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 3: e = batch_dense_n<3>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 4: e = batch_dense_n<4>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 5: e = batch_dense_n<5>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 6: e = batch_dense_n<6>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 7: e = batch_dense_n<7>(s, B, R, d_e, d_s, d_m, qbufs); break;
+                case 8: e = batch_dense_n<8>(s, B, R, d_e, d_s, d_m, qbufs); break;
                 default: e = cudaErrorInvalidValue;
             }
         }

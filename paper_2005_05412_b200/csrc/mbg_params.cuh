@@ -190,6 +190,10 @@ struct BatchRecs {
     double *re[kMaxRecords], *im[kMaxRecords];
 };
 
+// The media of a batch live in device global memory (one constant set per
+// distinct medium, up to MBG_MAX_BATCH_QM): a sweep over detunings or rates
+// is not capped by the 32 KB parameter block; each thread reads its own set
+// (L1-cached, one set per system).
 template <int N, class Q>
 struct BatchParams {
     int B;
@@ -198,7 +202,7 @@ struct BatchParams {
     double *state;        // [words][B], in and out
     const int *medium;    // [B] constant-set index
     int n_qm, real_a;
-    Q qm[kMaxDenseQm];
+    const Q *qm;          // [n_qm], device
     BatchRecs R;
 };
 
@@ -209,8 +213,8 @@ struct BlochBatchParams {
     double *state;  // Bloch (x, y, z) planes
     const int *medium;
     int n_qm, real_dipole;
-    BlochQm qm[kMaxQm];
-    BlochReal rq[kMaxQm];
+    const BlochQm *qm;    // [n_qm], device
+    const BlochReal *rq;  // [n_qm], device
     BatchRecs R;
 };
 

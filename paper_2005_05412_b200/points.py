@@ -11,7 +11,10 @@ solver.  ``run_points(problems)`` returns, per problem, the list of
 ``Result`` objects ``GpuFdtdSolver(device, scenario).run()`` returns.
 
 All problems share the stepper, the number of levels, the time grid and the
-record layout; they may use up to MBG_MAX_QM distinct quantum materials.
+record layout; their quantum materials are free (up to MBG_MAX_BATCH_QM
+distinct ones: the constant sets live in device memory, one per medium).
+Equal sources are sampled once per call (a caller-owned sample cache, see
+plan._cached_samples).
 """
 
 from __future__ import annotations
@@ -76,7 +79,9 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
     problems = list(problems)
     if not problems:
         return []
-    plans = [build_plan(dev, sce, stepper, seed) for dev, sce in problems]
+    t_host = time.perf_counter()
+    cache: dict = {}  # equal pulses of the sweep sampled once
+    plans = [build_plan(dev, sce, stepper, seed, cache) for dev, sce in problems]
     p0 = plans[0]
     if any(p.grid.num_x != 1 for p in plans):
         raise ValueError("run_points takes single-grid-point scenarios (num_gridpoints == 1)")
@@ -88,15 +93,16 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
             raise ValueError("run_points: every problem needs the same levels and time grid")
         if [(r.quantity, r.i, r.j, r.every) for r in p.plans] != layout:
             raise ValueError("run_points: every problem needs the same record layout")
-    # distinct quantum materials (by id) -> constant sets of the handle
-    media, medium = [], []
+    # distinct quantum materials (by id) -> constant sets of the batch
+    media, index, medium = [], {}, []
     for p in plans:
         mid = p.materials[0].id
-        if mid not in [m for m, _ in media]:
-            media.append((mid, p.qm[0]))
-        medium.append([m for m, _ in media].index(mid))
-    if len(media) > native.MAX_QM:
-        raise ValueError(f"run_points supports at most {native.MAX_QM} distinct quantum materials")
+        if mid not in index:
+            index[mid] = len(media)
+            media.append(p.qm[0])
+        medium.append(index[mid])
+    if len(media) > native.MAX_BATCH_QM:
+        raise ValueError(f"run_points supports at most {native.MAX_BATCH_QM} distinct quantum materials")
 
     B, nt = len(plans), p0.grid.num_t
     e_seq = np.empty((nt, B))
@@ -112,7 +118,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
     solver = GpuFdtdSolver(*problems[0], stepper=stepper, exact=exact, gpu=gpu, seed=seed)
     h = solver.open_handle()
     try:
-        for q, (_, qc) in enumerate(media):
+        for q, qc in enumerate(media):
             solver._upload_qm(h, q, qc)
         dens = [r for r, pl in enumerate(p0.plans) if pl.quantity in (MBG_Q_D, MBG_Q_INV)]
         outs = {r: (np.zeros((B, p0.plans[r].rows)),
@@ -127,6 +133,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
         med = native.i32(medium)
         es = np.ascontiguousarray(e_seq)
         t0 = time.perf_counter()
+        LAST_RUN["host_setup_s"] = t0 - t_host  # plans, media, field sequences, handle
         h.call("mbg_batch_points", B, native.ptr(med, native._i32p), native.ptr(es), native.ptr(state),
                len(dens), native.ptr(q, native._i32p), native.ptr(ii, native._i32p), native.ptr(jj, native._i32p),
                native.ptr(ev, native._i64p), C.cast(re_ptrs, C.POINTER(native._dp)),
@@ -136,6 +143,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
     finally:
         h.close()
 
+    t1 = time.perf_counter()
     results = []
     for b, p in enumerate(plans):
         res = []
@@ -152,6 +160,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
                 data = col[:, None]
             res.append(pl.to_result(p.grid, data))
         results.append(res)
+    LAST_RUN["host_results_s"] = time.perf_counter() - t1
     return results
 
 

@@ -25,20 +25,29 @@ from test_gpu_points import _song  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--systems", type=int, default=4096)
 ap.add_argument("--stepper", default="splitting")
+ap.add_argument("--sweep", choices=("pulse", "media"), default="pulse",
+                help="pulse: one three-level medium, pulse amplitudes swept; media: distinct two-level "
+                     "media (T2 swept), one shared pulse")
 a = ap.parse_args()
 mb.clear_material_library()
-scales = np.linspace(0.1, 3.0, a.systems)
-problems = [_song(scale=float(s)) for s in scales]
+if a.sweep == "pulse":
+    scales = np.linspace(0.1, 3.0, a.systems)
+    problems = [_song(scale=float(s)) for s in scales]
+else:
+    from test_gpu_points import _two_level  # noqa: E402
+
+    problems = [_two_level(t2=float(t), tag=f"m{i}") for i, t in enumerate(np.linspace(2e11, 5e12, a.systems))]
 run_points(problems[:8], stepper=a.stepper)  # warm (module load)
 t0 = time.perf_counter()
 res = run_points(problems, stepper=a.stepper)
 t_batch = time.perf_counter() - t0
-steps = 9999
+steps = problems[0][1].num_timesteps - 1 if problems[0][1].num_timesteps else 9999
 sol = gpu.GpuFdtdSolver(*problems[0], stepper=a.stepper)
 t0 = time.perf_counter()
 sol.run()
 t_one = time.perf_counter() - t0
 t_dev = LAST_RUN["batch_s"]
-print(f"{a.systems} systems x {steps} steps ({a.stepper}): run_points {t_batch:.3f} s (native batch call "
-      f"{t_dev:.3f} s -> {a.systems * steps / t_dev:.3e} system-steps/s; the rest is the host plan of every "
-      f"system); one single-point solver run {t_one:.3f} s ({steps / t_one:.3e} steps/s)")
+print(f"{a.systems} systems x {steps} steps ({a.stepper}, {a.sweep} sweep): run_points {t_batch:.3f} s = host "
+      f"setup {LAST_RUN['host_setup_s']:.3f} s (plans, media, field sequences) + native batch call {t_dev:.3f} s "
+      f"({a.systems * steps / t_dev:.3e} system-steps/s) + results {LAST_RUN['host_results_s']:.3f} s; "
+      f"one single-point solver run {t_one:.3f} s ({steps / t_one:.3e} steps/s)")
