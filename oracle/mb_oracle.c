@@ -470,4 +470,35 @@ int64_t orc_run(orc_problem *P)
     return 0;
 }
 
-int orc_version(void) { return 1; }
+/* One density step of M consecutive cells of quantum material q with the
+ * constants of P (TEST DOUBLE support: the CPU slab twin of the gloo
+ * multi-process tests steps its window's quantum runs with this, so an
+ * N-level slab rank runs the very arithmetic of orc_run).  state/next in the
+ * group layout of P->stepper (Bloch planes of M, or dense AoS complex). */
+void orc_density_step(const orc_problem *P, int32_t q, const double *state, double *next, int64_t M,
+                      const double *e_vals, double *p_out)
+{
+#ifdef _OPENMP
+    if (P->threads > 0) omp_set_num_threads(P->threads);
+#endif
+    if (M <= 0) return;
+    if (is_bloch(P)) {
+        orc_bloch_step(state, next, M, e_vals, P->qm_bloch + 14 * q, P->qm_pol_factor[q], p_out);
+        return;
+    }
+    const int n = P->levels, nn = n * n;
+    const cplx *pv = (const cplx *)(P->qm_pol_v + 2 * ORC_MAXP * q);
+    if (P->stepper == 0)
+        orc_split_step((const cplx *)state, (cplx *)next, M, n, e_vals, P->qm_pop_half + nn * q,
+                       P->qm_coh_half + nn * q, (const cplx *)(P->qm_b_const + 2 * nn * q),
+                       (const cplx *)(P->qm_b_field + 2 * nn * q), P->qm_npol[q], P->qm_pol_i + ORC_MAXP * q,
+                       P->qm_pol_j + ORC_MAXP * q, pv, P->qm_ndpol[q], P->qm_pol_di + ORC_MAXN * q,
+                       P->qm_pol_dv + ORC_MAXN * q, P->qm_pol_factor[q], p_out);
+    else
+        orc_rk4_step((const cplx *)state, (cplx *)next, M, n, e_vals, P->dt, (const cplx *)(P->qm_h0 + 2 * nn * q),
+                     (const cplx *)(P->qm_mu + 2 * nn * q), P->qm_pop_matrix + nn * q, P->qm_deph + nn * q,
+                     P->qm_npol[q], P->qm_pol_i + ORC_MAXP * q, P->qm_pol_j + ORC_MAXP * q, pv, P->qm_ndpol[q],
+                     P->qm_pol_di + ORC_MAXN * q, P->qm_pol_dv + ORC_MAXN * q, P->qm_pol_factor[q], p_out);
+}
+
+int orc_version(void) { return 2; }

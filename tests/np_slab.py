@@ -1,13 +1,15 @@
 """CPU twin of one native slab (TEST DOUBLE for the gloo multi-process tests).
 
 Implements the interface ``slabs.run_slab_rank`` drives (sample / advance /
-pack_into / unpack_from / poll / records / close) on numpy arrays, for
-two-level (Bloch) and classical media, so the multi-rank host logic --
-partitioning, ghost windows, neighbour exchange, record assembly, the
-non-finite reduction -- is exercised on CPU with torch.distributed/gloo.
-Each step restates solver_fdtd.py:53-66, _kernels.py:200-232 and
-solver_fdtd.py:362-426 on the window with elementwise IEEE numpy
-arithmetic in the reference's evaluation order (bit-exact vs the oracle).
+pack_into / unpack_from / poll / records / close) on numpy arrays, so the
+multi-rank host logic -- partitioning, ghost windows, neighbour exchange,
+record assembly, the non-finite reduction -- is exercised on CPU with
+torch.distributed/gloo.  Each step restates solver_fdtd.py:53-66 and
+solver_fdtd.py:362-426 on the window with elementwise IEEE numpy arithmetic
+in the reference's evaluation order; the density step is _kernels.py:200-232
+in numpy for two-level splitting, and for N-level splitting / RK4 the
+oracle's own per-cell step (oracle/mb_oracle.c orc_density_step) on the
+window's quantum runs -- so every rank is bit-exact against the oracle.
 """
 
 import numpy as np
@@ -18,9 +20,8 @@ from paper_2005_05412_b200.plan import NONFINITE_CHECK_EVERY
 class NumpySlab:
     def __init__(self, solver, slab):
         plan = solver.plan
-        if plan.levels not in (0, 2) or plan.stepper != "splitting":
-            raise NotImplementedError("the CPU slab twin covers two-level splitting and classical media")
         self.plan, self.slab = plan, slab
+        self.dense = plan.levels > 2 or (plan.levels == 2 and plan.stepper == "rk4")
         g = plan.grid
         self.nx, self.num_t = g.num_x, g.num_t
         lo, hi = slab.win_lo, slab.win_hi
@@ -38,14 +39,33 @@ class NumpySlab:
         self.x = np.zeros(self.n)
         self.y = np.zeros(self.n)
         self.z = np.zeros(self.n)
-        if plan.levels:
+        if self.dense:
+            import oracle as orc
+
+            n = plan.levels
+            self.orc = orc.OracleRun(plan, threads=1, step_limit=1)  # the plan's constants (nothing is run)
+            self.rho = np.zeros((self.n, n, n), complex)
+            self.rho[self.qm] = plan.rho_init
+            # contiguous runs of quantum cells of one material
+            self.runs = []
+            l = 0
+            while l < self.n:
+                if not self.qm[l]:
+                    l += 1
+                    continue
+                r = l
+                while r < self.n and self.qm[r] and self.qi[r] == self.qi[l]:
+                    r += 1
+                self.runs.append((l, r, int(self.qi[l])))
+                l = r
+        elif plan.levels:
             w = plan.rho_init_packed()
             self.x[self.qm], self.y[self.qm], self.z[self.qm] = w
             keys = ("kz", "cz", "fxy", "ax_c", "ax_s", "ay_c", "ay_s", "az_c", "az_s", "a0_c", "a0_s",
                     "mu_x", "mu_y", "mu_z")
             self.bc = {k: np.array([q.bloch[k] for q in plan.qm])[self.qi] for k in keys}
             self.pf = np.array([q.pol_factor for q in plan.qm])[self.qi]
-        self.words = 5
+        self.words = 2 + 2 * plan.levels ** 2 if self.dense else 5
         self.bad = -1
         self.rec = []
         for p in plan.plans:
@@ -78,6 +98,17 @@ class NumpySlab:
         self.z = np.where(m, z3, z0)
         return np.where(m, p, 0.0)
 
+    def _dense_step(self, e):
+        p = np.zeros(self.n)
+        for l0, l1, q in self.runs:
+            st = np.ascontiguousarray(self.rho[l0:l1]).view(np.float64).reshape(-1)
+            nxt = np.zeros_like(st)
+            pp = np.zeros(l1 - l0)
+            self.orc.density_step(q, st, nxt, np.ascontiguousarray(e[l0:l1]), pp)
+            self.rho[l0:l1] = nxt.view(np.complex128).reshape(l1 - l0, *self.rho.shape[1:])
+            p[l0:l1] = pp
+        return p
+
     def _owned(self):
         return slice(self.slab.own_lo - self.lo, self.slab.own_hi - self.lo)
 
@@ -92,6 +123,14 @@ class NumpySlab:
                 v = self.e
             elif p.record.quantity == "h":
                 v = self.h[:self.n]
+            elif self.dense:
+                i, j = p.i, p.j
+                if p.record.quantity == "inv":  # _kernels.py:391-392
+                    v = np.where(self.qm, self.rho[:, 1, 1].real - self.rho[:, 0, 0].real, 0.0)
+                elif i == j:
+                    v = np.where(self.qm, self.rho[:, i, i].real, 0.0)
+                else:
+                    v = np.where(self.qm, self.rho[:, i, j], 0.0)
             elif p.record.quantity == "inv":
                 v = np.where(self.qm, -self.z, 0.0)
             else:
@@ -123,7 +162,10 @@ class NumpySlab:
             upd[0] = False  # no left neighbour inside the window
             l = np.nonzero(upd)[0]
             hn[l] = h_old[l] + self.ch[l] * (e_old[l] - e_old[l - 1])
-            p = self._bloch(e_old) if plan.levels else np.zeros(self.n)
+            if self.dense:
+                p = self._dense_step(e_old)
+            else:
+                p = self._bloch(e_old) if plan.levels else np.zeros(self.n)
             if nx > 1:
                 en = self.a * e_old - self.bg * p + self.bdx * (hn[1:] - hn[:-1])
             else:
@@ -151,6 +193,8 @@ class NumpySlab:
     def _pack(self, cell0, count):
         l0 = cell0 - self.lo
         sl = slice(l0, l0 + count)
+        if self.dense:
+            return np.concatenate([self.e[sl], self.h[sl], np.ascontiguousarray(self.rho[sl]).view(np.float64).reshape(-1)])
         return np.concatenate([self.e[sl], self.h[sl], self.x[sl], self.y[sl], self.z[sl]])
 
     def pack_into(self, cell0, count, tensor):
@@ -160,6 +204,12 @@ class NumpySlab:
         buf = tensor.numpy()
         l0 = cell0 - self.lo
         sl = slice(l0, l0 + count)
+        if self.dense:
+            self.e[sl] = buf[:count]
+            self.h[sl] = buf[count:2 * count]
+            rest = buf[2 * count:self.words * count]
+            self.rho[sl] = rest.view(np.complex128).reshape(count, *self.rho.shape[1:])
+            return
         for k, arr in enumerate((self.e, self.h, self.x, self.y, self.z)):
             arr[sl] = buf[k * count:(k + 1) * count]
 

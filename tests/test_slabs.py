@@ -80,7 +80,11 @@ def _worker(rank, world, port, case, k, period, out_path):
 
 
 @pytest.mark.parametrize("world,k,period,case", [(2, 7, None, "sit_hard_whole"), (3, 16, 16, "multi_material"),
-                                                 (2, 5, None, "vacuum_sources"), (2, 3, 7, "sit_hard_whole")])
+                                                 (2, 5, None, "vacuum_sources"), (2, 3, 7, "sit_hard_whole"),
+                                                 # N-level splitting and RK4 ranks (the density step of the
+                                                 # twin is the oracle's own, on each window's quantum runs)
+                                                 (2, 4, 12, "rand3_split"), (3, 4, 8, "rand6_split"),
+                                                 (2, 4, 9, "rand4_rk4"), (2, 6, None, "rand2_rk4")])
 def test_gloo_ranks_match_oracle_bitwise(world, k, period, case):
     """period: steps between exchanges (ghost width); None = m chunks of k."""
     import oracle as orc
