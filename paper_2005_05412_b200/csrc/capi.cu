@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -69,6 +70,7 @@ struct mbg_solver {
     int src_hard[kMaxSources] = {};
     double *src_values = nullptr;
     double *src_host = nullptr;  // pinned staging of the sample table (rows uploaded as they are sampled)
+    size_t src_host_bytes = 0;
     std::vector<Rec> recs;
     unsigned long long *bad = nullptr;
     unsigned long long *inv = nullptr;  // running invariant keys (mbg_invariants_accumulate)
@@ -414,6 +416,42 @@ void dfree(cudaStream_t st, void *p) {
     if (p) cudaFreeAsync(p, st);
 }
 
+// Pinned host staging (the streamed source table) from a process-wide free
+// list: page-locking costs milliseconds per call, and every run of the same
+// workload asks for the same size again.  Blocks are returned only after the
+// owner's stream has drained (mbg_destroy / mbg_set_sources synchronise first).
+struct PinnedBlock {
+    void *p;
+    size_t bytes;
+};
+std::mutex g_pinned_mu;
+std::vector<PinnedBlock> g_pinned_free;
+constexpr size_t kPinnedKeep = 64;
+
+cudaError_t pinned_get(double **p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        for (size_t i = 0; i < g_pinned_free.size(); ++i) {
+            if (g_pinned_free[i].bytes == bytes) {
+                *p = static_cast<double *>(g_pinned_free[i].p);
+                g_pinned_free.erase(g_pinned_free.begin() + (long)i);
+                return cudaSuccess;
+            }
+        }
+    }
+    return cudaMallocHost(reinterpret_cast<void **>(p), bytes);
+}
+
+void pinned_put(void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (g_pinned_free.size() >= kPinnedKeep) {
+        cudaFreeHost(g_pinned_free.front().p);
+        g_pinned_free.erase(g_pinned_free.begin());
+    }
+    g_pinned_free.push_back({p, bytes});
+}
+
 bool window_ok(const mbg_grid *g) {
     return g->win_lo >= 0 && g->win_hi <= g->num_x && g->win_lo < g->win_hi && g->own_lo >= g->win_lo &&
            g->own_hi <= g->win_hi && g->own_lo < g->own_hi;
@@ -521,7 +559,7 @@ void mbg_destroy(mbg_solver *s) {
         dfree(st, r.im);
     }
     if (st) cudaStreamSynchronize(st);
-    if (s->src_host) cudaFreeHost(s->src_host);
+    if (s->src_host) pinned_put(s->src_host, s->src_host_bytes);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     for (cudaEvent_t e : s->marks)
@@ -669,7 +707,7 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
     cudaSetDevice(s->g.device);
     if (s->src_host) {
         CK(cudaStreamSynchronize(s->stream));  // no copy out of the old staging in flight
-        cudaFreeHost(s->src_host);
+        pinned_put(s->src_host, s->src_host_bytes);
         s->src_host = nullptr;
     }
     dfree(s->stream, s->src_values);
@@ -689,7 +727,8 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
         } else {
             // rows arrive later (mbg_set_source_rows) through a pinned staging copy
             CK(cudaMemsetAsync(s->src_values, 0, bytes, s->stream));
-            CK(cudaMallocHost(reinterpret_cast<void **>(&s->src_host), bytes));
+            CK(pinned_get(&s->src_host, bytes));
+            s->src_host_bytes = bytes;
         }
     }
     return MBG_OK;

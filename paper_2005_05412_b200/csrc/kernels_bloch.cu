@@ -129,14 +129,18 @@ __device__ __forceinline__ double bloch_cell_real(const BlochQm &q, const BlochR
 }
 
 #if !(defined(MBG_EXACT) && MBG_EXACT)
-// 1/d for d >= 1/4 (a quarter of the Cayley denominator (1+q-u)^2 + 4u >= 1):
-// hardware seed refined by one cubically convergent step r + r(e + e^2),
-// e = 1 - d r (seed error 2^-22 -> below double rounding), no special cases
-__device__ __forceinline__ double rcp_ge1(double d) {
+// 2/d for d >= 1/4 (a quarter of the Cayley denominator (1+q-u)^2 + 4u >= 1):
+// hardware seed r ~ 1/d refined by one cubically convergent step
+// 2r + 2r(e + e^2), e = 1 - d r (seed error 2^-22 -> below double rounding),
+// no special cases.  The doubling 2r is exact and done on the integer pipe
+// (exponent + 1 of the normal seed, 1/4 <= ... so r <= 4), so the factor 2
+// of the rotation costs no FP64 operation.
+__device__ __forceinline__ double rcp2_ge1(double d) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
     const double e = fma(-d, r, 1.0);
-    return fma(r, fma(e, e, e), r);
+    const double r2 = __hiloint2double(__double2hiint(r) + (1 << 20), __double2loint(r));
+    return fma(r2, fma(e, e, e), r2);
 }
 
 // Fast variant of bloch_cell_real on the relaxed-frame state (BlochFrame):
@@ -159,16 +163,16 @@ __device__ __forceinline__ double bloch_cell_real_frame(const BlochQm &q, const 
     // With D = nh^2 + |a|^2 the y row simplifies to y2 = 2 nh s - y1:
     //   2 nh (nh y1 + cy)/D - y1 = ((nh^2 - |a|^2) y1 + 2 nh cy)/D,
     // so with t = 2 s (exact doubling) all three rows are one FMA each:
-    //   x2 = x1 - az t,  z2 = z1 + ax t,  y2 = nh t - y1.
-    // 20 FP64 operations (30 in the g / dot-product grouping), tolerance-level
+    //   x2 = x1 - az t,  z2 = z1 + ax t,  y2 = nh t - y1,
+    // and 2/D comes out of the reciprocal's refinement (rcp2_ge1).
+    // 18 FP64 operations (30 in the g / dot-product grouping), tolerance-level
     // against the reference (not bitwise).
     const double ax = q.ax_s * e, az = q.az_c;
     const double qq = fma(ax, ax, r.az2);
     const double nh = fma(-0.5, qq, r.c1h);
-    const double iD = rcp_ge1(fma(nh, nh, qq));
+    const double i2D = rcp2_ge1(fma(nh, nh, qq));
     const double cy = fma(az, x1, -(ax * z1));
-    const double in = iD * fma(nh, y1, cy);
-    const double t = in + in;
+    const double t = i2D * fma(nh, y1, cy);
     x = fma(-az, t, x1);
     y = fma(nh, t, -y1);
     z = fma(ax, t, z1);

@@ -44,9 +44,17 @@ __host__ __device__ constexpr int dense_tile_width(int n, bool rk4) {
 #ifdef MBG_DENSE_TW
     if (n >= 5 && !rk4) return MBG_DENSE_TW;  // tuning builds
 #endif
+#ifdef MBG_DENSE_TW3
+    if (n == 3 && !rk4) return MBG_DENSE_TW3;
+#endif
     return n <= 3 ? 256 : (rk4 && n == 6 ? 96 : (n <= 6 ? 128 : 64));
 }
-__host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) { return n <= 3 ? 2 : 1; }
+__host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) {
+#ifdef MBG_DENSE_MINB3
+    if (n == 3 && !rk4) return MBG_DENSE_MINB3;
+#endif
+    return n <= 3 ? 2 : 1;
+}
 
 // One persistent launch of the two-level kernel over many fused chunks
 // (non-windowed solvers): work items (chunk c, tile t) are claimed in

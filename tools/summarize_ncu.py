@@ -74,7 +74,6 @@ def summarize(rep, key):
     out = {
         "kernel": d.get("Kernel Name", "?")[:120],
         "duration_us": f(d, "gpu__time_duration.sum") * (1000.0 if dur_unit == "ms" else 1.0),
-        "dram_read_MB": dram_r, "dram_write_MB": dram_w,
         "registers": f(d, "launch__registers_per_thread"),
         "fp64_pipe_pct": f(d, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "warps_active_pct": f(d, "sm__warps_active.avg.pct_of_peak_sustained_active"),
@@ -85,8 +84,9 @@ def summarize(rep, key):
     rows = ncu_csv(rep, "raw")
     units = dict(zip(rows[0], rows[1]))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    out["dram_bytes_per_launch"] = dram_r * scale.get(units.get("dram__bytes_read.sum"), 1) + \
-        dram_w * scale.get(units.get("dram__bytes_write.sum"), 1)
+    out["dram_read_bytes"] = dram_r * scale.get(units.get("dram__bytes_read.sum"), 1)
+    out["dram_write_bytes"] = dram_w * scale.get(units.get("dram__bytes_write.sum"), 1)
+    out["dram_bytes_per_launch"] = out["dram_read_bytes"] + out["dram_write_bytes"]
     tu = units.get("gpu__time_duration.sum", "ns")
     out["duration_us"] = f(d, "gpu__time_duration.sum") * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
                                                            "msecond": 1e3, "nsecond": 1e-3}.get(tu, 1.0)
