@@ -357,6 +357,11 @@ def run_mine(args, world, rank, local):
             "fp64_flops_per_cell_step": round(executed, 1),
             "fp64_pipe_pct": nc.get("fp64_pipe_pct"),
             "achieved_tflops": executed * cells_per_launch / (per_launch_ms * 1e-3) / 1e12,
+            # FP64 instructions issued per second against the pipe's peak
+            # instruction rate (one DFMA = 2 flops of the measured peak): the
+            # pipe utilisation, independent of how few operations a step takes
+            "fp64_instr_frac": (nc.get("fp64_instr_per_cell_step") or 0.0) * cells_per_launch
+                               / (per_launch_ms * 1e-3) / (peak_fp64 * 1e12 / 2.0),
             "note": ("frac counts SURVEY 8(d)'s algorithmic flops (the reference's 82-flop Bloch step); the fast "
                      "kernel evaluates the same step in fewer FP64 operations (Rodrigues-form rotation, fused "
                      "relaxations), so frac can exceed 1 -- the executed figures and the FP64 pipe share "
