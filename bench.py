@@ -510,6 +510,8 @@ SAMPLE_STEPS = 128
 def scaling_samples(world, rank, device, backend=None, reps=3):
     """north_star's multi-GPU targets as bounded samples:
 
+    * ``cfg3_strong``: BASELINE configs[2] (three levels, 2^23 cells) split
+      over the ranks (north_star: "run on 1/2/4 GPUs"), as cfg4 below;
     * ``cfg4_strong``: BASELINE configs[3] (six levels, 2^24 cells) split over
       the ranks, SAMPLE_STEPS steps per run with the halo exchange every
       period; efficiency = rate_N / (N * rate_1), rate_1 timed on rank 0
@@ -550,6 +552,13 @@ def scaling_samples(world, rank, device, backend=None, reps=3):
         return box[0]
 
     out = {"steps_per_run": SAMPLE_STEPS, "runs": reps}
+    # BASELINE configs[2]: cfg3 (three levels, 2^23 cells) over the ranks
+    rate, k, period, overlap = timed(lambda: configs.cfg3(mb), world)
+    one = single(lambda: configs.cfg3(mb))
+    out["cfg3_strong"] = {"num_x": 1 << 23, "levels": 3, "ranks": world, "tile_steps": k,
+                          "exchange_period": period if world > 1 else None, "overlap": overlap,
+                          "value": rate, "unit": UNIT, "single_gpu_value": one if world > 1 else rate,
+                          "efficiency": rate / (world * one) if one else 1.0}
     rate, k, period, overlap = timed(lambda: configs.cfg4(mb), world)
     one = single(lambda: configs.cfg4(mb))
     out["cfg4_strong"] = {"num_x": 1 << 24, "levels": 6, "ranks": world, "tile_steps": k,

@@ -128,6 +128,24 @@ def test_native_slabs_on_one_gpu_match_single_domain(case, count, period):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,count,period", [("rand6_split", 3, None), ("rand3_split", 2, 29), ("cfg4_r14", 4, None),
+                                               ("rand4_rk4", 2, None), ("four_media", 3, 24)])
+def test_edge_strips_match_single_domain(case, count, period):
+    """Exchange overlapped with the slab's advance (EdgeStrips: the sent cells
+    computed ahead by strip solvers on a side stream, the default under NCCL
+    for N-level / RK4 slabs): bit-identical to the single domain."""
+    dev, sce, stepper = build_case(case)
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case(case)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
+    got = slabs.run_slabs_local(solver, count, period, overlap=True)
+    for a, b in zip(ref, got):
+        assert a.name == b.name and a.data.shape == b.data.shape
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
+
+
 def _nccl_single(fn):
     """Run fn() inside a one-rank NCCL process group (the only NCCL shape one GPU allows)."""
     import torch
@@ -180,7 +198,7 @@ def test_bench_rank_prints_a_line(capsys, monkeypatch):
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
 
 
-def _gpu_worker(rank, world, port, case, period, out_path):
+def _gpu_worker(rank, world, port, case, period, out_path, overlap=None):
     """One rank of a gloo run whose slabs all live on cuda:0 (native kernels,
     host-staged exchanges: the ranks only meet on the host)."""
     sys.path.insert(0, str(ROOT))
@@ -204,7 +222,7 @@ def _gpu_worker(rank, world, port, case, period, out_path):
         dev, sce = build(mbw)
         torch.cuda.set_device(0)
         solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper, gpu=0)
-        recs = sl.run_slab_rank(solver, world, rank, torch.device("cuda", 0), period=period)
+        recs = sl.run_slab_rank(solver, world, rank, torch.device("cuda", 0), period=period, overlap=overlap)
         if rank == 0:
             np.savez(out_path, *[r.data for r in recs])
     finally:
@@ -212,9 +230,13 @@ def _gpu_worker(rank, world, port, case, period, out_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,case,period", [(2, "multi_material", None), (3, "cfg2_r16", None),
-                                               (2, "rand3_split", None), (2, "vacuum_sources", 100)])
-def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period):
+@pytest.mark.parametrize("world,case,period,overlap", [(2, "multi_material", None, None), (3, "cfg2_r16", None, None),
+                                                       (2, "rand3_split", None, None),
+                                                       (2, "vacuum_sources", 100, None),
+                                                       # the NCCL default for N-level slabs, edge strips on a
+                                                       # side stream, here through the host-staged transport
+                                                       (2, "rand6_split", None, True), (3, "rand3_split", 29, True)])
+def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period, overlap):
     """run_slab_rank across processes with the native slab kernels: the
     TorchTransport exchange plan, pack/unpack on the adopted stream, scan-flag
     reduction and record gather, bit-identical to the single-domain run."""
@@ -222,7 +244,7 @@ def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period):
     ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "recs.npz")
-        mp.spawn(_gpu_worker, args=(world, _free_port(), case, period, out), nprocs=world, join=True)
+        mp.spawn(_gpu_worker, args=(world, _free_port(), case, period, out, overlap), nprocs=world, join=True)
         got = np.load(out)
         for r, a in enumerate(ref):
             have = got[f"arr_{r}"]
