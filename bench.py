@@ -127,7 +127,9 @@ def algorithmic_per_cell(plan):
     n = plan.levels
     sn = plan.state_words
     b = 32 + fq * 16 * sn
-    if n == 2:
+    if plan.stepper == "rk4" and n >= 2:
+        fn = rk4_flops(n, int(np.count_nonzero(plan.qm[0].pol_v)), len(plan.qm[0].pol_di))
+    elif n == 2:
         fn = 82
     elif n == 0:
         fn = 9
@@ -140,6 +142,19 @@ def algorithmic_per_cell(plan):
         fn += 8 * n ** 3 + 4 * n * n * (n + 1) + 10 * nnz_off + 3 * nnz_d + 1 + 9
     f = 9 + fq * (fn - 9)
     return b, f, fq
+
+
+def rk4_flops(n, nnz_off, nnz_d):
+    """Algorithmic flops of one RK4 cell-update in the reference's loop
+    (_kernels.py:256-332; complex mul 6, add 2, real x complex 2), plus the
+    FDTD's 9: H = h0 - E mu (4 n^2); per stage the commutator
+    -i/hbar sum_k (H_ik S_kj - S_ik H_kj) (n^2 (14 n + 4)), dephasing
+    (4 n (n - 1)) and population transfer (4 n^2); three stage states
+    (4 n^2 each); the RK4 combination (14 n^2); symmetrisation (2 n (n - 1));
+    the polarisation trace (10 per off-diagonal dipole, 3 per diagonal)."""
+    stage = n * n * (14 * n + 4) + 4 * n * (n - 1) + 4 * n * n
+    return (4 * n * n + 4 * stage + 3 * 4 * n * n + 14 * n * n + 2 * n * (n - 1) + 10 * nnz_off + 3 * nnz_d + 1
+            + 9)
 
 
 def measured_hbm_gbs():
@@ -428,10 +443,13 @@ def n_level_samples(local, peak_tflops, chunks=16):
     from paper_2005_05412_b200 import configs, native
 
     out = {}
-    for name, n in (("cfg3", 3), ("cfg4", 6)):
+    # the splitting headline media, and the six-level medium under the RK4
+    # stepper (the second registered solver)
+    for name, cfg, n, stepper in (("cfg3", "cfg3", 3, "splitting"), ("cfg4", "cfg4", 6, "splitting"),
+                                  ("cfg4_rk4", "cfg4", 6, "rk4")):
         mb.clear_material_library()
-        dev, sce = getattr(configs, name)(mb)
-        sol = gpu.GpuFdtdSolver(dev, sce, gpu=local)
+        dev, sce = getattr(configs, cfg)(mb)
+        sol = gpu.GpuFdtdSolver(dev, sce, gpu=local, stepper=stepper)
         h = sol.open_handle()
         sol.upload_initial_state(h)
         k = C.c_int32(0)
@@ -448,7 +466,8 @@ def n_level_samples(local, peak_tflops, chunks=16):
         h.close()
         rate = sol.grid.num_x * steps / (ms.value * 1e-3)
         b, f, fq = algorithmic_per_cell(sol.plan)
-        out[name] = {"levels": n, "num_x": sol.grid.num_x, "tile_steps": k.value, "sampled_steps": steps,
+        out[name] = {"levels": n, "stepper": stepper, "num_x": sol.grid.num_x, "tile_steps": k.value,
+                     "sampled_steps": steps,
                      "of_steps": sol.grid.num_t - 1, "value": rate, "unit": UNIT,
                      "algorithmic_flops_per_cell_update": f, "achieved_tflops": rate * f / 1e12,
                      "fp64_peak_tflops": peak_tflops, "frac": rate * f / 1e12 / peak_tflops,

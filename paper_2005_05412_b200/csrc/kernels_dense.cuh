@@ -556,7 +556,11 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     double *col = sm + 6 * W + threadIdx.x;  // per-thread state column
     const Launch &L = P.L;
     const long long nx = L.num_x;
-    constexpr bool kLean = !Lay::kRegState && !RK4;  // splitting N >= 5 (RK4 measured 1.5 % slower lean)
+#ifndef MBG_LEAN_MIN_N
+#define MBG_LEAN_MIN_N 5
+#endif
+    // splitting N >= MBG_LEAN_MIN_N (RK4 measured 1.5 % slower lean)
+    constexpr bool kLean = !RK4 && (!Lay::kRegState || N >= MBG_LEAN_MIN_N);
     const int j = threadIdx.x;
     const long long c0 = base + j, l0 = c0 - L.win_lo;
     const auto cell = [&]() { return kLean ? base + j : c0; };
