@@ -143,6 +143,8 @@ Launch base_launch(const mbg_solver *s) {
         L.src_hard[q] = s->src_hard[q];
     }
     L.src_values = s->src_values;
+    L.words = s->words;
+    L.num_t = s->g.num_t;
     L.n_rec = (int)s->recs.size();
     for (int r = 0; r < L.n_rec; ++r) {
         const Rec &R = s->recs[r];
@@ -156,6 +158,7 @@ Launch base_launch(const mbg_solver *s) {
         L.rec_row0[r] = R.row0;
         L.rec_re[r] = R.re;
         L.rec_im[r] = R.im;
+        L.rec_len[r] = R.cap * R.cols;
     }
     L.bad_step = s->bad;
     L.inv = s->inv_every > 0 ? s->inv : nullptr;

@@ -61,6 +61,8 @@ __global__ void sample_kernel(const Launch L, int levels, int bloch, long long s
         } else if (qm >= 0) {
             const double *s = L.s_in + l;
             const long long P = L.plane;
+            MBG_CHK(l, P, "sample s_in");
+            MBG_CHK((long long)(L.words - 1) * P + l, P * L.words, "sample s_in plane");
             if (bloch) {
                 double x, y, z;
                 frame_true(F, qm, s[0], s[P], s[2 * P], x, y, z);
@@ -92,6 +94,7 @@ __global__ void sample_kernel(const Launch L, int levels, int bloch, long long s
                 }
             }
         }
+        MBG_CHK(idx, L.rec_len[r], "sample record");
         L.rec_re[r][idx] = re;
         if (L.rec_im[r]) L.rec_im[r][idx] = im;
     }
@@ -104,6 +107,7 @@ __global__ void halo_kernel(bool pack, double *e, double *h, double *s, long lon
     const long long total = (long long)(2 + words) * count;
     if (t >= total) return;
     const long long w = t / count, c = t % count, l = l0 + c;
+    MBG_CHK(l, plane, "halo cell");  // the host checks the window range (mbg_pack_halo / mbg_unpack_halo)
     double *p = (w == 0) ? e + l : (w == 1) ? h + l : s + (w - 2) * plane + l;
     if (pack)
         buf[t] = *p;

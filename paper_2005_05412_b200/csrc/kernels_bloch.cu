@@ -237,7 +237,9 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
         const long long c = base + i * 32 + lane;
         const long long l = c - L.win_lo;
         const bool in_e = (l >= 0 && l < L.win_n);
+        if (in_e) MBG_CHK(l, L.win_n, "run_tile e_in");
         E[i] = in_e ? ld(K.e_in + l) : 0.0;
+        if (l >= 0 && l <= L.win_n) MBG_CHK(l, L.win_n + 1, "run_tile h_in");
         H[i] = (l >= 0 && l <= L.win_n) ? ld(K.h_in + l) : 0.0;
         const int re = UNI ? re_u : region_of(L.rg.e_start, L.rg.n, c);
         const int rh = UNI ? rh_u : region_of(L.rg.h_start, L.rg.n, c);
@@ -254,6 +256,8 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
         rmask |= (right_edge && c == nx - 1) ? 1u << i : 0u;
         for (int q = 0; q < L.n_src; ++q) smask |= c == L.src_cell[q] ? 1u << i : 0u;
         if (qi[i] >= 0) {
+            MBG_CHK(l, L.plane, "run_tile s_in");
+            MBG_CHK(2 * L.plane + l, L.plane * L.words, "run_tile s_in plane");
             X[i] = ld(K.s_in + l);
             Y[i] = ld(K.s_in + L.plane + l);
             Z[i] = ld(K.s_in + 2 * L.plane + l);
@@ -325,6 +329,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                 const long long c = base + i * 32 + lane;
                 for (int q = 0; q < L.n_src; ++q) {
                     if (c == L.src_cell[q]) {
+                        MBG_CHK(n * L.n_src + q, L.num_t * L.n_src, "run_tile src_values");
                         const double v = L.src_values[n * L.n_src + q];
                         en = L.src_hard[q] ? v : en + v;
                     }
@@ -365,6 +370,7 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
                                     vre = -z;
                             }
                     }
+                    MBG_CHK(idx, L.rec_len[r], "bloch record");
                     L.rec_re[r][idx] = vre;
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
@@ -390,6 +396,8 @@ __device__ __forceinline__ void run_tile(const BlochParams &P, const Chunk &K, l
         const long long c = base + i * 32 + lane;
         if (c < t_lo || c >= t_hi) continue;
         const long long l = c - L.win_lo;
+        MBG_CHK(l, L.win_n, "run_tile e_out");
+        MBG_CHK(l, L.plane, "run_tile s_out");
         K.e_out[l] = E[i];
         K.h_out[l] = H[i];
         if (qi[i] >= 0) {
@@ -450,6 +458,9 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     const long long lane_off = (long long)warp * W + (long long)lane * C;  // this lane's first cell - base
     double E[C], H[C], X[C], Y[C], Z[C];
     const long long l0 = span.base() + lane_off - L.win_lo;
+    MBG_CHK(l0, L.win_n, "interior e_in");
+    MBG_CHK(l0 + C - 1, L.win_n, "interior e_in");
+    if (QM) MBG_CHK(2 * L.plane + l0 + C - 1, L.plane * L.words, "interior s_in");
     if ((l0 & 1) == 0) {  // 16-byte aligned pairs (the usual case: even tile bases, padded planes)
 #pragma unroll
         for (int i = 0; i < C; i += 2) {
@@ -529,6 +540,7 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
                                     vre = -z;
                             }
                     }
+                    MBG_CHK(idx, L.rec_len[r], "bloch record");
                     L.rec_re[r][idx] = vre;
                     if (L.rec_im[r]) L.rec_im[r][idx] = vim;
                 }
@@ -551,6 +563,8 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     const long long first = span.base() + lane_off, t_lo = span.lo(), t_hi = span.hi();
     const long long o0 = first - L.win_lo;
     if (first >= t_lo && first + C <= t_hi && (o0 & 1) == 0) {  // the whole lane, 16-byte pairs
+        MBG_CHK(o0, L.win_n, "interior e_out");
+        MBG_CHK(o0 + C - 1, L.win_n, "interior e_out");
 #pragma unroll
         for (int i = 0; i < C; i += 2) {
             st2(K.e_out + o0 + i, E[i], E[i + 1]);
@@ -567,6 +581,7 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
     for (int i = 0; i < C; ++i) {
         const long long c = first + i;
         if (c < t_lo || c >= t_hi) continue;
+        MBG_CHK(o0 + i, L.win_n, "interior e_out");
         K.e_out[o0 + i] = E[i];
         K.h_out[o0 + i] = H[i];
         if (QM) {
@@ -694,6 +709,7 @@ __device__ bool deps_done(const BlochWave &V, long long item, bool wait) {
     if (c == 0) return true;
     const unsigned *prev = V.done + (c - 1) * V.tiles;
     const long long a = t > 0 ? t - 1 : t, b = t + 1 < V.tiles ? t + 1 : t;
+    MBG_CHK((c - 1) * V.tiles + b, (long long)V.n_chunks * V.tiles, "wave done flags");
     unsigned long long deadline = 0;
     for (;;) {
         const unsigned fa = ld_acquire(prev + a), ft = ld_acquire(prev + t), fb = ld_acquire(prev + b);
@@ -742,6 +758,7 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
         chunk_s = Chunk{V.e[buf],     V.h[buf],  V.s[buf], V.e[buf ^ 1], V.h[buf ^ 1],
                         V.s[buf ^ 1], V.n0 + (long long)c * L.k,
                         c == V.n_chunks - 1 ? V.last_steps : L.k, s_mask, s_check};
+        MBG_CHK(t, V.tiles, "wave items");
         item_range_s = V.items[t];
     };
     if (threadIdx.x == 0) {
@@ -766,6 +783,7 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
             if (threadIdx.x == 0) next_s = atomicAdd(V.ticket, 1u);
             const long long k0 = K.n0 - V.n0;
             if (threadIdx.x < K.steps) {
+                MBG_CHK(k0 + threadIdx.x, (long long)V.n_chunks * L.k, "wave masks");
                 s_mask[threadIdx.x] = V.masks[k0 + threadIdx.x];
                 s_check[threadIdx.x] = V.checks[k0 + threadIdx.x];
             }
@@ -791,6 +809,7 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
             const unsigned done_item = item_s;
             if (V.trace) V.trace[4 * done_item + 2] = global_ns();
             __threadfence();
+            MBG_CHK(done_item, items, "wave release");
             st_release(V.done + done_item, 1u);
             if (!ready) deps_done(V, next, true);
             stage(next);

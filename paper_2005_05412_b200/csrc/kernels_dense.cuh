@@ -566,7 +566,9 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     const auto cell = [&]() { return kLean ? base + j : c0; };
     const auto loc = [&]() { return kLean ? base + j - L.win_lo : l0; };
     const bool in_e = INTERIOR || (l0 >= 0 && l0 < L.win_n && c0 < nx);
+    if (in_e) MBG_CHK(l0, L.win_n, "dense e_in");
     double E = in_e ? L.e_in[l0] : 0.0;
+    if (INTERIOR || (l0 >= 0 && l0 <= L.win_n)) MBG_CHK(l0, L.win_n + 1, "dense h_in");
     double H = (INTERIOR || (l0 >= 0 && l0 <= L.win_n)) ? L.h_in[l0] : 0.0;
     const int re = region_of(L.rg.e_start, L.rg.n, INTERIOR ? base : c0);
     const int rh = region_of(L.rg.h_start, L.rg.n, INTERIOR ? base : c0);
@@ -579,6 +581,8 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     if (qi >= 0) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
+            MBG_CHK(l0, L.plane, "dense s_in");
+            MBG_CHK(w * L.plane + l0, L.plane * L.words, "dense s_in plane");
             const double v = L.s_in[w * L.plane + l0];
             if constexpr (Lay::kRegState) rA[w] = v; else col[w * W] = v;
         }
@@ -628,6 +632,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
             }
             for (int qq = 0; qq < L.n_src; ++qq) {
                 if (c == L.src_cell[qq]) {
+                    MBG_CHK(n * L.n_src + qq, L.num_t * L.n_src, "dense src_values");
                     const double v = L.src_values[n * L.n_src + qq];
                     en = L.src_hard[qq] ? v : en + v;
                 }
@@ -682,6 +687,7 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
                         }
                     }
                 }
+                MBG_CHK(idx, L.rec_len[r], "dense record");
                 L.rec_re[r][idx] = vre;
                 if (L.rec_im[r]) L.rec_im[r][idx] = vim;
             }
@@ -690,6 +696,8 @@ __device__ __forceinline__ void dense_tile(const DenseParams<N, Q> &P, double *s
     const long long c = cell();
     if (c >= t_lo && c < t_hi) {
         const long long l = loc();
+        MBG_CHK(l, L.win_n, "dense e_out");
+        MBG_CHK(l, L.plane, "dense s_out");
         L.e_out[l] = E;
         L.h_out[l] = H;
         if (qi >= 0) {

@@ -8,6 +8,7 @@
 // exists, so any number of solver handles can coexist.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 #include "../../include/mbgpu.h"
 
@@ -70,8 +71,35 @@ struct Launch {
     // running min-eigenvalue key at inv[2], every inv_every steps
     unsigned long long *inv;
     long long inv_every;
+    // extents for the bounds-checked build (MBG_BOUNDS): state words per cell,
+    // time steps of the source table, resident elements of each record
+    int words;
+    long long num_t;
+    long long rec_len[kMaxRecords];
     Regions rg;
 };
+
+// Bounds-checked build (make EXTRA=-DMBG_BOUNDS=1, tools/bounds_check.sh): every
+// global access of the step, sample and halo kernels is checked against the
+// extents of its buffer; a violation prints the site and index and traps (the
+// launch fails with an error, the run raises).  compute-sanitizer is not
+// available on this GPU pool; this is the evidence in its place.
+#if defined(MBG_BOUNDS) && MBG_BOUNDS && defined(__CUDACC__)
+__device__ __noinline__ inline void mbg_oob(const char *site, long long idx, long long len) {
+    printf("MBG_BOUNDS violation: %s index %lld of %lld (block %d thread %d)\n", site, idx, len, (int)blockIdx.x,
+           (int)threadIdx.x);
+    __trap();
+}
+#define MBG_CHK(idx, len, site)                                                   \
+    do {                                                                          \
+        const long long _i = (long long)(idx), _n = (long long)(len);           \
+        if (_i < 0 || _i >= _n) mbg_oob(site, _i, _n);                           \
+    } while (0)
+#else
+#define MBG_CHK(idx, len, site) \
+    do {                        \
+    } while (0)
+#endif
 
 // per-step flags (Launch::check, the persistent launch's check bytes)
 enum : unsigned char { MBG_STEP_SCAN = 1, MBG_STEP_MONITOR = 2 };
