@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 
@@ -41,7 +42,9 @@ class GpuFdtdSolver:
 
     Extra keyword arguments (all optional):
       ``tile_steps`` -- time steps fused per kernel launch (k; default per N),
-      ``exact``      -- disable FMA contraction (bit-exact two-level path),
+      ``exact``      -- disable FMA contraction (bit-exact two-level path);
+                        None (default): the MBG_EXACT environment variable
+                        ("1": exact), so CLI runs can ask for it too,
       ``gpu``        -- CUDA device ordinal,
       ``persistent`` -- two-level / classical runs: True = one persistent
                         wavefront launch per advance, False = one launch per
@@ -55,7 +58,7 @@ class GpuFdtdSolver:
     """
 
     def __init__(self, device, scenario, stepper="splitting", threads=None, seed=None,
-                 monitor_invariants=False, *, tile_steps=None, exact=False, gpu=0, persistent=None,
+                 monitor_invariants=False, *, tile_steps=None, exact=None, gpu=0, persistent=None,
                  record_segment=None):
         self.plan = build_plan(device, scenario, stepper, seed)
         self.device = device
@@ -67,6 +70,8 @@ class GpuFdtdSolver:
         self.monitor_invariants = monitor_invariants
         self.invariant_report = None
         self.tile_steps = tile_steps
+        if exact is None:
+            exact = os.environ.get("MBG_EXACT", "0") == "1"
         self.exact = bool(exact)
         self.gpu = int(gpu)
         self.persistent = None if persistent is None else bool(persistent)
