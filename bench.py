@@ -210,7 +210,9 @@ def run_reference(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(plan, args, None),
+        "data": "synthetic", "config": workload_config(plan, args),
+        "implementation": {"kind": "CPU restatement of the reference loop (oracle/mb_oracle.c), OpenMP",
+                           "threads": threads},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} of {plan.grid.num_t - 1} time steps at full Nx={nx} per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -220,12 +222,14 @@ def run_reference(args, world, rank):
     return 0
 
 
-def workload_config(plan, args, k):
+def workload_config(plan, args):
+    """The workload, identical for both arms (implementation knobs such as the
+    GPU's temporal tile depth go under ``implementation``)."""
     return {
         "workload": "cfg2 (BASELINE configs[1]): two-level SIT, T1=1ns T2=1ps, Strang splitting, "
                     "soft sech source, 3 point records x 4 quantities every 100 steps",
         "num_x": plan.grid.num_x, "time_steps": plan.grid.num_t - 1, "levels": plan.levels,
-        "tile_steps": k, "exact": bool(args.exact),
+        "exact": bool(args.exact),
         "parallelism": f"slab{args.gpus}" if args.gpus > 1 else "single-gpu",
         "l2": "inputs larger than L2 (E/H/Bloch state ping-pong ~335 MB per GPU vs 126 MB L2)",
     }
@@ -250,7 +254,11 @@ def run_mine(args, world, rank, local):
         backend, _ = slabs.slab_backend(local)
         samples = None if args.no_scaling_samples else (
             lambda w, r, d: scaling_samples(w, r, d, backend=backend))
+        from paper_2005_05412_b200.plan import build_plan
+
+        cfg = workload_config(build_plan(dev, sce), args)
         return slabs.bench_rank(args, dev, sce, world, rank, local, METRIC, UNIT, clock_sampler=ClockSampler,
+                                config=cfg,
                                 rebuild=lambda: build_workload(mb, args.gpus), samples=samples)
 
     solver = gpu.GpuFdtdSolver(dev, sce, tile_steps=args.tile_steps, exact=args.exact, gpu=local)
@@ -412,7 +420,8 @@ def run_mine(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(plan, args, k),
+        "config": workload_config(plan, args),
+        "implementation": {"tile_steps": k, "kernel": "bloch_wave_kernel (persistent wavefront)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "note": e2e_note},
         "gpu_launches": int(launches),  # persistent step + step-mask + row-0 sample kernels (library count)

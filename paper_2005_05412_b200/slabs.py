@@ -681,7 +681,7 @@ class SlabTimer:
 
 
 def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=None, rebuild=None,
-               samples=None):
+               samples=None, config=None):
     """bench.py --gpus N under torchrun: weak-scaled cfg2, one slab per GPU,
     device time of K full runs, max over ranks.
 
@@ -748,20 +748,22 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"cfg2 weak-scaled: {world} copies of the cfg2 device, {world} slabs x 2^22 "
-                                   f"cells, 20000 steps",
-                       "num_x": grid.num_x, "tile_steps": k, "exchange_period": period,
-                       "parallelism": f"slab{world}",
-                       "exchange": f"NCCL batched isend/irecv of {period} ghost cells per interface every "
-                                   f"{period} steps (one persistent launch of {period // k} chunks between)",
-                       "l2": "inputs larger than L2 (~335 MB of state per GPU vs 126 MB L2)"},
+            # the workload (bench.py's, identical for the reference arm) and
+            # the implementation knobs separately
+            "config": dict(config) if config is not None else
+                      {"workload": f"cfg2 weak-scaled: {world} copies of the cfg2 device, {world} slabs x 2^22 "
+                                   f"cells, 20000 steps", "num_x": grid.num_x, "parallelism": f"slab{world}"},
+            "implementation": {
+                "tile_steps": k, "exchange_period": period,
+                "exchange": f"NCCL batched isend/irecv of {period} ghost cells per interface every "
+                            f"{period} steps (one persistent launch of {period // k} chunks between)"},
             "e2e": e2e,
             # this rank's kernels (step, step-mask, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),
             "scaling_samples": extra,
         }
         if backend != "nccl" or local != int(os.environ.get("LOCAL_RANK", local)):
-            line["config"]["shared_gpu"] = (f"all {world} ranks on GPU {local}, {backend} exchanges staged "
+            line["shared_gpu"] = (f"all {world} ranks on GPU {local}, {backend} exchanges staged "
                                             f"through the host: a functional run of the multi-rank path, "
                                             f"not a scaling measurement")
         if sampler is not None:

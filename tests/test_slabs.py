@@ -269,4 +269,5 @@ def test_bench_under_torchrun_two_ranks_on_one_gpu():
     assert len(lines) == 1, out.stdout
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
-    assert line["config"]["num_x"] == 2 << 22 and "shared_gpu" in line["config"]
+    assert line["config"]["num_x"] == 2 << 22 and "shared_gpu" in line
+    assert line["config"]["parallelism"] == "slab2" and "tile_steps" in line["implementation"]
