@@ -596,7 +596,6 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
 #ifndef MBG_BLOCH_MINB
 #define MBG_BLOCH_MINB (16 / MBG_BLOCH_WARPS > 0 ? 16 / MBG_BLOCH_WARPS : 1)
 #endif
-constexpr int kEdgeWarps = 4;
 // interior CTA tile: dispatch on the medium (the density step must be the very
 // same formula the edge path uses -- bitwise independence of the tiling -- so
 // the real-dipole choice is global)
@@ -623,6 +622,156 @@ __device__ __forceinline__ void interior_tile(const BlochParams &P, const Chunk 
     else
         P.n_qm == 1 ? interior_cta<true, true, false, false, true>(P, K, span, re, rh, hook)
                     : interior_cta<true, false, false, false, true>(P, K, span, re, rh, hook);
+}
+
+// General tile as a CTA: the W = 32*C cells of one edge tile with ONE cell
+// per thread (kEdgeCtaWarps warps x 32 lanes, blocked by warp), so a step of
+// an edge tile costs one cell's dependency chain instead of C cells' worth of
+// one warp (run_tile, ~2.6 us per step: the per-launch critical path of small
+// domains).  Every per-cell property (coefficients, quantum material, H/E
+// update, boundary and source flags) is a register of its thread; neighbours
+// come by shuffle, across warps through double-buffered shared seams (two
+// barriers per step).  The cell arithmetic is run_tile's, operation for
+// operation (bitwise equal to every other path).
+constexpr int kEdgeCtaWarps = W / 32;
+static_assert(kEdgeCtaWarps * 32 == W, "one cell per thread");
+
+__device__ __forceinline__ void edge_cta(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi) {
+    __shared__ double seam_e[2][kEdgeCtaWarps], seam_h[2][kEdgeCtaWarps];
+    const Launch &L = P.L;
+    const long long nx = L.num_x;
+    const long long base = tile_base(L, t_lo);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long c = base + tid;
+    const long long l = c - L.win_lo;
+    const bool in_e = (l >= 0 && l < L.win_n);
+    if (in_e) MBG_CHK(l, L.win_n, "edge_cta e_in");
+    double E = in_e ? ld(K.e_in + l) : 0.0;
+    if (l >= 0 && l <= L.win_n) MBG_CHK(l, L.win_n + 1, "edge_cta h_in");
+    double H = (l >= 0 && l <= L.win_n) ? ld(K.h_in + l) : 0.0;
+    const int re = region_of(L.rg.e_start, L.rg.n, c);
+    const int rh = region_of(L.rg.h_start, L.rg.n, c);
+    const int qi = (in_e && c >= 0 && c < nx) ? L.rg.qm[re] : -1;
+    const double ca = L.rg.a[re], cbdx = L.rg.bdx[re], cch = L.rg.ch[rh];
+    const double bgp = pol_coef(L.rg.bg[re], P.rq[qi < 0 ? 0 : qi], P.real_dipole);
+    const bool hf = c >= 1 && c <= nx - 1;
+    const bool ef = nx > 1 && c >= 0 && c < nx;
+    const bool lf = L.has_boundary && base == 0 && tid == 0;  // cell 0
+    const bool rf = L.has_boundary && c == nx - 1;
+    bool sf = false;
+    for (int q = 0; q < L.n_src; ++q) sf |= c == L.src_cell[q];
+    double X = 0.0, Y = 0.0, Z = 0.0;
+    if (qi >= 0) {
+        MBG_CHK(l, L.plane, "edge_cta s_in");
+        MBG_CHK(2 * L.plane + l, L.plane * L.words, "edge_cta s_in plane");
+        X = ld(K.s_in + l);
+        Y = ld(K.s_in + L.plane + l);
+        Z = ld(K.s_in + 2 * L.plane + l);
+    }
+    const bool own_tile = c >= t_lo && c < t_hi;
+    const bool own = own_tile && c >= L.own_lo && c < L.own_hi;
+    for (int s = 0; s < K.steps; ++s) {
+        const long long n = K.n0 + s;
+        const int b = s & 1;
+        // ---- H update: needs E[m-1] (left neighbour) -------------------------
+        if (lane == 31) seam_e[b][warp] = E;
+        double El = __shfl_up_sync(kFull, E, 1);
+        const double e_right0 = __shfl_down_sync(kFull, E, 1);  // old E[1], H[1] for cell 0
+        const double h_right0 = __shfl_down_sync(kFull, H, 1);
+        __syncthreads();
+        if (lane == 0 && warp > 0) El = seam_e[b][warp - 1];
+        const double Hn = hf ? mad(cch, E - El, H) : H;
+        // ---- density step with E^{n-1} and polarisation rate -----------------
+        double p = 0.0;
+        if (qi >= 0)
+            p = P.real_dipole ? MBG_BLOCH_REAL(P.qm[qi], P.rq[qi], E, X, Y, Z) : bloch_cell(P.qm[qi], E, X, Y, Z);
+        // ---- E update: needs H[m+1] (right neighbour) ---------------------------
+        if (lane == 0) seam_h[b][warp] = Hn;
+        double hr = __shfl_down_sync(kFull, Hn, 1);
+        __syncthreads();
+        if (lane == 31 && warp < kEdgeCtaWarps - 1) hr = seam_h[b][warp + 1];
+        double en = E;
+        if (ef)
+            en = ca == 1.0 ? e_update<true>(ca, cbdx, bgp, E, hr - Hn, p) : e_update<false>(ca, cbdx, bgp, E, hr - Hn, p);
+        if (lf) {
+            // solver_fdtd.py:372-374
+            const double e_at = mad(L.l_c, e_right0, L.l_omc * E);
+            const double h_at = 0.5 * (h_right0 + hr);
+            en = L.l_hw * mad(L.l_z, h_at, e_at);
+        }
+        if (rf) {
+            // solver_fdtd.py:375-377 (E[Nx-2] old is the left neighbour)
+            const double e_at = mad(L.r_c, El, L.r_omc * E);
+            const double h_at = 0.5 * (H + Hn);
+            en = L.r_hw * mad(-L.r_z, h_at, e_at);
+        }
+        if (sf) {
+            for (int q = 0; q < L.n_src; ++q) {
+                if (c == L.src_cell[q]) {
+                    MBG_CHK(n * L.n_src + q, L.num_t * L.n_src, "edge_cta src_values");
+                    const double v = L.src_values[n * L.n_src + q];
+                    en = L.src_hard[q] ? v : en + v;
+                }
+            }
+        }
+        E = en;
+        H = Hn;
+        // ---- non-finite scan and records (owned result cells only) ------------
+        const unsigned long long mask = K.mask[s];
+        const unsigned char flags = K.check[s];
+        const bool check = (flags & MBG_STEP_SCAN) != 0;
+        if (mask || flags) {
+            if (own) {
+                if (check && !isfinite(E)) atomicMin(L.bad_step, (unsigned long long)n);
+                for (int r = 0; r < L.n_rec; ++r) {
+                    if (!((mask >> r) & 1ull)) continue;
+                    const long long cell = L.rec_cell[r];
+                    if (cell >= 0 && cell != c) continue;
+                    const long long col = cell >= 0 ? 0 : c - L.rec_col0[r];
+                    const long long idx = (n / L.rec_every[r] - L.rec_row0[r]) * L.rec_cols[r] + col;
+                    double vre = 0.0, vim = 0.0;
+                    switch (L.rec_q[r]) {
+                        case MBG_Q_E: vre = E; break;
+                        case MBG_Q_H: vre = H; break;
+                        case MBG_Q_D:
+                        default:
+                            if (qi >= 0) {
+                                double x, y, z;
+                                frame_true(P.frame, qi, X, Y, Z, x, y, z);
+                                if (L.rec_q[r] == MBG_Q_D)
+                                    bloch_entry(L.rec_i[r], L.rec_j[r], x, y, z, vre, vim);
+                                else
+                                    vre = -z;
+                            }
+                    }
+                    MBG_CHK(idx, L.rec_len[r], "edge_cta record");
+                    L.rec_re[r][idx] = vre;
+                    if (L.rec_im[r]) L.rec_im[r][idx] = vim;
+                }
+            }
+            if (L.inv && (flags & MBG_STEP_MONITOR)) {  // eigenvalues (1 +- |v|)/2 (_kernels.py:541-546)
+                unsigned long long key = ~0ull;
+                if (own && qi >= 0) {
+                    double x, y, z;
+                    frame_true(P.frame, qi, X, Y, Z, x, y, z);
+                    key = order_key(0.5 * (1.0 - sqrt(x * x + y * y + z * z)));
+                }
+                fold_min_eig(L.inv, key);
+            }
+        }
+    }
+    // ---- write back the tile's result cells -------------------------------------
+    if (own_tile) {
+        MBG_CHK(l, L.win_n, "edge_cta e_out");
+        MBG_CHK(l, L.plane, "edge_cta s_out");
+        K.e_out[l] = E;
+        K.h_out[l] = H;
+        if (qi >= 0) {
+            K.s_out[l] = X;
+            K.s_out[L.plane + l] = Y;
+            K.s_out[2 * L.plane + l] = Z;
+        }
+    }
 }
 
 // one warp over the result range [t_lo, t_hi) of at most 32*C - 2k cells
@@ -663,13 +812,13 @@ bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     });
 }
 
-// the few remaining cells (domain/window edges, region interfaces, sources),
-// one warp per result range of at most 32*C - 2k cells
-__global__ void __launch_bounds__(kEdgeWarps * 32)
+// the few remaining cells (domain/window edges, region interfaces, sources):
+// one CTA per result range of at most 32*C - 2k cells, one cell per thread
+// (edge_cta), so these ranges keep pace with the interior CTAs
+__global__ void __launch_bounds__(kEdgeCtaWarps * 32)
 bloch_edge_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ EdgeTiles T) {
-    const int w = blockIdx.x * kEdgeWarps + (threadIdx.x >> 5);
-    if (w >= T.n) return;
-    edge_range(P, launch_chunk(P.L), T.lo[w], T.hi[w], threadIdx.x & 31);
+    if ((int)blockIdx.x >= T.n) return;
+    edge_cta(P, launch_chunk(P.L), T.lo[blockIdx.x], T.hi[blockIdx.x]);
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -869,8 +1018,7 @@ cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,
     T.n = 0;
     auto flush = [&]() -> cudaError_t {
         if (T.n == 0) return cudaSuccess;
-        const int blocks = (T.n + kEdgeWarps - 1) / kEdgeWarps;
-        bloch_edge_kernel<<<blocks, kEdgeWarps * 32, 0, st_edge>>>(P, T);
+        bloch_edge_kernel<<<T.n, kEdgeCtaWarps * 32, 0, st_edge>>>(P, T);
         ++*kernels;
         T.n = 0;
         return cudaGetLastError();
