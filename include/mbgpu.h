@@ -72,6 +72,9 @@ extern "C" {
  * narrower domain is a chain of few tiles, faster as one launch per chunk
  * with a whole SM per tile) */
 #define MBG_FLAG_PERSISTENT 2
+/* mbg_grid.flags: the kernels' default tile depth as such (no small-domain
+   deepening, see mbg_create): what a slab of this scenario uses */
+#define MBG_FLAG_DEFAULT_DEPTH 4
 
 typedef struct mbg_solver mbg_solver;
 

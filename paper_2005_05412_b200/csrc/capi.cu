@@ -499,6 +499,23 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
     s->plane = (s->win_n + 31) / 32 * 32;  // 256-byte aligned planes
     int k = g.tile_steps > 0 ? g.tile_steps : default_tile_steps(g.levels, g.stepper);
     const int w = tile_width(s);
+    if (g.tile_steps <= 0 && !(s->bloch || g.levels == 0) && g.win_lo == 0 && g.win_hi == g.num_x &&
+        !(g.flags & MBG_FLAG_DEFAULT_DEPTH)) {
+        // small N-level domains (every tile on its own SM even at a deeper
+        // chunk): fewer, deeper launches -- the per-launch overhead (~3.7 us)
+        // is then paid every 32 steps instead of every 4 while the extra halo
+        // work lands on idle SMs (tzenov2016-full, 8192 five-level cells:
+        // 2.02 s at k = 4, 1.58 s at k = 32)
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device) != cudaSuccess || sms <= 0) sms = 148;
+        for (int kk : {32, 16, 8}) {
+            if (kk <= k || 2 * kk + 32 > w) continue;
+            if ((s->win_n + (w - 2 * kk) - 1) / (w - 2 * kk) <= sms) {
+                k = kk;
+                break;
+            }
+        }
+    }
     // every tile (and, for the two-level kernel, every warp tile of the edge
     // kernel) must keep at least 32 result cells
     const int wmin = (s->bloch || g.levels == 0) ? std::min(w, kBlochTile) : w;

@@ -29,6 +29,7 @@ HEADER = PKG.parent / "include" / "mbgpu.h"
 MBG_STEPPER = {"splitting": 0, "rk4": 1}
 MBG_FLAG_PER_LAUNCH = 1
 MBG_FLAG_PERSISTENT = 2
+MBG_FLAG_DEFAULT_DEPTH = 4
 MAX_REGIONS, MAX_QM, MAX_SOURCES, MAX_RECORDS, MAX_LEVELS, MAX_TILE_STEPS = 128, 4, 32, 64, 8, 128
 MAX_BATCH_QM = 65536
 

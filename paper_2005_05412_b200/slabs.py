@@ -469,7 +469,9 @@ def tile_steps_of(solver) -> int:
     """The k the native solver will use for this scenario (asks the library
     through a throw-away handle on a tiny window, so nothing big is allocated)."""
     w = min(solver.grid.num_x, 1024)
-    h = native.Handle(solver._grid_struct(win=(0, w), own=(0, w)))
+    g = solver._grid_struct(win=(0, w), own=(0, w))
+    g.flags |= native.MBG_FLAG_DEFAULT_DEPTH  # a slab's depth (slabs are windows: no small-domain deepening)
+    h = native.Handle(g)
     try:
         k = C.c_int32(0)
         h.call("mbg_tile_steps", C.byref(k))
