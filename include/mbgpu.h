@@ -5,7 +5,8 @@
  * (/root/reference/pkg/src/mblight/solver_fdtd.py:444-498) calling numba
  * loops per step.  This ABI is the seam a Python (ctypes) or any other host
  * binds to replace that loop; the setup arithmetic stays in the host
- * (paper_2005_05412_b200/plan.py restates FdtdSolver.__init__,
+ * (paper_2005_05412_b200/plan.py builds it with the reference's own setup
+ * functions and kernel constructors, FdtdSolver.__init__,
  * solver_fdtd.py:207-326) and is passed here as plain arrays.
  *
  * Entry point -> reference interface it replaces:
@@ -25,6 +26,7 @@
  *   mbg_poll_nonfinite    SolverError("non-finite ... at step n")  solver_fdtd.py:386-388
  *   mbg_download_record   plan.to_result                           solver_fdtd.py:164-172
  *   mbg_invariants        DensityKernel.invariant_stats            _kernels.py:394-401, 541-546
+ *   mbg_batch_points      many Nx = 1 runs (ScalarKernel path)     solver_fdtd.py:89-96,347-349; _kernels.py:404-425
  *   mbg_pack_halo/unpack  (new) slab ghost exchange, no reference analogue
  *
  * Conventions: every function returns 0 on success or a negative MBG_E_*
