@@ -15,3 +15,6 @@ run cfg4 --stepper rk4 --steps 48
 timeout 300 python tools/slab_step.py --config cfg2 --world 3 | tail -1          # slab path, per rank
 timeout 300 python tools/slab_step.py --config cfg5 --world 3 --period 16 --tile-steps 4 --steps 512 | tail -1
 timeout 600 python tools/points_bench.py --systems 4096 | tail -1                 # batched single points
+timeout 600 python tools/points_bench.py --systems 4096 --sweep media | tail -1   # 4096 distinct media
+timeout 600 python tools/published_setups.py 2>/dev/null                          # the paper's examples, public call
+timeout 600 python tools/small_nlevel.py 2>/dev/null                              # small N-level domains
