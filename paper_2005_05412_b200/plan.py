@@ -349,10 +349,13 @@ def _first_at_or_after(end: float, dx: float, lo: int, hi: int, offset: float = 
     return m
 
 
-def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_cache: dict | None = None) -> SolverPlan:
+def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_cache: dict | None = None,
+               qm_cache: dict | None = None) -> SolverPlan:
     """Validate and precompute a run (``FdtdSolver.__init__`` minus state
     arrays, same checks in the same order).  ``sample_cache``: see
-    :func:`_cached_samples`.
+    :func:`_cached_samples`; ``qm_cache``: a caller-owned dict that shares
+    the stepper constants of one quantum description across the plans of a
+    sweep (``run_points``).
 
     Nothing here is O(Nx) for the default zero initial fields: the region
     table comes from the region ends by exact comparisons of the reference's
@@ -413,7 +416,17 @@ def build_plan(device, scenario, stepper: str = "splitting", seed=None, sample_c
             continue
         if m.id not in qm_ids:
             qm_ids.append(m.id)
-            qm_list.append(qm_constants(m.qm, dt, stepper))
+            # qm_cache (caller-owned, one sweep): the stepper constants of the
+            # same quantum description at the same dt are built once
+            # (the entry keeps the description alive, so its id is not reused)
+            key = (id(m.qm), dt, stepper) if qm_cache is not None else None
+            hit = qm_cache.get(key) if key is not None else None
+            qc = hit[1] if hit is not None and hit[0] is m.qm else None
+            if qc is None:
+                qc = qm_constants(m.qm, dt, stepper)
+                if key is not None:
+                    qm_cache[key] = (m.qm, qc)
+            qm_list.append(qc)
         qm_index[r] = qm_ids.index(m.id)
     levels = qm_list[0].levels if qm_list else 0
 

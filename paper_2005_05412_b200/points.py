@@ -20,12 +20,13 @@ plan._cached_samples).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import time
 
 import numpy as np
 
 from . import native
-from .reference import mblight
+from .reference import core, mblight
 
 SolverError = mblight.SolverError
 from .plan import QUANTITY_CODES, build_plan, unpack_density
@@ -88,14 +89,48 @@ def _check_finite(e: np.ndarray, num_t: int) -> None:
         raise SolverError(f"non-finite electric field at step {int(bad[0])}")
 
 
-def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu: int = 0, seed=None):
-    """Run many single-grid-point (device, scenario) problems in one launch."""
+def vector_samples(src, dt: float, num_t: int):
+    """Source.value(n dt), n = 0..num_t-1, as one numpy evaluation, for the
+    reference's two frozen pulse types (None for any other source): the
+    expressions of SechPulse.value / GaussianPulse.value (core.py:296-300,
+    320-324; the sech in the overflow-safe exp form of core.py:251-254) in the
+    same operation order, with numpy's exp/cos in place of libm's -- so each
+    sample is within an ulp or two of the reference's (tests/test_points_host.py),
+    not bit-identical.  Opt-in: ``run_points(..., fast_sources=True)``."""
+    if type(src) not in (core.SechPulse, core.GaussianPulse):
+        return None
+    t = np.arange(num_t) * dt
+    phase = np.cos(2.0 * math.pi * src.carrier_freq * t - src.carrier_phase)
+    if type(src) is core.SechPulse:
+        e = np.exp(-np.abs(src.envelope_rate * t - src.envelope_shift))
+        return src.amplitude * (2.0 * e / (1.0 + e * e)) * phase
+    arg = (t - src.peak_time) / src.width
+    return src.amplitude * np.exp(-arg * arg) * phase
+
+
+def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu: int = 0, seed=None,
+               fast_sources: bool = False):
+    """Run many single-grid-point (device, scenario) problems in one launch.
+
+    ``fast_sources``: sample the reference's pulse types with one numpy
+    evaluation per source (:func:`vector_samples`, within an ulp or two of
+    Source.value) instead of one Python call per step -- for sweeps over the
+    pulses themselves, where the per-call sampling dominates the host time."""
     problems = list(problems)
     if not problems:
         return []
     t_host = time.perf_counter()
     cache: dict = {}  # equal pulses of the sweep sampled once
-    plans = [build_plan(dev, sce, stepper, seed, cache) for dev, sce in problems]
+    qm_cache: dict = {}  # one constant set per quantum description
+    plans = [build_plan(dev, sce, stepper, seed, cache, qm_cache) for dev, sce in problems]
+    if fast_sources:
+        for p in plans:
+            cols = [vector_samples(src, p.grid.dt, p.grid.num_t) for src in p.sources]
+            if cols and all(c is not None for c in cols):
+                buf = p.src_buffer
+                for k, c in enumerate(cols):
+                    buf[1:, k] = c[1:]  # row 0 unused (solver_fdtd.py:379-385 samples n >= 1)
+                p.sampled_to = p.grid.num_t
     p0 = plans[0]
     if any(p.grid.num_x != 1 for p in plans):
         raise ValueError("run_points takes single-grid-point scenarios (num_gridpoints == 1)")
@@ -126,7 +161,7 @@ def run_points(problems, stepper: str = "splitting", *, exact: bool = False, gpu
     memo: dict = {}
     for b, p in enumerate(plans):
         key = None
-        if cache_ok(p):
+        if not fast_sources and cache_ok(p):
             key = (float(p.e_init[0]), tuple(id(c) for c in _sample_columns(p)), tuple(p.src_hard.tolist()))
         row = memo.get(key) if key is not None else None
         if row is None:

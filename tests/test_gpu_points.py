@@ -139,3 +139,16 @@ def test_sweep_over_many_media_in_one_call(stepper):
     # distinct media give distinct populations
     inv = np.array([batch[i][0].data[-1, 0] for i in (0, 4095)])
     assert inv[0] != inv[1]
+
+
+def test_fast_sources_match_reference_sampling():
+    """run_points(fast_sources=True): the pulse sweep with numpy-sampled
+    sources agrees with the Source.value-sampled batch to tolerance."""
+    mb.clear_material_library()
+    variants = [dict(scale=s) for s in (0.3, 1.0, 2.7)]
+    a = run_points([_song(**v) for v in variants])
+    mb.clear_material_library()
+    b = run_points([_song(**v) for v in variants], fast_sources=True)
+    for ra, rb in zip(a, b):
+        for x, y in zip(ra, rb):
+            assert rel_err(y.data, x.data) <= 1e-11, (x.name, rel_err(y.data, x.data))

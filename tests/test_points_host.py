@@ -58,3 +58,25 @@ def test_batch_rejects_extended_grids_before_any_work():
     with pytest.raises(ValueError):
         P.run_points([(dev, sce)])
     assert P.run_points([]) == []
+
+
+def test_vector_samples_within_two_ulp_of_source_value():
+    """run_points(fast_sources=True) samples the reference's pulse types with
+    one numpy evaluation; every sample is within 2 ulp (of the pulse
+    amplitude's scale) of Source.value."""
+    import numpy as np
+
+    from paper_2005_05412_b200.points import vector_samples
+    from paper_2005_05412_b200.reference import mblight as mb
+
+    srcs = [mb.SechPulse("s", 0.0, "soft", 3.5e9, 3.8e14, 17.2, 3.5e14, -1.5),
+            mb.SechPulse("h", 0.0, "hard", 1.0, 2e14, 10.0, 2e14),
+            mb.GaussianPulse("g", 0.0, "soft", 1e9, 1.9e14, 0.75e-15, 0.25e-15),
+            mb.GaussianPulse("g2", 0.0, "soft", 2e9, 2.1e14, 600e-15, 200e-15, 0.3)]
+    for src in srcs:
+        dt, n = 7.6e-18, 20000
+        got = vector_samples(src, dt, n)
+        want = np.array([src.value(i * dt) for i in range(n)])
+        scale = abs(src.amplitude)
+        assert np.max(np.abs(got - want)) <= 2 * np.spacing(scale), src.name
+    assert vector_samples(mb.ConstantField(0.0), 1e-18, 10) is None

@@ -25,6 +25,7 @@ from test_gpu_points import _song  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--systems", type=int, default=4096)
 ap.add_argument("--stepper", default="splitting")
+ap.add_argument("--fast-sources", action="store_true", help="run_points(fast_sources=True)")
 ap.add_argument("--sweep", choices=("pulse", "media"), default="pulse",
                 help="pulse: one three-level medium, pulse amplitudes swept; media: distinct two-level "
                      "media (T2 swept), one shared pulse")
@@ -39,7 +40,7 @@ else:
     problems = [_two_level(t2=float(t), tag=f"m{i}") for i, t in enumerate(np.linspace(2e11, 5e12, a.systems))]
 run_points(problems[:8], stepper=a.stepper)  # warm (module load)
 t0 = time.perf_counter()
-res = run_points(problems, stepper=a.stepper)
+res = run_points(problems, stepper=a.stepper, fast_sources=a.fast_sources)
 t_batch = time.perf_counter() - t0
 steps = problems[0][1].num_timesteps - 1 if problems[0][1].num_timesteps else 9999
 sol = gpu.GpuFdtdSolver(*problems[0], stepper=a.stepper)
@@ -47,7 +48,7 @@ t0 = time.perf_counter()
 sol.run()
 t_one = time.perf_counter() - t0
 t_dev = LAST_RUN["batch_s"]
-print(f"{a.systems} systems x {steps} steps ({a.stepper}, {a.sweep} sweep): run_points {t_batch:.3f} s = host "
+print(f"{a.systems} systems x {steps} steps ({a.stepper}, {a.sweep} sweep{', fast sources' if a.fast_sources else ''}): run_points {t_batch:.3f} s = host "
       f"setup {LAST_RUN['host_setup_s']:.3f} s (plans, media, field sequences) + native batch call {t_dev:.3f} s "
       f"({a.systems * steps / t_dev:.3e} system-steps/s) + results {LAST_RUN['host_results_s']:.3f} s; "
       f"one single-point solver run {t_one:.3f} s ({steps / t_one:.3e} steps/s)")
