@@ -33,8 +33,10 @@ SOLVER_NAMES = ("gpu-fdtd-reg-cayley", "gpu-fdtd-rk4")
 RECORD_HBM_BYTES = 4 << 30
 # ... sized so one segment's rows take about this much device memory
 RECORD_SEGMENT_BYTES = 512 << 20
-# first run segment when the sources are sampled during the run (see _run_on)
+# first run segment when the sources are sampled during the run (see _run_on),
+# and the factor by which the segments grow
 FIRST_FEED = 1024
+FEED_GROWTH = 4
 
 
 class GpuFdtdSolver:
@@ -308,7 +310,7 @@ class GpuFdtdSolver:
             chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
         # sources not sampled yet: sampled (Source.value, as the reference's
         # loop calls it per step) for the next segment while the device steps
-        # the current one; segments grow from FIRST_FEED steps by 4x
+        # the current one; segments grow from FIRST_FEED steps by FEED_GROWTH
         feed = self._fed < num_t
         cap = FIRST_FEED if feed and split is None else chunk
         n = 1
@@ -321,7 +323,7 @@ class GpuFdtdSolver:
             n += cnt
             since += cnt
             if feed and n < num_t:
-                cap = min(4 * cap, chunk)
+                cap = min(FEED_GROWTH * cap, chunk)
                 self._feed_sources(h, n + min(chunk, cap, num_t - n))
             if split is not None and (n - 1) % split == 0:
                 h.call("mbg_invariants_accumulate")
