@@ -130,6 +130,9 @@ int mbg_set_sources(mbg_solver *s, int32_t n, const int64_t *cell, const int32_t
  * by segment while the device steps (Source.value inside the reference's
  * loop, solver_fdtd.py:379-385) */
 int mbg_set_source_rows(mbg_solver *s, int64_t lo, int64_t hi, const double *rows);
+/* *idle = 1 when every operation enqueued on the solver's stream has completed
+ * (non-blocking; paces the host's source sampling against the device) */
+int mbg_stream_idle(mbg_solver *s, int32_t *idle);
 /* quantity MBG_Q_*, cell -1 = whole domain, i/j 0-based, every >= 1; complex for d with i != j */
 int mbg_set_records(mbg_solver *s, int32_t n, const int32_t *quantity, const int64_t *cell,
                     const int32_t *i, const int32_t *j, const int64_t *every);

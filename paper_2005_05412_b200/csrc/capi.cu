@@ -1126,6 +1126,19 @@ int mbg_advance(mbg_solver *s, int64_t first, int64_t n_steps) {
     return MBG_OK;
 }
 
+int mbg_stream_idle(mbg_solver *s, int32_t *idle) {
+    if (!s || !idle) return MBG_E_ARG;
+    cudaSetDevice(s->g.device);
+    const cudaError_t e = cudaStreamQuery(s->stream);
+    if (e == cudaErrorNotReady) {
+        *idle = 0;
+        return MBG_OK;
+    }
+    CK(e);
+    *idle = 1;
+    return MBG_OK;
+}
+
 int mbg_synchronize(mbg_solver *s) {
     if (!s) return MBG_E_ARG;
     cudaSetDevice(s->g.device);

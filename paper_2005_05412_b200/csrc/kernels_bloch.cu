@@ -812,6 +812,30 @@ bloch_interior_kernel(const __grid_constant__ BlochParams P) {
     });
 }
 
+// One step launch of the per-launch path: CTAs [0, tiles) are the CTA tiles
+// (interior ones step, the others leave), CTAs [tiles, tiles + T.n) the edge
+// ranges (edge_cta) -- one kernel, no second stream and no fork/join events
+// per launch (the cross-stream pair cost cfg1 ~20 % of its device time)
+static_assert(kEdgeCtaWarps == kBlochWarpsPerBlock, "edge ranges run in the step kernel's CTAs");
+__global__ void __launch_bounds__(kBlochWarpsPerBlock * 32, MBG_BLOCH_MINB)
+bloch_step_kernel(const __grid_constant__ BlochParams P, const __grid_constant__ EdgeTiles T, int tiles) {
+    const Launch &L = P.L;
+    if ((int)blockIdx.x >= tiles) {
+        const int e = (int)blockIdx.x - tiles;
+        edge_cta(P, launch_chunk(L), T.lo[e], T.hi[e]);
+        return;
+    }
+    const LaunchSpan span{L};
+    if (span.lo() >= L.res_hi) return;
+    if (!tile_is_interior(L, span.base(), kBlochCtaTile)) return;
+    interior_tile(P, launch_chunk(L), span, [&]() {
+        if (threadIdx.x < L.k) {
+            s_mask[threadIdx.x] = L.step_mask[threadIdx.x];
+            s_check[threadIdx.x] = L.check[threadIdx.x];
+        }
+    });
+}
+
 // the few remaining cells (domain/window edges, region interfaces, sources):
 // one CTA per result range of at most 32*C - 2k cells, one cell per thread
 // (edge_cta), so these ranges keep pace with the interior CTAs
@@ -1008,22 +1032,30 @@ int bloch_cta_tile() { return kBlochCtaTile; }
 // interior kernel instead of trailing it.
 cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, cudaStream_t st_edge,
                          cudaEvent_t fork, cudaEvent_t join, int *kernels) {
+    (void)st_edge;
+    (void)fork;
+    (void)join;
     const Launch &L = P.L;
-    *kernels = 1;
-    cudaError_t err = cudaEventRecord(fork, st);
-    if (err == cudaSuccess) err = cudaStreamWaitEvent(st_edge, fork, 0);
-    if (err != cudaSuccess) return err;
+    *kernels = 0;
     // host-side twin of the device classification: collect the non-interior tiles
     EdgeTiles T;
     T.n = 0;
+    bool fused = false;  // the first batch of edge ranges rides with the CTA tiles
+    cudaError_t err = cudaSuccess;
     auto flush = [&]() -> cudaError_t {
-        if (T.n == 0) return cudaSuccess;
-        bloch_edge_kernel<<<T.n, kEdgeCtaWarps * 32, 0, st_edge>>>(P, T);
+        if (!fused) {
+            bloch_step_kernel<<<(unsigned)(tiles + T.n), kBlochWarpsPerBlock * 32, 0, st>>>(P, T, (int)tiles);
+            fused = true;
+        } else if (T.n > 0) {
+            bloch_edge_kernel<<<T.n, kEdgeCtaWarps * 32, 0, st>>>(P, T);
+        } else {
+            return cudaSuccess;
+        }
         ++*kernels;
         T.n = 0;
         return cudaGetLastError();
     };
-    const long long warp_own = W - 2 * L.k;  // result cells one warp tile can deliver
+    const long long warp_own = W - 2 * L.k;  // result cells one edge range can deliver
     for (long long t = 0; t < tiles; ++t) {
         const long long t_lo = L.res_lo + t * L.tile_own;
         if (tile_is_interior(L, tile_base(L, t_lo), kBlochCtaTile)) continue;
@@ -1034,11 +1066,7 @@ cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,
             if (++T.n == kMaxEdgeTiles && (err = flush()) != cudaSuccess) return err;
         }
     }
-    if ((err = flush()) != cudaSuccess) return err;
-    bloch_interior_kernel<<<(unsigned)tiles, kBlochWarpsPerBlock * 32, 0, st>>>(P);
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    if ((err = cudaEventRecord(join, st_edge)) != cudaSuccess) return err;
-    return cudaStreamWaitEvent(st, join, 0);
+    return flush();
 }
 
 cudaError_t launch_wave_masks(const Launch &L, long long n_steps, long long last_step, unsigned long long *masks,

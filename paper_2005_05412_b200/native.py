@@ -66,6 +66,7 @@ SIGNATURES = {
     "mbg_set_boundary": (C.c_int, [_h] + [C.c_double] * 6),
     "mbg_set_sources": (C.c_int, [_h, C.c_int32, _i64p, _i32p, _dp]),
     "mbg_set_source_rows": (C.c_int, [_h, C.c_int64, C.c_int64, _dp]),
+    "mbg_stream_idle": (C.c_int, [_h, _i32p]),
     "mbg_set_records": (C.c_int, [_h, C.c_int32, _i32p, _i64p, _i32p, _i32p, _i64p]),
     "mbg_upload_fields": (C.c_int, [_h, _dp, _dp]),
     "mbg_upload_density": (C.c_int, [_h, _dp]),

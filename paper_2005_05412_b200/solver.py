@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
+import time
 
 import numpy as np
 
@@ -309,32 +310,41 @@ class GpuFdtdSolver:
         if segment:
             chunk = min(chunk, segment)  # with the monitor: a multiple of its cadence (see _segment_steps)
         # sources not sampled yet: sampled (Source.value, as the reference's
-        # loop calls it per step) for the next segment while the device steps
-        # the current one; segments grow from FIRST_FEED steps by FEED_GROWTH
+        # loop calls it per step) by a host thread while the device steps the
+        # rows already there; each advance takes the rows sampled by then
+        # (see _SourceSampler / _next_count).  With the monitor split the run
+        # cuts at monitored steps: rows are then sampled segment by segment.
         feed = self._fed < num_t
-        cap = FIRST_FEED if feed and split is None else chunk
+        sampler = _SourceSampler(self.plan) if feed and split is None else None
+        last = 0
         n = 1
         since = 0
         h.call("mbg_event_begin")
-        while n < num_t:
-            cnt = min(chunk, cap, num_t - n)
-            self._feed_sources(h, n + cnt)
-            h.call("mbg_advance", n, cnt)
-            n += cnt
-            since += cnt
-            if feed and n < num_t:
-                cap = min(FEED_GROWTH * cap, chunk)
-                self._feed_sources(h, n + min(chunk, cap, num_t - n))
-            if split is not None and (n - 1) % split == 0:
-                h.call("mbg_invariants_accumulate")
-            if segment:
-                self._drain_streams(h, n - 1)
-            if since >= poll_every or n >= num_t or segment:
-                since = 0
-                bad = C.c_int64(-1)
-                h.call("mbg_poll_nonfinite", C.byref(bad))
-                if bad.value >= 0:
-                    raise SolverError(f"non-finite electric field at step {bad.value}")
+        try:
+            while n < num_t:
+                if sampler is not None:
+                    cnt = self._next_count(h, sampler, n, min(chunk, num_t - n), last)
+                    last = cnt
+                else:
+                    cnt = min(chunk, num_t - n)
+                    self.plan.sample_sources(n + cnt)
+                self._feed_sources(h, n + cnt)
+                h.call("mbg_advance", n, cnt)
+                n += cnt
+                since += cnt
+                if split is not None and (n - 1) % split == 0:
+                    h.call("mbg_invariants_accumulate")
+                if segment:
+                    self._drain_streams(h, n - 1)
+                if since >= poll_every or n >= num_t or segment:
+                    since = 0
+                    bad = C.c_int64(-1)
+                    h.call("mbg_poll_nonfinite", C.byref(bad))
+                    if bad.value >= 0:
+                        raise SolverError(f"non-finite electric field at step {bad.value}")
+        finally:
+            if sampler is not None:
+                sampler.stop()
         ms = C.c_float(0)
         h.call("mbg_event_end", C.byref(ms))
         self.kernel_ms = float(ms.value)
@@ -349,14 +359,33 @@ class GpuFdtdSolver:
         self.launches = int(launches.value)
 
     def _feed_sources(self, h, hi):
-        """Sample the sources up to row ``hi`` (exclusive) and queue those rows
-        for the device (stream-ordered before the next launch)."""
+        """Queue the sampled source rows [fed, hi) for the device
+        (stream-ordered before the next launch)."""
+        hi = min(hi, self.plan.sampled_to)
         if hi <= self._fed:
             return
-        lo, hi = self.plan.sample_sources(hi)
-        if hi > lo:
-            h.call("mbg_set_source_rows", lo, hi, native.ptr(self.plan.src_buffer[lo:hi]))
+        lo = self._fed
+        h.call("mbg_set_source_rows", lo, hi, native.ptr(self.plan.src_buffer[lo:hi]))
         self._fed = hi
+
+    @staticmethod
+    def _next_count(h, sampler, n, most, last):
+        """Steps of the next advance from step n (at most ``most``): once the
+        sampler is at least twice the last advance (and FIRST_FEED) ahead, or
+        has every row up to n + most, or the device has run dry with
+        FIRST_FEED rows ready -- so the device queue stays fed while the rows
+        are sampled, and advances grow as fast as the sampling allows."""
+        want = max(FIRST_FEED, FEED_GROWTH * last)
+        idle = C.c_int32(0)
+        while True:
+            ready = sampler.ready()
+            if ready - n >= min(want, most):
+                return min(ready - n, most)
+            if ready - n >= min(FIRST_FEED, most):
+                h.call("mbg_stream_idle", C.byref(idle))
+                if idle.value:
+                    return min(ready - n, most)
+            sampler.wait(n + min(want, most))
 
     # -- invariant monitor (solver_fdtd.py:306-308, 425-440) ---------------------
 
@@ -371,6 +400,56 @@ class GpuFdtdSolver:
         h.call("mbg_invariants_read", native.ptr(out))
         self.invariant_report = {"max_trace_dev": float(out[0]), "max_herm_dev": float(out[1]),
                                  "min_eigenvalue": float(out[2])}
+
+
+class _SourceSampler:
+    """Samples the plan's sources (Source.value, plan.sample_sources) on a
+    host thread, block by block, ahead of the run; the run's thread releases
+    the GIL inside every native call, so the sampling proceeds while it
+    enqueues launches or waits for the device.  Errors of Source.value are
+    re-raised in the run's thread."""
+
+    BLOCK = 256
+
+    def __init__(self, plan):
+        import threading
+
+        self.plan = plan
+        plan.src_buffer  # allocated here, before the thread writes into it
+        self.cv = threading.Condition()
+        self.error = None
+        self.stopped = False
+        self.thread = threading.Thread(target=self._work, name="mbg-source-sampler", daemon=True)
+        self.thread.start()
+
+    def _work(self):
+        try:
+            end = self.plan.grid.num_t
+            while not self.stopped and self.plan.sampled_to < end:
+                self.plan.sample_sources(self.plan.sampled_to + self.BLOCK)
+                with self.cv:
+                    self.cv.notify_all()
+                time.sleep(0)  # hand the GIL to the run's thread between blocks
+        except BaseException as exc:  # noqa: BLE001  (re-raised in the run's thread)
+            self.error = exc
+            with self.cv:
+                self.cv.notify_all()
+
+    def ready(self) -> int:
+        if self.error is not None:
+            raise self.error
+        return self.plan.sampled_to
+
+    def wait(self, rows: int):
+        with self.cv:
+            self.cv.wait_for(lambda: self.error is not None or self.plan.sampled_to >= min(rows, self.plan.grid.num_t),
+                             timeout=2e-4)
+        if self.error is not None:
+            raise self.error
+
+    def stop(self):
+        self.stopped = True
+        self.thread.join()
 
 
 def _rk4_factory(device, scenario, **kw):
