@@ -53,8 +53,6 @@ struct mbg_solver {
     int k = 1;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    cudaStream_t side = nullptr;  // edge tiles of the two-level kernel
-    cudaEvent_t fork = nullptr, join = nullptr;
     long long win_n = 0, plane = 0;
     double *e[2] = {nullptr, nullptr}, *h[2] = {nullptr, nullptr}, *s[2] = {nullptr, nullptr};
     int cur = 0;
@@ -382,8 +380,8 @@ cudaError_t launch_step(const mbg_solver *s, const Launch &L, long long tiles, i
     *kernels = 1;
     if (s->bloch || s->g.levels == 0) {
         const BlochParams P = bloch_params(s, L);
-        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels)
-                          : fast::launch_bloch(P, tiles, s->stream, s->side, s->fork, s->join, kernels);
+        return s->g.exact ? exact::launch_bloch(P, tiles, s->stream, kernels)
+                          : fast::launch_bloch(P, tiles, s->stream, kernels);
     }
     switch (s->g.levels) {
         case 2: return launch_dense_n<2>(s, L, tiles);
@@ -528,10 +526,6 @@ int mbg_create(const mbg_grid *grid, mbg_solver **out) {
     if (cudaSetDevice(g.device) != cudaSuccess) return cleanup(MBG_E_CUDA);
     if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) return cleanup(MBG_E_CUDA);
     s->own_stream = true;
-    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) != cudaSuccess)
-        return cleanup(MBG_E_CUDA);
     configure_pool(g.device);
     const size_t fb = sizeof(double) * (s->win_n + 1);
     const size_t sb = sizeof(double) * (size_t)std::max(1, s->words) * s->plane;
@@ -584,12 +578,6 @@ void mbg_destroy(mbg_solver *s) {
     if (s->ev1) cudaEventDestroy(s->ev1);
     for (cudaEvent_t e : s->marks)
         if (e) cudaEventDestroy(e);
-    if (s->side) {
-        cudaStreamSynchronize(s->side);
-        cudaStreamDestroy(s->side);
-    }
-    if (s->fork) cudaEventDestroy(s->fork);
-    if (s->join) cudaEventDestroy(s->join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
 }

@@ -1027,14 +1027,10 @@ __global__ void bloch_batch_kernel(const __grid_constant__ BlochBatchParams P) {
 
 int bloch_cta_tile() { return kBlochCtaTile; }
 
-// The edge tiles (a handful of latency-bound warps) run on a side stream,
-// forked from and joined back into the launch stream, so they overlap the
-// interior kernel instead of trailing it.
-cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, cudaStream_t st_edge,
-                         cudaEvent_t fork, cudaEvent_t join, int *kernels) {
-    (void)st_edge;
-    (void)fork;
-    (void)join;
+// One step launch (bloch_step_kernel): the CTA tiles and, in the same grid,
+// the edge ranges the host classifies (overflow beyond kMaxEdgeTiles in
+// further edge-only launches on the same stream).
+cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, int *kernels) {
     const Launch &L = P.L;
     *kernels = 0;
     // host-side twin of the device classification: collect the non-interior tiles

@@ -93,9 +93,7 @@ struct BlochWave {
 #define MBG_DECLARE_LAUNCHERS(NS)                                                             \
     namespace NS {                                                                            \
     int bloch_cta_tile();                                                                     \
-    cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st,          \
-                             cudaStream_t st_edge, cudaEvent_t fork, cudaEvent_t join,         \
-                             int *kernels);                                                    \
+    cudaError_t launch_bloch(const BlochParams &P, long long tiles, cudaStream_t st, int *kernels); \
     cudaError_t launch_bloch_wave(const BlochParams &P, const BlochWave &V, cudaStream_t st);     \
     cudaError_t launch_wave_masks(const Launch &L, long long n_steps, long long last_step,          \
                                   unsigned long long *masks, unsigned char *checks, cudaStream_t st); \
