@@ -968,8 +968,12 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
                 items.push_back(WaveItem{t_lo, t_hi, 0, 0});
                 continue;
             }
-            for (long long lo = t_lo; lo < t_hi; lo += kBlochWarpsPerBlock * warp_own)
-                items.push_back(WaveItem{lo, std::min(lo + kBlochWarpsPerBlock * warp_own, t_hi), 1, 0});
+            // one item per edge range (flag 2: the CTA steps it one cell per
+            // thread), the ranges of equal length (each >= k when possible)
+            const long long len = t_hi - t_lo;
+            const long long parts = (len + warp_own - 1) / warp_own;
+            for (long long q = 0; q < parts; ++q)
+                items.push_back(WaveItem{t_lo + len * q / parts, t_lo + len * (q + 1) / parts, 2, 0});
         }
         // every item but the last must span >= k cells (dependencies j-1 .. j+1)
         std::vector<WaveItem> merged;

@@ -789,6 +789,17 @@ __device__ __forceinline__ void edge_range(const BlochParams &P, const Chunk &K,
         run_tile<false>(P, K, t_lo, t_hi, base, lane);
 }
 
+// the persistent kernel's edge items of one range (flag 2): the whole CTA
+// steps the range's 32C-cell tile one cell per thread (edge_cta), so an edge
+// item takes about as long as an interior one -- edge items sit on the
+// wavefront's dependency chain, and stepped by single warps at 8 cells per
+// lane they made it ~0.45 ms per chunk (2^20 cells: 60 % of the CTA time
+// waiting on them).  A call keeps its registers out of the interior path.
+static_assert(kEdgeCtaWarps == kBlochWarpsPerBlock, "edge items use the wave CTA as one tile");
+__device__ __noinline__ void edge_cta_call(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi) {
+    edge_cta(P, K, t_lo, t_hi);
+}
+
 // the persistent kernel's rare edge items: a call keeps the general path's
 // register allocation (and spills) out of the interior path
 __device__ __noinline__ void edge_range_call(const BlochParams &P, const Chunk &K, long long t_lo, long long t_hi,
@@ -963,6 +974,11 @@ bloch_wave_kernel(const __grid_constant__ BlochParams P, const __grid_constant__
         };
         if (!item_range_s.edge) {
             interior_tile(P, K, SharedSpan{L, item_range_s}, hook);
+        } else if (item_range_s.edge == 2) {
+            const long long lo = item_range_s.lo, hi = item_range_s.hi;
+            hook();
+            __syncthreads();
+            edge_cta_call(P, K, lo, hi);
         } else {
             const long long lo = item_range_s.lo, hi = item_range_s.hi;
             hook();
