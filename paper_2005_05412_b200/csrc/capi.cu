@@ -347,15 +347,11 @@ BlochReal bloch_real(const BlochQm &b) {
                      1.0 + u,
                      4.0 * u,
                      b.az_c * b.az_c,
-                     1.0 - u,
                      b.pol_factor * b.mu_x * b.fxy,
                      b.fxy * b.fxy,
                      b.kz * b.kz,
                      b.kz * b.cz + b.cz,
-                     0.5 * (1.0 + u),
-                     0.5 * (1.0 - u),
-                     2.0 * b.az_c,
-                     2.0 * b.ax_s};
+                     0.5 * (1.0 + u)};
 }
 
 BlochParams bloch_params(const mbg_solver *s, const Launch &L) {

@@ -126,15 +126,11 @@ struct BlochReal {
     double c1;    // 1.0 + u
     double c4u;   // 4.0 * u
     double az2;   // az_c * az_c
-    double c2;    // 1.0 - u          (fast variant)
     double pfmu;  // pol_factor * mu_x * fxy (fast variant, relaxed-frame state)
     double f2;    // fxy * fxy
     double kz2;   // kz * kz
     double czz;   // kz * cz + cz
     double c1h;   // (1 + u) / 2
-    double c2h;   // (1 - u) / 2
-    double az2x;  // 2 az_c
-    double axs2;  // 2 ax_s
 };
 
 // Relaxed-frame state of the fast two-level path: the device holds each
