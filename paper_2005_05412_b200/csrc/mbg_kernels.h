@@ -50,6 +50,9 @@ __host__ __device__ constexpr int dense_tile_width(int n, bool rk4) {
     return n <= 3 ? 256 : (rk4 && n == 6 ? 96 : (n <= 6 ? 128 : 64));
 }
 __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) {
+#ifdef MBG_DENSE_MINB
+    if (n >= 5 && !rk4) return MBG_DENSE_MINB;  // tuning builds
+#endif
 #ifdef MBG_DENSE_MINB3
     if (n == 3 && !rk4) return MBG_DENSE_MINB3;
 #endif
