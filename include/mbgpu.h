@@ -28,6 +28,8 @@
  *   mbg_invariants        DensityKernel.invariant_stats            _kernels.py:394-401, 541-546
  *   mbg_batch_points      many Nx = 1 runs (ScalarKernel path)     solver_fdtd.py:89-96,347-349; _kernels.py:404-425
  *   mbg_pack_halo/unpack  (new) slab ghost exchange, no reference analogue
+ *   mbg_push_halo/pull    (new) the same exchange through peer device memory (the worker
+ *                         threads' shared arrays across the partition)  solver_fdtd.py:465-498
  *
  * Conventions: every function returns 0 on success or a negative MBG_E_*
  * code; mbg_last_error() gives the message.  All host pointers are plain
@@ -202,6 +204,35 @@ int mbg_batch_points(mbg_solver *s, int32_t B, const int32_t *medium, const doub
 int mbg_halo_words(const mbg_solver *s, int32_t *words);
 int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
 int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t dev_buf);
+
+/* Peer-memory ghost exchange (multi-device slabs without a library collective
+ * on the data path; the reference's counterpart is the shared arrays its
+ * worker threads read across the partition bounds, solver_fdtd.py:465-498).
+ * A mailbox is plain device memory owned by the RECEIVING rank, exported
+ * through CUDA IPC and mapped by the neighbour (mbg_mailbox_map in the
+ * neighbour's process; the same process passes the pointer itself).  The
+ * caller lays it out: per interface two slots of (2 + words) * count doubles
+ * and one zero-initialised 64-bit flag per slot.
+ *   mbg_push_halo: store `count` cells from `cell0` (E, H, state planes, the
+ *     mbg_pack_halo order) into the neighbour's slot and publish `seq` (> 0,
+ *     increasing per slot) in its flag with a system-scope release -- NVLink
+ *     stores on a multi-GPU box, ordered on the solver's stream.
+ *   mbg_pull_halo: wait on the device until the flag reaches `seq`, then copy
+ *     the slot into the ghost cells from `cell0`.  A strip that does not
+ *     arrive within timeout_ms leaves the ghosts stale and sets the handle's
+ *     sticky stall flag: the next mbg_synchronize / mbg_poll_nonfinite fails.
+ * Slot reuse needs no acknowledgement with two slots used alternately: a
+ * rank's push of period p + 2 is ordered after its pull of period p + 1, which
+ * waited for the neighbour's push of p + 1, itself ordered after the
+ * neighbour's pull of period p from the same slot. */
+#define MBG_IPC_HANDLE_BYTES 64
+int mbg_mailbox_alloc(int32_t device, int64_t bytes, uint64_t *dev_ptr, unsigned char *ipc_handle /* [64] or NULL */);
+int mbg_mailbox_free(int32_t device, uint64_t dev_ptr);
+int mbg_mailbox_map(int32_t device, const unsigned char *ipc_handle, uint64_t *dev_ptr);
+int mbg_mailbox_unmap(int32_t device, uint64_t dev_ptr);
+int mbg_push_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t peer_slot, uint64_t peer_flag, uint64_t seq);
+int mbg_pull_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t slot, uint64_t flag, uint64_t seq,
+                  int64_t timeout_ms);
 
 /* device-side checkpoint of E, H and the density state (save / restore the
  * current buffers; no reference analogue: FdtdSolver has no checkpointing) */

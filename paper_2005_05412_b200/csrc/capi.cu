@@ -80,6 +80,8 @@ struct mbg_solver {
     long long wave_cap = 0;
     WaveItem *wave_items = nullptr;  // work items of one chunk (fixed per solver)
     long long wave_n = 0;
+    unsigned *push_ticket = nullptr;  // peer-memory exchange: block ticket of the push kernel
+    bool peer_used = false;           // a pull may have set the stall flag (bit 1)
     long long launches = 0;
     std::string err;
 };
@@ -560,6 +562,7 @@ void mbg_destroy(mbg_solver *s) {
     dfree(st, s->inv);
     dfree(st, s->wave);
     dfree(st, s->wave_items);
+    dfree(st, s->push_ticket);
     dfree(st, s->ck_e);
     dfree(st, s->ck_h);
     dfree(st, s->ck_s);
@@ -1053,11 +1056,13 @@ int advance_wave(mbg_solver *s, long long first, long long n_steps, int tw) {
 // so a timeout is reported at the first synchronisation after it, however
 // many advances were enqueued in between; it is cleared once reported.
 int check_stall(mbg_solver *s) {
-    if (!s->wave) return MBG_OK;
+    if (!s->wave && !s->peer_used) return MBG_OK;
     unsigned v = 0;
     CK(cudaMemcpy(&v, s->bad + 1, sizeof(v), cudaMemcpyDeviceToHost));
     if (v) {
         CK(cudaMemset(s->bad + 1, 0, sizeof(unsigned long long)));
+        if (v & 2u)  // halo_pull_kernel: the ghosts of that period were left stale
+            return fail(s, MBG_E_CUDA, "peer halo exchange: a neighbour's strip did not arrive within the timeout");
         return fail(s, MBG_E_CUDA, "persistent step kernel: dependency wait timed out");
     }
     return MBG_OK;
@@ -1420,6 +1425,95 @@ static int halo(mbg_solver *s, bool pack, int64_t cell0, int64_t count, uint64_t
 
 int mbg_pack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, true, cell0, count, buf); }
 int mbg_unpack_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t buf) { return halo(s, false, cell0, count, buf); }
+
+/* ---- peer-memory ghost exchange (kernels_aux.cu: halo_push_kernel / halo_pull_kernel) ---- */
+
+int mbg_mailbox_alloc(int32_t device, int64_t bytes, uint64_t *dev_ptr, unsigned char *ipc) {
+    mbg_solver *s = nullptr;
+    if (!dev_ptr || bytes <= 0) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    void *p = nullptr;
+    CK(cudaMalloc(&p, (size_t)bytes));  // plain cudaMalloc: pool memory cannot be exported
+    cudaError_t e = cudaMemset(p, 0, (size_t)bytes);
+    if (e == cudaSuccess && ipc) {
+        static_assert(sizeof(cudaIpcMemHandle_t) == MBG_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t hnd;
+        e = cudaIpcGetMemHandle(&hnd, p);
+        if (e == cudaSuccess) std::memcpy(ipc, &hnd, sizeof(hnd));
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        CK(e);
+    }
+    *dev_ptr = reinterpret_cast<uint64_t>(p);
+    return MBG_OK;
+}
+
+int mbg_mailbox_free(int32_t device, uint64_t dev_ptr) {
+    mbg_solver *s = nullptr;
+    if (!dev_ptr) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    CK(cudaFree(reinterpret_cast<void *>(dev_ptr)));
+    return MBG_OK;
+}
+
+int mbg_mailbox_map(int32_t device, const unsigned char *ipc, uint64_t *dev_ptr) {
+    mbg_solver *s = nullptr;
+    if (!ipc || !dev_ptr) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, ipc, sizeof(hnd));
+    void *p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = reinterpret_cast<uint64_t>(p);
+    return MBG_OK;
+}
+
+int mbg_mailbox_unmap(int32_t device, uint64_t dev_ptr) {
+    mbg_solver *s = nullptr;
+    if (!dev_ptr) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    CK(cudaIpcCloseMemHandle(reinterpret_cast<void *>(dev_ptr)));
+    return MBG_OK;
+}
+
+static int halo_range(mbg_solver *s, int64_t cell0, int64_t count, long long *l0) {
+    *l0 = cell0 - s->g.win_lo;
+    if (*l0 < 0 || *l0 + count > s->win_n) return fail(s, MBG_E_ARG, "halo range outside the window");
+    return MBG_OK;
+}
+
+int mbg_push_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t peer_slot, uint64_t peer_flag, uint64_t seq) {
+    if (!s || !peer_slot || !peer_flag || count <= 0 || !seq) return MBG_E_ARG;
+    long long l0 = 0;
+    if (int rc = halo_range(s, cell0, count, &l0)) return rc;
+    cudaSetDevice(s->g.device);
+    if (!s->push_ticket) {
+        CK(dalloc(s->stream, reinterpret_cast<double **>(&s->push_ticket), sizeof(double)));
+        CK(cudaMemsetAsync(s->push_ticket, 0, sizeof(double), s->stream));
+    }
+    CK(launch_halo_push(s->e[s->cur], s->h[s->cur], s->s[s->cur], s->plane, s->words, l0, count,
+                        reinterpret_cast<double *>(peer_slot), reinterpret_cast<unsigned long long *>(peer_flag),
+                        seq, s->push_ticket, s->stream));
+    ++s->launches;
+    return MBG_OK;
+}
+
+int mbg_pull_halo(mbg_solver *s, int64_t cell0, int64_t count, uint64_t slot, uint64_t flag, uint64_t seq,
+                  int64_t timeout_ms) {
+    if (!s || !slot || !flag || count <= 0 || !seq || timeout_ms <= 0) return MBG_E_ARG;
+    long long l0 = 0;
+    if (int rc = halo_range(s, cell0, count, &l0)) return rc;
+    cudaSetDevice(s->g.device);
+    s->peer_used = true;
+    CK(launch_halo_pull(s->e[s->cur], s->h[s->cur], s->s[s->cur], s->plane, s->words, l0, count,
+                        reinterpret_cast<const double *>(slot), reinterpret_cast<const unsigned long long *>(flag),
+                        seq, (unsigned long long)timeout_ms * 1000000ull, reinterpret_cast<unsigned *>(s->bad + 1),
+                        s->stream));
+    ++s->launches;
+    return MBG_OK;
+}
 
 int mbg_checkpoint_save(mbg_solver *s) {
     if (!s) return MBG_E_ARG;

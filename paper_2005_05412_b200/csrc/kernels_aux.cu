@@ -115,6 +115,83 @@ __global__ void halo_kernel(bool pack, double *e, double *h, double *s, long lon
         *p = buf[t];
 }
 
+// Peer-memory ghost exchange (no library collective on the data path).  The
+// receiver owns a mailbox per interface: two slots of [E | H | state planes] x
+// count doubles and one 64-bit sequence flag per slot.  The sender's push
+// kernel stores its edge cells straight into the receiver's slot -- peer
+// device memory mapped through CUDA IPC, NVLink stores on a multi-GPU box --
+// and the last block to finish publishes the period's sequence number with a
+// system-scope release; the receiver's pull kernel acquires the flag and
+// copies the slot into its ghost cells.  Neither kernel is ever waited on by
+// the sender, so the exchange cannot deadlock; a strip that does not arrive
+// within the timeout sets the handle's sticky stall flag (bit 1) instead.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long aux_global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ double *halo_word(double *e, double *h, double *s, long long plane, long long l0,
+                                             long long count, long long t) {
+    const long long w = t / count, l = l0 + t % count;
+    MBG_CHK(l, plane, "halo cell");
+    return (w == 0) ? e + l : (w == 1) ? h + l : s + (w - 2) * plane + l;
+}
+
+__global__ void __launch_bounds__(256) halo_push_kernel(double *e, double *h, double *s, long long plane, int words,
+                                                        long long l0, long long count, double *slot,
+                                                        unsigned long long *flag, unsigned long long seq,
+                                                        unsigned *ticket) {
+    const long long total = (long long)(2 + words) * count;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x)
+        slot[t] = *halo_word(e, h, s, plane, l0, count, t);
+    __threadfence_system();  // this thread's stores before its block's ticket
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned done = atomicAdd(ticket, 1u);
+        if (done == gridDim.x - 1) {  // every block's stores are ordered before its ticket
+            *ticket = 0;              // re-armed for the next push on this stream
+            __threadfence_system();
+            st_release_sys(flag, seq);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) halo_pull_kernel(double *e, double *h, double *s, long long plane, int words,
+                                                        long long l0, long long count, const double *slot,
+                                                        const unsigned long long *flag, unsigned long long seq,
+                                                        unsigned long long timeout_ns, unsigned *stall) {
+    __shared__ int arrived;
+    if (threadIdx.x == 0) {
+        const unsigned long long t0 = aux_global_ns();
+        int ok = 1;
+        while (ld_acquire_sys(flag) < seq) {
+            if (aux_global_ns() - t0 > timeout_ns) {
+                ok = 0;
+                atomicOr(stall, 2u);
+                break;
+            }
+            __nanosleep(200);
+        }
+        arrived = ok;
+    }
+    __syncthreads();
+    if (!arrived) return;  // ghosts stay stale; the host reports the stall at its next synchronisation
+    const long long total = (long long)(2 + words) * count;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x)
+        *halo_word(e, h, s, plane, l0, count, t) = __ldcg(slot + t);
+}
+
 // 16 independent FMA chains per thread keep the DFMA pipe busy
 __global__ void __launch_bounds__(256) fp64_fma_kernel(double *out, int iters, double m, double c) {
     double a[16];
@@ -390,6 +467,29 @@ cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long pl
     const long long total = (long long)(2 + words) * count;
     if (total <= 0) return cudaSuccess;
     halo_kernel<<<blocks_for(total, 256), 256, 0, st>>>(pack, e, h, s, plane, words, l0, count, buf);
+    return cudaGetLastError();
+}
+
+static unsigned halo_blocks(long long total) {
+    const long long b = (total + 255) / 256;
+    return (unsigned)(b < 1 ? 1 : (b > 64 ? 64 : b));
+}
+
+cudaError_t launch_halo_push(double *e, double *h, double *s, long long plane, int words, long long l0,
+                             long long count, double *slot, unsigned long long *flag, unsigned long long seq,
+                             unsigned *ticket, cudaStream_t st) {
+    const long long total = (long long)(2 + words) * count;
+    halo_push_kernel<<<halo_blocks(total), 256, 0, st>>>(e, h, s, plane, words, l0, count, slot, flag, seq, ticket);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pull(double *e, double *h, double *s, long long plane, int words, long long l0,
+                             long long count, const double *slot, const unsigned long long *flag,
+                             unsigned long long seq, unsigned long long timeout_ns, unsigned *stall,
+                             cudaStream_t st) {
+    const long long total = (long long)(2 + words) * count;
+    halo_pull_kernel<<<halo_blocks(total), 256, 0, st>>>(e, h, s, plane, words, l0, count, slot, flag, seq,
+                                                        timeout_ns, stall);
     return cudaGetLastError();
 }
 

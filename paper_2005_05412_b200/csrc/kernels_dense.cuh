@@ -493,7 +493,10 @@ template <int N, bool RK4>
 struct Layout {
     static constexpr int NW = N * N;
     static constexpr bool kRegState = RK4 ? (N <= 3) : (N <= 4);
-    static constexpr bool kRegG = N <= 6;
+#ifndef MBG_REG_G_MAX
+#define MBG_REG_G_MAX 6
+#endif
+    static constexpr bool kRegG = N <= MBG_REG_G_MAX;
     // smem words per thread: A/B (or A/S/K/Acc for RK4) when not in registers, G when not in regs
     static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 3 * NW : 2 * NW);
     static constexpr int kGWords = (RK4 || kRegG) ? 0 : 2 * NW;

@@ -121,6 +121,17 @@ cudaError_t launch_broadcast_state(double *s, long long plane, long long win_n, 
 cudaError_t launch_halo(bool pack, double *e, double *h, double *s, long long plane, int words,
                         long long l0, long long count, double *buf, cudaStream_t st);
 
+// peer-memory ghost exchange: store the cells into the receiver's mailbox slot
+// and publish `seq` in its flag (push); wait for `seq`, copy the slot into the
+// ghost cells (pull; sets bit 1 of *stall after timeout_ns without the strip)
+cudaError_t launch_halo_push(double *e, double *h, double *s, long long plane, int words, long long l0,
+                             long long count, double *slot, unsigned long long *flag, unsigned long long seq,
+                             unsigned *ticket, cudaStream_t st);
+cudaError_t launch_halo_pull(double *e, double *h, double *s, long long plane, int words, long long l0,
+                             long long count, const double *slot, const unsigned long long *flag,
+                             unsigned long long seq, unsigned long long timeout_ns, unsigned *stall,
+                             cudaStream_t st);
+
 // invariant monitor: out[0] max |trace - 1|, out[1] max Hermiticity deviation
 // (0: packed storage), out[2] min eigenvalue, as order-preserving uint64 keys
 cudaError_t launch_invariants(const Launch &L, int levels, int bloch, const BlochFrame &F, unsigned long long *out,

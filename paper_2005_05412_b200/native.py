@@ -91,6 +91,12 @@ SIGNATURES = {
     "mbg_halo_words": (C.c_int, [_h, _i32p]),
     "mbg_pack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
     "mbg_unpack_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64]),
+    "mbg_mailbox_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_uint64), C.c_char_p]),
+    "mbg_mailbox_free": (C.c_int, [C.c_int32, C.c_uint64]),
+    "mbg_mailbox_map": (C.c_int, [C.c_int32, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "mbg_mailbox_unmap": (C.c_int, [C.c_int32, C.c_uint64]),
+    "mbg_push_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_uint64]),
+    "mbg_pull_halo": (C.c_int, [_h, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64]),
     "mbg_checkpoint_save": (C.c_int, [_h]),
     "mbg_checkpoint_restore": (C.c_int, [_h]),
     "mbg_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
@@ -101,6 +107,8 @@ SIGNATURES = {
     "mbg_mark_elapsed": (C.c_int, [_h, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "mbg_launch_count": (C.c_int, [_h, _i64p]),
 }
+
+MBG_IPC_HANDLE_BYTES = 64  # include/mbgpu.h
 
 _LIB = None
 

@@ -23,6 +23,12 @@ Transports:
     path, no kernel ever waits on another).
   * :class:`TorchTransport` -- one process per GPU, ``torch.distributed``
     batched isend/irecv (NCCL over NVLink on the B200 box, gloo on CPU).
+  * :class:`PeerTransport` -- one process per GPU, no library collective on
+    the data path: every rank owns a device mailbox per interface, exported
+    through CUDA IPC; the neighbour's push kernel stores its edge cells
+    straight into it (NVLink stores) and publishes a sequence flag, the
+    owner's pull kernel acquires the flag and fills the ghosts
+    (``mbg_push_halo`` / ``mbg_pull_halo``).  The default under NCCL.
 """
 
 from __future__ import annotations
@@ -196,7 +202,9 @@ class EdgeStrips:
     def run(self, first: int, count: int, main_stream, send: dict):
         """Enqueue one period: copy the strips' 3g cells from the slab (main
         stream), then on the side stream advance them ``count`` steps and pack
-        the sent cells into ``send[side]`` (device tensors)."""
+        the sent cells into ``send[side]`` (device tensors) -- or, when
+        ``send`` is a peer transport's sender, push them into the neighbour's
+        mailbox (``send.push``)."""
         import torch
 
         for h, win, own, scratch in self.sides.values():
@@ -207,7 +215,10 @@ class EdgeStrips:
         for side, (h, win, own, scratch) in self.sides.items():
             h.call("mbg_unpack_halo", win[0], win[1] - win[0], scratch.data_ptr())
             h.call("mbg_advance", first, count)
-            h.call("mbg_pack_halo", own[0], own[1] - own[0], send[side].data_ptr())
+            if hasattr(send, "push"):  # peer mailboxes: the strip stores into the neighbour's memory itself
+                send.push(side, h, own[0], own[1] - own[0])
+            else:
+                h.call("mbg_pack_halo", own[0], own[1] - own[0], send[side].data_ptr())
 
     def close(self):
         for h, *_ in self.sides.values():
@@ -364,6 +375,238 @@ class TorchTransport:
         self.finish()
 
 
+class Mailbox:
+    """Device memory a neighbour stores its ghost strips into (include/mbgpu.h,
+    mbg_push_halo): a 128-byte header holding the two slot flags, then two
+    slots of ``doubles`` doubles.  Owned (allocated here, exportable through
+    CUDA IPC) or mapped from a neighbour's exported handle."""
+
+    HEADER = 128
+
+    def __init__(self, device: int, doubles: int, ipc: bytes | None = None):
+        self.lib = native.load()
+        self.device, self.doubles = int(device), int(doubles)
+        ptr = C.c_uint64(0)
+        self.owned = ipc is None
+        if self.owned:
+            buf = C.create_string_buffer(native.MBG_IPC_HANDLE_BYTES)
+            rc = self.lib.mbg_mailbox_alloc(self.device, self.HEADER + 16 * self.doubles, C.byref(ptr), buf)
+            self.ipc = buf.raw
+        else:
+            rc = self.lib.mbg_mailbox_map(self.device, ipc, C.byref(ptr))
+            self.ipc = ipc
+        if rc != 0:
+            raise native.NativeError(f"peer mailbox {'allocation' if self.owned else 'mapping'} failed ({rc})")
+        self.ptr = ptr.value
+
+    def flag(self, slot: int) -> int:
+        return self.ptr + 8 * slot
+
+    def slot(self, slot: int) -> int:
+        return self.ptr + self.HEADER + 8 * self.doubles * slot
+
+    def close(self):
+        if getattr(self, "ptr", 0):
+            (self.lib.mbg_mailbox_free if self.owned else self.lib.mbg_mailbox_unmap)(self.device, self.ptr)
+            self.ptr = 0
+
+
+PULL_TIMEOUT_MS = 30000
+
+
+def _pull_timeout() -> int:
+    import os
+
+    return int(os.environ.get("MBG_PULL_TIMEOUT_MS", PULL_TIMEOUT_MS))
+
+
+class _PeerSender:
+    """What EdgeStrips.run receives as ``send`` under a peer transport."""
+
+    def __init__(self, push):
+        self.push = push
+
+
+class LocalPeerTransport:
+    """All slabs in this process on one device, ghosts through peer mailboxes:
+    the push / pull kernels and the slot and sequence protocol of
+    :class:`PeerTransport` without a second process (every push is enqueued
+    before the pull that waits for it, on one stream: no kernel ever waits)."""
+
+    def __init__(self, states):
+        self.states = states
+        self.seq = 0
+        dev = states[0].solver.gpu
+        self.box = []  # per slab: side -> Mailbox it receives in
+        for st in states:
+            _, rl, _, rr = exchange_plan(st.slab)
+            self.box.append({side: Mailbox(dev, st.words * spec[1])
+                             for side, spec in (("left", rl), ("right", rr)) if spec is not None})
+
+    def _push(self, i, side, handle, cell0, count):
+        seq = self.seq + 1
+        box = self.box[i - 1]["right"] if side == "left" else self.box[i + 1]["left"]
+        handle.call("mbg_push_halo", cell0, count, box.slot(seq & 1), box.flag(seq & 1), seq)
+
+    def sender(self, i):
+        return _PeerSender(lambda side, handle, cell0, count: self._push(i, side, handle, cell0, count))
+
+    def _pull_all(self):
+        self.seq += 1
+        for st, box in zip(self.states, self.box):
+            _, rl, _, rr = exchange_plan(st.slab)
+            for side, spec in (("left", rl), ("right", rr)):
+                if spec is not None:
+                    b = box[side]
+                    st.h.call("mbg_pull_halo", spec[0], spec[1], b.slot(self.seq & 1), b.flag(self.seq & 1),
+                              self.seq, _pull_timeout())
+        for st in self.states:
+            st.h.call("mbg_synchronize")
+
+    def exchange(self):
+        for i, st in enumerate(self.states):
+            sl, _, sr, _ = exchange_plan(st.slab)
+            if sl is not None:
+                self._push(i, "left", st.h, sl[0], sl[1])
+            if sr is not None:
+                self._push(i, "right", st.h, sr[0], sr[1])
+        self._pull_all()
+
+    def exchange_from(self, sends):
+        self._pull_all()  # the edge strips pushed through sender(i)
+
+    def close(self):
+        for box in self.box:
+            for b in box.values():
+                b.close()
+        self.box = []
+
+
+class PeerTransport:
+    """One slab per process; ghost strips travel as stores into the
+    neighbour's device memory, with no library collective on the data path.
+
+    Setup (once): every rank allocates a :class:`Mailbox` per interface and the
+    CUDA IPC handles go round with one ``all_gather_object``; each rank maps
+    its neighbours' boxes (peer access over NVLink on a multi-GPU box, plain
+    device memory when ranks share a GPU).  Per period: ``mbg_push_halo``
+    stores the edge cells into the neighbour's slot ``seq & 1`` and publishes
+    ``seq`` in its flag; ``mbg_pull_halo`` waits on the device for the flag and
+    copies the slot into the ghosts.  Two slots need no acknowledgement (see
+    include/mbgpu.h).  The host never waits inside the step loop.
+
+    ``host_ordered`` (ranks sharing one GPU, tests and the one-GPU bench):
+    every rank drains its device and meets the others on the host before the
+    pulls are enqueued, so no kernel of one rank ever waits on a kernel of
+    another rank on the same GPU."""
+
+    def __init__(self, state: SlabState, device, side_stream=None, host_ordered: bool = False):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.state, self.side_stream, self.host_ordered = state, side_stream, host_ordered
+        self.device = torch.device(device)
+        self.plan = exchange_plan(state.slab)
+        sl, rl, sr, rr = self.plan
+        idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        w = state.words
+        self.box = {side: Mailbox(idx, w * spec[1]) for side, spec in (("left", rl), ("right", rr))
+                    if spec is not None}
+        mine = {side: (b.ipc, b.doubles) for side, b in self.box.items()}
+        every = [None] * dist.get_world_size()
+        dist.all_gather_object(every, mine)
+        rank = state.slab.rank
+        self.peer = {}
+        if sl is not None:  # what I send left lands in the left neighbour's right box
+            ipc, doubles = every[rank - 1]["right"]
+            self.peer["left"] = Mailbox(idx, doubles, ipc=ipc)
+        if sr is not None:
+            ipc, doubles = every[rank + 1]["left"]
+            self.peer["right"] = Mailbox(idx, doubles, ipc=ipc)
+        self.seq = 0
+
+    @property
+    def send(self):
+        return _PeerSender(self.push)
+
+    def push(self, side, handle, cell0, count):
+        seq = self.seq + 1
+        box = self.peer[side]
+        handle.call("mbg_push_halo", cell0, count, box.slot(seq & 1), box.flag(seq & 1), seq)
+
+    def start(self, packed: bool = False):
+        sl, _, sr, _ = self.plan
+        if not packed:
+            if sl is not None:
+                self.push("left", self.state.h, sl[0], sl[1])
+            if sr is not None:
+                self.push("right", self.state.h, sr[0], sr[1])
+        self.seq += 1
+
+    def finish(self):
+        _, rl, _, rr = self.plan
+        if self.host_ordered:
+            self.torch.cuda.synchronize(self.device)  # this rank's pushes have landed ...
+            self.dist.barrier()                       # ... and so have everyone else's
+        for side, spec in (("left", rl), ("right", rr)):
+            if spec is not None:
+                b = self.box[side]
+                self.state.h.call("mbg_pull_halo", spec[0], spec[1], b.slot(self.seq & 1), b.flag(self.seq & 1),
+                                  self.seq, _pull_timeout())
+
+    def exchange(self):
+        self.start()
+        self.finish()
+
+    def close(self):
+        self.torch.cuda.synchronize(self.device)
+        for b in self.peer.values():
+            b.close()
+        self.peer = {}
+        self.dist.barrier()  # nobody still maps a box when its owner frees it
+        for b in self.box.values():
+            b.close()
+        self.box = {}
+
+
+def exchange_mode(backend: str) -> str:
+    """``MBG_SLAB_EXCHANGE`` = ``p2p`` (peer mailboxes) or ``nccl`` (batched
+    isend/irecv; under gloo the host-staged send/recv).  Default: p2p under
+    NCCL, send/recv under gloo."""
+    import os
+
+    mode = os.environ.get("MBG_SLAB_EXCHANGE", "p2p" if backend == "nccl" else "nccl")
+    if mode not in ("p2p", "nccl"):
+        raise ValueError(f"MBG_SLAB_EXCHANGE must be p2p or nccl, not {mode!r}")
+    return mode
+
+
+def make_transport(state: SlabState, device, side_stream=None):
+    """The rank's ghost transport (torch.distributed initialised): peer
+    mailboxes when asked for / by default under NCCL -- if every rank could
+    set them up (CUDA IPC between the GPUs), else the send/recv transport."""
+    import warnings
+
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend()
+    if torch.device(device).type == "cuda" and dist.get_world_size() > 1 and exchange_mode(backend) == "p2p":
+        tr, err = None, None
+        try:
+            tr = PeerTransport(state, device, side_stream=side_stream, host_ordered=(backend != "nccl"))
+        except Exception as exc:  # IPC unavailable between these devices: every rank must agree
+            err = exc
+        ok = int(_reduce_scalar(0 if tr is None else 1, dist.ReduceOp.MIN, device, torch.int64))
+        if ok:
+            return tr
+        if tr is not None:
+            tr.close()
+        warnings.warn(f"peer mailboxes unavailable ({err}); ghost exchange by send/recv")
+    return TorchTransport(state, device, side_stream=side_stream)
+
+
 # ---------------------------------------------------------------- drivers --
 
 def _step_loop(grid, period, step_period, poll, poll_every=1 << 14):
@@ -390,11 +633,13 @@ def _check_monitor(solver):
                                   "use GpuFdtdSolver.run() for a monitored run")
 
 
-def run_slabs_local(solver, slabs_count: int, period=None, overlap: bool = False):
+def run_slabs_local(solver, slabs_count: int, period=None, overlap: bool = False, exchange: str = "copy"):
     """Run ``solver``'s scenario as ``slabs_count`` slabs on one device (tests);
     ``period`` = steps between exchanges (default exchange_period);
     ``overlap``: the sent cells come from edge strips (EdgeStrips) on a side
-    stream instead of the slabs themselves."""
+    stream instead of the slabs themselves; ``exchange``: ``"copy"`` (pack /
+    unpack through one scratch buffer) or ``"p2p"`` (peer mailboxes,
+    :class:`LocalPeerTransport`)."""
     if solver._ran:
         raise SolverError("run() may only be called once per solver instance")
     _check_monitor(solver)
@@ -410,12 +655,15 @@ def run_slabs_local(solver, slabs_count: int, period=None, overlap: bool = False
     states = [SlabState(solver, s, stream=stream.cuda_stream) for s in slabs]
     strips, sends = [], []
     try:
-        tr = LocalTransport(states)
+        tr = LocalPeerTransport(states) if exchange == "p2p" else LocalTransport(states)
         if overlap:
             side = torch.cuda.Stream(device=device, priority=-1)
             strips = [EdgeStrips(st, period, side) for st in states]
-            sends = [{k2: torch.empty(st.words * period, dtype=torch.float64, device=device) for k2 in sp.sides}
-                     for st, sp in zip(states, strips)]
+            if exchange == "p2p":
+                sends = [tr.sender(i) for i in range(len(states))]
+            else:
+                sends = [{k2: torch.empty(st.words * period, dtype=torch.float64, device=device)
+                          for k2 in sp.sides} for st, sp in zip(states, strips)]
         for st in states:
             st.sample(0)
 
@@ -444,6 +692,8 @@ def run_slabs_local(solver, slabs_count: int, period=None, overlap: bool = False
             sp.close()
         for st in states:
             st.close()
+        if exchange == "p2p" and "tr" in locals():
+            tr.close()
     solver.results = [p.to_result(solver.grid, d) for p, d in zip(solver.plan.plans, recs)]
     return solver.results
 
@@ -550,7 +800,7 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     strips = None
     try:
         with torch.cuda.stream(stream) if stream is not None else _nullcontext():
-            tr = TorchTransport(st, device, side_stream=side)
+            tr = make_transport(st, device, side_stream=side)
             if overlap:
                 strips = EdgeStrips(st, period, side)
             st.sample(0)
@@ -575,6 +825,8 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     finally:
         if strips is not None:
             strips.close()
+        if hasattr(locals().get("tr"), "close"):
+            tr.close()
         st.close()
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(mine, gathered, dst=0)
@@ -608,7 +860,7 @@ class SlabTimer:
         self.strips = None
         with torch.cuda.stream(self.stream):
             if world > 1:
-                self.tr = TorchTransport(self.st, device, side_stream=self.side)
+                self.tr = make_transport(self.st, device, side_stream=self.side)
                 if overlap:
                     self.strips = EdgeStrips(self.st, self.period, self.side)
         self.st.h.call("mbg_checkpoint_save")
@@ -679,6 +931,8 @@ class SlabTimer:
     def close(self):
         if self.strips is not None:
             self.strips.close()
+        if hasattr(self.tr, "close"):
+            self.tr.close()
         self.st.close()
 
 
@@ -715,6 +969,7 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
     sampler = clock_sampler(local) if clock_sampler is not None else None
     ms = timer.time(args.steps, warmup=args.warmup, sampler=sampler)
     launches = timer.timed_launches
+    peer = isinstance(timer.tr, PeerTransport)
     timer.close()
     cells = grid.num_x * (grid.num_t - 1) * args.steps
 
@@ -757,8 +1012,10 @@ def bench_rank(args, dev, sce, world, rank, local, metric, unit, clock_sampler=N
                                    f"cells, 20000 steps", "num_x": grid.num_x, "parallelism": f"slab{world}"},
             "implementation": {
                 "tile_steps": k, "exchange_period": period,
-                "exchange": f"NCCL batched isend/irecv of {period} ghost cells per interface every "
-                            f"{period} steps (one persistent launch of {period // k} chunks between)"},
+                "exchange": (f"peer mailboxes (mbg_push_halo stores into the neighbour's device memory, "
+                             f"mbg_pull_halo acquires the flag)" if peer else f"{backend} batched isend/irecv")
+                            + f" of {period} ghost cells per interface every {period} steps (one persistent "
+                              f"launch of {period // k} chunks between)"},
             "e2e": e2e,
             # this rank's kernels (step, step-mask, sample, halo pack/unpack; library count)
             "gpu_launches": int(launches),

@@ -146,6 +146,53 @@ def test_edge_strips_match_single_domain(case, count, period):
         assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,count,period,overlap", [("cfg2_r16", 3, None, False), ("multi_material", 2, 64, False),
+                                                       ("cfg4_r14", 4, None, False), ("rand3_split", 3, 29, False),
+                                                       ("rand6_split", 3, None, True), ("rand4_rk4", 2, None, True),
+                                                       ("cfg2_r16", 8, None, False)])
+def test_peer_mailboxes_in_one_process_match_single_domain(case, count, period, overlap):
+    """The peer-memory exchange (mbg_push_halo / mbg_pull_halo: slots, sequence
+    flags, two-slot reuse) between slabs of one process, with and without edge
+    strips pushing from their side stream: bit-identical to the single domain."""
+    dev, sce, stepper = build_case(case)
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    mb.clear_material_library()
+    dev, sce, stepper = build_case(case)
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
+    got = slabs.run_slabs_local(solver, count, period, overlap=overlap, exchange="p2p")
+    for a, b in zip(ref, got):
+        assert a.name == b.name and a.data.shape == b.data.shape
+        assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), a.name
+
+
+@pytest.mark.gpu
+def test_pull_without_a_push_times_out_and_is_reported():
+    """A strip that never arrives: the pull kernel gives up after its timeout,
+    leaves the ghosts alone and the next synchronisation raises."""
+    import ctypes as C
+
+    from paper_2005_05412_b200 import native
+
+    dev, sce, stepper = build_case("multi_material")
+    solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
+    slab = slabs.partition(solver.grid.num_x, 2, 64)[1]
+    st = slabs.SlabState(solver, slab)
+    box = slabs.Mailbox(solver.gpu, st.words * slab.ghost_left)
+    try:
+        st.h.call("mbg_pull_halo", slab.win_lo, slab.ghost_left, box.slot(1), box.flag(1), 1, 50)
+        with pytest.raises(native.NativeError, match="did not arrive"):
+            st.h.call("mbg_synchronize")
+        st.h.call("mbg_synchronize")  # reported once, then cleared
+        # a push with the awaited sequence number makes the same pull succeed
+        st.h.call("mbg_push_halo", slab.own_lo, slab.ghost_left, box.slot(1), box.flag(1), 1)
+        st.h.call("mbg_pull_halo", slab.win_lo, slab.ghost_left, box.slot(1), box.flag(1), 1, 50)
+        st.h.call("mbg_synchronize")
+    finally:
+        st.close()
+        box.close()
+
+
 def _nccl_single(fn):
     """Run fn() inside a one-rank NCCL process group (the only NCCL shape one GPU allows)."""
     import torch
@@ -240,6 +287,27 @@ def test_native_ranks_sharing_one_gpu_match_single_domain(world, case, period, o
     """run_slab_rank across processes with the native slab kernels: the
     TorchTransport exchange plan, pack/unpack on the adopted stream, scan-flag
     reduction and record gather, bit-identical to the single-domain run."""
+    dev, sce, stepper = build_case(case)
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "recs.npz")
+        mp.spawn(_gpu_worker, args=(world, _free_port(), case, period, out, overlap), nprocs=world, join=True)
+        got = np.load(out)
+        for r, a in enumerate(ref):
+            have = got[f"arr_{r}"]
+            assert have.shape == a.data.shape, a.name
+            assert np.array_equal(have, a.data), (a.name, np.max(np.abs(have - a.data)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,case,period,overlap", [(2, "multi_material", None, None), (3, "cfg2_r16", None, None),
+                                                       (2, "rand6_split", None, True), (3, "rand3_split", 29, None)])
+def test_peer_mailboxes_across_processes_match_single_domain(world, case, period, overlap, monkeypatch):
+    """PeerTransport between processes: mailboxes exported through CUDA IPC,
+    mapped by the neighbour rank, strips stored into them by the neighbour's
+    push kernel.  The ranks share cuda:0 here, so the transport runs host
+    ordered (no kernel of one rank waits on another rank's kernel)."""
+    monkeypatch.setenv("MBG_SLAB_EXCHANGE", "p2p")
     dev, sce, stepper = build_case(case)
     ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
     with tempfile.TemporaryDirectory() as d:
