@@ -5,7 +5,7 @@
 // two-level kernel).  The per-cell density matrix never leaves the SM while
 // the launch runs: it is Hermitian-packed (N real diagonal words, then re/im
 // of the upper triangle in row-major order) in registers for N <= 4 and in a
-// per-thread shared-memory column for larger N.  E and H live in registers;
+// per-thread shared-memory column for larger N (G always in registers).  E and H live in registers;
 // neighbours are exchanged through two small double-buffered shared arrays
 // (two barriers per step).
 //
@@ -50,19 +50,10 @@ struct SmemVec {
 };
 template <int N>
 struct RegMat {
-    static constexpr bool kShared = false;
     double re[N * N], im[N * N];
     __device__ __forceinline__ double &r(int i, int j) { return re[i * N + j]; }
     __device__ __forceinline__ double &m(int i, int j) { return im[i * N + j]; }
 };
-template <int N, int TW>
-struct SmemMat {
-    static constexpr bool kShared = true;
-    SmemVec<TW> re, im;
-    __device__ __forceinline__ double &r(int i, int j) { return re[i * N + j]; }
-    __device__ __forceinline__ double &m(int i, int j) { return im[i * N + j]; }
-};
-
 // Hermitian element (i, j) of a packed state
 template <int N, class V>
 __device__ __forceinline__ void herm(V &s, int i, int j, double &re, double &im) {
@@ -105,121 +96,6 @@ struct SymMat {
 template <int N, class VA, class VB, class MG, class VR>
 __device__ __forceinline__ double congruence(const DenseQm<N> &q, VA &A, VB &B, MG &G, VR &raw);
 
-// Rolled inversion and congruence for N >= 7 (G and the state in shared
-// memory, dynamically indexed): the loops over pivots and rows are real
-// loops.  Fully unrolled, one cell step is 100 KB (N = 7) to 160 KB (N = 8) of
-// straight-line code -- more than the instruction cache holds, so every step
-// streamed its code from L2 (N = 8: 8.4e7 cell-updates/s, a twentieth of the
-// flop-proportional rate) -- and the compiler forwarded G through registers
-// into local memory (2900 LDL + 2500 STL per cell step).  The arithmetic per
-// element is the unrolled code's, operation for operation: the pivot column
-// takes the general update with a zero addend (fma(a, b, 0) = a * b).
-template <int N, class VA, class VB, class MG, class VR>
-__device__ __forceinline__ double split_rolled(const DenseQm<N> &q, double e, VA &A, VB &B, MG &G, VR &raw) {
-#ifndef MBG_ROLL_U
-#define MBG_ROLL_U 2
-#endif
-    constexpr int kRollU = MBG_ROLL_U;  // rows per iteration of the rolled row loops
-#pragma unroll 1
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            G.r(i, j) = mad(e, q.bf_re[i * N + j], q.bc_re[i * N + j]);
-            G.m(i, j) = mad(e, q.bf_im[i * N + j], q.bc_im[i * N + j]);
-        }
-#pragma unroll 1
-    for (int k = 0; k < N; ++k) {
-        const double pr = G.r(k, k), pi = G.m(k, k);
-        const double rd = recip_pos(mad(pi, pi, pr * pr));
-        const double ir = pr * rd, ii = -pi * rd;
-        double kr[N], ki[N];  // the scaled pivot row (the inverse pivot in column k)
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            const double xr = G.r(k, j), xi = G.m(k, j);
-            const double nr = mad(xr, ir, -(xi * ii)), ni = mad(xr, ii, xi * ir);
-            kr[j] = j == k ? ir : nr;
-            ki[j] = j == k ? ii : ni;
-            G.r(k, j) = kr[j];
-            G.m(k, j) = ki[j];
-        }
-#pragma unroll kRollU
-        for (int i = 0; i < N; ++i) {
-            if (i == k) continue;
-            const double fr = G.r(i, k), fi = G.m(i, k);
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const double gr = j == k ? 0.0 : G.r(i, j), gi = j == k ? 0.0 : G.m(i, j);
-                G.r(i, j) = mad(-fr, kr[j], mad(fi, ki[j], gr));
-                G.m(i, j) = mad(-fr, ki[j], mad(-fi, kr[j], gi));
-            }
-        }
-    }
-    // U = G - I; rho' = U r1 U^H row by row (congruence<N>, rolled over the rows)
-    double acc_p = 0.0;
-#pragma unroll 1
-    for (int i = 0; i < N; ++i) {
-        double ur[N], ui[N], tr[N], ti[N];
-#pragma unroll
-        for (int m = 0; m < N; ++m) {
-            ur[m] = m == i ? G.r(i, m) - 1.0 : G.r(i, m);
-            ui[m] = G.m(i, m);
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            double ar = 0.0, ai = 0.0;
-#pragma unroll
-            for (int m = 0; m < N; ++m) {
-                if (m == k) {  // real diagonal of r1
-                    const double rr = B[m];
-                    ar = mad(ur[m], rr, ar);
-                    ai = mad(ui[m], rr, ai);
-                } else {
-                    double rr, ri;
-                    herm<N>(B, m, k, rr, ri);
-                    ar = mad(ur[m], rr, mad(-ui[m], ri, ar));
-                    ai = mad(ur[m], ri, mad(ui[m], rr, ai));
-                }
-            }
-            tr[k] = ar;
-            ti[k] = ai;
-        }
-#pragma unroll kRollU
-        for (int j = i; j < N; ++j) {
-            double ar = 0.0, ai = 0.0;
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-                const double vr = k == j ? G.r(j, k) - 1.0 : G.r(j, k), vi = G.m(j, k);  // conj(U_jk) = vr - i vi
-                ar = mad(tr[k], vr, mad(ti[k], vi, ar));
-                ai = mad(ti[k], vr, mad(-tr[k], vi, ai));
-            }
-            if (j == i) {
-                raw[i] = ar;  // raw diagonal; relaxed below (A keeps the old one until then)
-            } else {
-                const double c = q.coh[i * N + j];
-                const double fr = ar * c, fi = ai * c;
-                const int p = pair_index(N, i, j);
-                acc_p += 2.0 * mad(q.pol.pol_im[p], fi - A[N + 2 * p + 1], q.pol.pol_re[p] * (fr - A[N + 2 * p]));
-                A[N + 2 * p] = fr;
-                A[N + 2 * p + 1] = fi;
-            }
-        }
-    }
-    double nd[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        double acc = q.pop[i * N] * raw[0];
-#pragma unroll
-        for (int j = 1; j < N; ++j) acc = mad(q.pop[i * N + j], raw[j], acc);
-        nd[i] = acc;
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        acc_p = mad(q.pol.pol_dv[i], nd[i] - A[i], acc_p);
-        A[i] = nd[i];
-    }
-    return q.pol.pol_factor * acc_p;
-}
-
 // ---------------------------------------------------------------------------
 // splitting: A holds rho (in/out), B is scratch for r1, G scratch N x N complex
 template <int N, bool RA, class VA, class VB, class MG, class VR>
@@ -240,14 +116,18 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
             B[wim(N, i, j)] = A[wim(N, i, j)] * q.coh[i * N + j];
         }
 #ifndef MBG_SPLIT_FENCE
-#define MBG_SPLIT_FENCE 1
+#define MBG_SPLIT_FENCE (N >= 7 ? 3 : 1)
 #endif
     // compiler fences (bit 0 here, bit 1 per congruence row): the state words
     // are re-read from shared memory where used again instead of being held
     // (spilled) across the inversion.  Measured on cfg4: none 4.77e9, bit 0
     // 4.92e9 (1588 -> 324 spill bytes), bits 0+1 4.54e9 (120 spill bytes),
-    // bit 1 alone 4.54e9 -- the per-row fence costs more schedule freedom than
-    // the spills it removes
+    // bit 1 alone 4.54e9 -- at six levels the per-row fence costs more
+    // schedule freedom than the spills it removes.  At seven and eight levels
+    // (G alone is 98 / 128 registers) it is the other way round: the shared
+    // memory of the resident CTAs leaves no L1 for local memory, every spill
+    // access runs at L2 latency, and the row fence cuts the spills from 8.7 KB
+    // to 0.7 KB (N = 7: 1.35e9 -> 2.57e9) and from 48 KB to 4.4 KB (N = 8)
     if constexpr ((MBG_SPLIT_FENCE & 1) != 0) asm volatile("" ::: "memory");
     if constexpr (RA) {
         // Real Hamiltonian and dipole (fast variant): A real symmetric, so
@@ -311,7 +191,6 @@ __device__ __forceinline__ double split_cell(const DenseQm<N> &q, double e, VA &
     } else {
         // G = (B/2)^-1 = 2 (I + iA)^-1: the host halves bc and bf (exact), so the
         // Gauss-Jordan inverse (in place, no pivoting) is already 2(I + iA)^-1
-        if constexpr (MG::kShared) return split_rolled<N>(q, e, A, B, G, raw);
 #pragma unroll
         for (int i = 0; i < N * N; ++i) {
             G.r(i / N, i % N) = mad(e, q.bf_re[i], q.bc_re[i]);
@@ -634,20 +513,14 @@ template <int N, bool RK4>
 struct Layout {
     static constexpr int NW = N * N;
     static constexpr bool kRegState = RK4 ? (N <= 3) : (N <= 4);
-#ifndef MBG_REG_G_MAX
-#define MBG_REG_G_MAX 7
-#endif
-    static constexpr bool kRegG = N <= MBG_REG_G_MAX;
-    // smem words per thread: A/B (or A/S/K/Acc for RK4) when not in registers, G when not in regs
-    // shared-memory G (N >= 7): the rolled step holds r1 in registers, so only rho is in shared memory
-    static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 3 * NW : (kRegG ? 2 * NW : NW));
-    static constexpr int kGWords = (RK4 || kRegG) ? 0 : 2 * NW;
+    // smem words per thread: A/B (or A/K/Acc for RK4) when not in registers; G is always in registers
+    static constexpr int kStateWords = kRegState ? 0 : (RK4 ? 3 * NW : 2 * NW);
     // shared-memory splitting: the congruence's raw diagonal in shared memory too
     static constexpr int kRawWords = (RK4 || kRegState) ? 0 : N;
     static constexpr int kFieldWords = 6;  // Es[2], Hs[2], Ho[2]
     static constexpr int TW = tile_width<N, RK4>();
     static constexpr size_t smem_bytes() {
-        return sizeof(double) * TW * (kFieldWords + kStateWords + kGWords + kRawWords);
+        return sizeof(double) * TW * (kFieldWords + kStateWords + kRawWords);
     }
 };
 
@@ -669,14 +542,9 @@ __device__ __forceinline__ double cell_step(const Q &q, double e, double *col, R
             RegMat<N> G;
             RegVec<N> raw;
             return split_cell<N, RA>(q, e, A, B, G, raw);
-        } else if constexpr (Lay::kRegG) {
+        } else {
             SmemVec<TW> As{col}, B{col + NW * TW}, raw{col + 2 * NW * TW};
             RegMat<N> G;
-            return split_cell<N, RA>(q, e, As, B, G, raw);
-        } else {
-            SmemVec<TW> As{col}, raw{col + 3 * NW * TW};
-            RegVec<NW> B;
-            SmemMat<N, TW> G{{col + NW * TW}, {col + 2 * NW * TW}};
             return split_cell<N, RA>(q, e, As, B, G, raw);
         }
     }
