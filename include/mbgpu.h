@@ -242,6 +242,13 @@ int mbg_checkpoint_restore(mbg_solver *s);
 /* measured FP64 FMA throughput of the device (TFLOP/s), the FP64 roofline
  * denominator: independent DFMA chains on every SM, timed with CUDA events */
 int mbg_fp64_peak(int device, double *tflops);
+/* the same measurement by operand pattern: mode 1 = two registers and a
+ * uniform addend (the pipe's peak: what mbg_fp64_peak measures), 0 = multiplier
+ * and addend registers shared by every instruction, 2 = one multiplier register
+ * shared by consecutive DFMAs (operand reuse cache), 3 = three distinct register
+ * operands per DFMA (matrix arithmetic with every operand fresh: limited by the
+ * register file's operand bandwidth) */
+int mbg_fp64_peak_operands(int device, int32_t mode, double *tflops);
 /* the same DFMA chains back to back for at least `seconds` (sustained clocks
  * and power): the denominator for kernels timed inside a long run */
 int mbg_fp64_peak_sustained(int device, double seconds, double *tflops);

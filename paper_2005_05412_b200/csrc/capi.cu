@@ -1554,6 +1554,16 @@ int mbg_fp64_peak_sustained(int device, double seconds, double *tflops) {
     return MBG_OK;
 }
 
+int mbg_fp64_peak_operands(int device, int32_t mode, double *tflops) {
+    mbg_solver *s = nullptr;
+    if (!tflops || mode < 0 || mode > 3) return MBG_E_ARG;
+    CK(cudaSetDevice(device));
+    double ms = 0.0, flops = 0.0;
+    CK(measure_fp64_peak_operands(mode, &ms, &flops));
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return MBG_OK;
+}
+
 int mbg_fp64_peak(int device, double *tflops) {
     mbg_solver *s = nullptr;
     if (!tflops) return MBG_E_ARG;

@@ -140,5 +140,8 @@ cudaError_t launch_invariants(const Launch &L, int levels, int bloch, const Bloc
 // FP64 roofline denominator: best-of-5 DFMA throughput (ms of the best launch, flops per launch)
 cudaError_t measure_fp64_peak(double *ms, double *flops);
 cudaError_t measure_fp64_sustained(double seconds, double *ms, double *flops);
+// the same chains by operand pattern: mode 3 three distinct register operands per
+// DFMA, 2 a multiplier register shared by consecutive DFMAs, 1 a uniform addend
+cudaError_t measure_fp64_peak_operands(int mode, double *ms, double *flops);
 
 }  // namespace mbg

@@ -100,6 +100,7 @@ SIGNATURES = {
     "mbg_checkpoint_save": (C.c_int, [_h]),
     "mbg_checkpoint_restore": (C.c_int, [_h]),
     "mbg_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "mbg_fp64_peak_operands": (C.c_int, [C.c_int, C.c_int32, C.POINTER(C.c_double)]),
     "mbg_fp64_peak_sustained": (C.c_int, [C.c_int, C.c_double, C.POINTER(C.c_double)]),
     "mbg_event_begin": (C.c_int, [_h]),
     "mbg_event_end": (C.c_int, [_h, C.POINTER(C.c_float)]),

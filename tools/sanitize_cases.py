@@ -32,3 +32,10 @@ build, stepper = CASES["multi_material"]
 dev, sce = build(mb)
 slabs.run_slabs_local(gpu.GpuFdtdSolver(dev, sce, stepper=stepper), 3)
 print("ok slabs", flush=True)
+# peer-mailbox exchange (push / pull kernels), with and without edge strips
+for case, count, overlap in (("multi_material", 3, False), ("rand6_split", 3, True)):
+    mb.clear_material_library()
+    build, stepper = CASES[case]
+    dev, sce = build(mb)
+    slabs.run_slabs_local(gpu.GpuFdtdSolver(dev, sce, stepper=stepper), count, overlap=overlap, exchange="p2p")
+    print("ok slabs p2p", case, flush=True)
