@@ -509,7 +509,8 @@ class PeerTransport:
         self.device = torch.device(device)
         self.plan = exchange_plan(state.slab)
         sl, rl, sr, rr = self.plan
-        idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.cuda = self.device.type == "cuda"  # (tests drive the protocol with host mailboxes on CPU)
+        idx = self.device.index if self.device.index is not None else (torch.cuda.current_device() if self.cuda else 0)
         w = state.words
         self.box = {side: Mailbox(idx, w * spec[1]) for side, spec in (("left", rl), ("right", rr))
                     if spec is not None}
@@ -547,8 +548,9 @@ class PeerTransport:
     def finish(self):
         _, rl, _, rr = self.plan
         if self.host_ordered:
-            self.torch.cuda.synchronize(self.device)  # this rank's pushes have landed ...
-            self.dist.barrier()                       # ... and so have everyone else's
+            if self.cuda:
+                self.torch.cuda.synchronize(self.device)  # this rank's pushes have landed ...
+            self.dist.barrier()                           # ... and so have everyone else's
         for side, spec in (("left", rl), ("right", rr)):
             if spec is not None:
                 b = self.box[side]
@@ -560,7 +562,8 @@ class PeerTransport:
         self.finish()
 
     def close(self):
-        self.torch.cuda.synchronize(self.device)
+        if self.cuda:
+            self.torch.cuda.synchronize(self.device)
         for b in self.peer.values():
             b.close()
         self.peer = {}
@@ -768,14 +771,16 @@ def overlaps_by_default(solver, backend: str) -> bool:
     return dense and backend == "nccl"
 
 
-def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None, overlap=None):
+def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=None, period=None, overlap=None,
+                  transport=None):
     """This process's slab of a ``world``-way run (torch.distributed initialised).
     Returns the assembled records on rank 0 and None elsewhere.
 
     ``state_factory(solver, slab)`` replaces the native slab (tests drive the
     same host logic with a CPU slab stepper under gloo).  ``overlap``: send
     the edge strips' cells while the slab advances (default: N-level / RK4
-    under NCCL, see :func:`overlaps_by_default`)."""
+    under NCCL, see :func:`overlaps_by_default`).  ``transport(state, device,
+    side_stream)`` replaces :func:`make_transport` (tests)."""
     import torch
     import torch.distributed as dist
 
@@ -800,7 +805,7 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     strips = None
     try:
         with torch.cuda.stream(stream) if stream is not None else _nullcontext():
-            tr = make_transport(st, device, side_stream=side)
+            tr = (transport or make_transport)(st, device, side_stream=side)
             if overlap:
                 strips = EdgeStrips(st, period, side)
             st.sample(0)

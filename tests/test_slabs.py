@@ -103,6 +103,135 @@ def test_gloo_ranks_match_oracle_bitwise(world, k, period, case):
             assert np.array_equal(have, want), (p.record.name, np.max(np.abs(have - want)))
 
 
+def _peer_worker(rank, world, port, case, k, period, out_path, box_dir):
+    """One gloo rank driving slabs.PeerTransport itself (handle exchange, which
+    box a side's push lands in, slot and sequence numbers, close order) with
+    host stand-ins for the device pieces: mailboxes are files mapped by both
+    neighbours, the push / pull 'kernels' are numpy copies with the flag
+    protocol of halo_push_kernel / halo_pull_kernel."""
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import time
+
+    import torch
+    import torch.distributed as dist
+    from np_slab import NumpySlab
+
+    import paper_2005_05412_b200 as gpu
+
+    from paper_2005_05412_b200.reference import mblight as mbw
+    from paper_2005_05412_b200 import slabs as sl
+
+    class FileMailbox:
+        HEADER = 128
+        count = 0
+
+        def __init__(self, device, doubles, ipc=None):
+            self.doubles, self.owned = int(doubles), ipc is None
+            if self.owned:
+                FileMailbox.count += 1
+                path = os.path.join(box_dir, f"box_{rank}_{FileMailbox.count}.bin")
+                np.zeros(self.HEADER // 8 + 2 * self.doubles).tofile(path)
+                self.ipc = path.encode()
+            else:
+                self.ipc = ipc
+            self.mem = np.memmap(self.ipc.decode(), dtype=np.float64, mode="r+")
+
+        def flag(self, slot):
+            return (self.mem, slot)  # flag words at the head of the box
+
+        def slot(self, slot):
+            o = self.HEADER // 8 + slot * self.doubles
+            return (self.mem, o)
+
+        def close(self):
+            self.mem.flush()
+
+    class Handle:
+        def __init__(self, slab):
+            self.slab, self.calls = slab, []
+
+        def call(self, name, cell0, count, slot, flag, seq, timeout_ms=None):
+            self.calls.append((name, cell0, count, slot[1], flag[1], seq))
+            mem, o = slot
+            fmem, fo = flag
+            n = self.slab.words * count
+            if name == "mbg_push_halo":
+                mem[o:o + n] = self.slab._pack(cell0, count)
+                mem.flush()
+                fmem.view(np.uint64)[fo] = seq  # published after the data
+                fmem.flush()
+            else:
+                assert name == "mbg_pull_halo"
+                t0 = time.time()
+                while fmem.view(np.uint64)[fo] < seq:
+                    assert time.time() - t0 < timeout_ms / 1e3, "strip did not arrive"
+                    time.sleep(0.0005)
+                self.slab.unpack_from(cell0, count, torch.from_numpy(np.array(mem[o:o + n])))
+
+    class PeerSlab:  # the twin behind the attributes PeerTransport uses (state.h is the native handle there)
+        def __init__(self, solver, slab):
+            self.twin = NumpySlab(solver, slab)
+            self.slab, self.words = slab, self.twin.words
+            self.h = Handle(self.twin)
+
+        def __getattr__(self, name):
+            return getattr(self.twin, name)
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cases import CASES
+
+        sl.Mailbox = FileMailbox
+        build, stepper = CASES[case]
+        mbw.clear_material_library()
+        dev, sce = build(mbw)
+        solver = gpu.GpuFdtdSolver(dev, sce, stepper=stepper)
+        made = []
+
+        def transport(state, device, side_stream=None):
+            made.append(sl.PeerTransport(state, device, side_stream=side_stream))
+            return made[0]
+
+        recs = sl.run_slab_rank(solver, world, rank, "cpu", state_factory=PeerSlab, k=k, period=period,
+                                transport=transport)
+        tr = made[0]
+        calls = tr.state.h.calls
+        # every exchange: pushes first (both sides), then the pulls, same sequence number, slot = seq & 1
+        per = (2 if 0 < rank < world - 1 else 1) * 2
+        assert len(calls) == tr.seq * per and tr.seq > 2
+        for e in range(tr.seq):
+            chunk = calls[e * per:(e + 1) * per]
+            assert [c[0] for c in chunk] == ["mbg_push_halo"] * (per // 2) + ["mbg_pull_halo"] * (per // 2)
+            assert all(c[5] == e + 1 and c[4] == (e + 1) & 1 for c in chunk)
+        if rank == 0:
+            np.savez(out_path, *recs)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,period,case", [(3, 16, 16, "multi_material"), (2, 4, 12, "rand3_split")])
+def test_peer_transport_protocol_between_gloo_ranks(world, k, period, case):
+    """slabs.PeerTransport across processes on CPU: its own host logic with
+    file-backed mailboxes and numpy push / pull, bit-identical to the oracle."""
+    import oracle as orc
+
+    dev, sce, stepper = build_case(case)
+    plan = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).plan
+    ref, bad = orc.run_oracle(plan)
+    assert bad == 0
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "recs.npz")
+        mp.spawn(_peer_worker, args=(world, _free_port(), case, k, period, out, d), nprocs=world, join=True)
+        got = np.load(out)
+        for r, (p, want) in enumerate(zip(plan.plans, ref)):
+            have = got[f"arr_{r}"]
+            assert have.shape == want.shape, p.record.name
+            assert np.array_equal(have, want), (p.record.name, np.max(np.abs(have - want)))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("case,count,period", [("sit_hard_whole", 2, None), ("sit_hard_whole", 5, None),
                                                ("multi_material", 3, None), ("multi_material", 2, 64),
