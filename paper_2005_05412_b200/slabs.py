@@ -34,6 +34,7 @@ Transports:
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from contextlib import nullcontext as _nullcontext
 from dataclasses import dataclass
 
@@ -96,11 +97,16 @@ def exchange_plan(slab: Slab):
 class SlabState:
     """One slab on one device: the native handle plus its geometry."""
 
-    def __init__(self, solver, slab: Slab, stream: int = 0, records: bool = True):
+    def __init__(self, solver, slab: Slab, stream: int = 0, records: bool = True, stream_sources: bool = False):
+        """``stream_sources``: the source samples (``Source.value`` per step, as
+        the reference's loop calls it) are taken period by period while the
+        device steps, as in ``GpuFdtdSolver.run`` -- for the one slab of a
+        solver that steps alone (one rank per process, no edge strips)."""
         self.solver = solver
         self.slab = slab
         self.h = solver.open_handle(win=(slab.win_lo, slab.win_hi), own=(slab.own_lo, slab.own_hi),
-                                    records=records)
+                                    records=records, stream_sources=stream_sources)
+        self.streaming = stream_sources and solver._fed < solver.grid.num_t
         if stream:
             self.h.call("mbg_set_stream", stream)
         solver.upload_initial_state(self.h, win=(slab.win_lo, slab.win_hi))
@@ -112,6 +118,9 @@ class SlabState:
         self.h.call("mbg_sample", step)
 
     def advance(self, first, count):
+        if self.streaming:  # rows of this period, queued stream-ordered before its launch
+            self.solver.plan.sample_sources(first + count)
+            self.solver._feed_sources(self.h, first + count)
         self.h.call("mbg_advance", first, count)
 
     def pack(self, cell0, count, ptr):
@@ -512,19 +521,29 @@ class PeerTransport:
         self.cuda = self.device.type == "cuda"  # (tests drive the protocol with host mailboxes on CPU)
         idx = self.device.index if self.device.index is not None else (torch.cuda.current_device() if self.cuda else 0)
         w = state.words
-        self.box = {side: Mailbox(idx, w * spec[1]) for side, spec in (("left", rl), ("right", rr))
-                    if spec is not None}
-        mine = {side: (b.ipc, b.doubles) for side, b in self.box.items()}
+        self.box, self.peer = {}, {}
+        try:  # a rank that cannot allocate still takes part in the gather (no rank may skip a collective)
+            self.box = {side: Mailbox(idx, w * spec[1]) for side, spec in (("left", rl), ("right", rr))
+                        if spec is not None}
+            mine = {side: (b.ipc, b.doubles) for side, b in self.box.items()}
+        except native.NativeError:
+            mine = None
         every = [None] * dist.get_world_size()
         dist.all_gather_object(every, mine)
+        if any(e is None for e in every):  # the same verdict on every rank
+            self.close(abort=True)
+            raise native.NativeError("a rank could not allocate its peer mailboxes")
         rank = state.slab.rank
-        self.peer = {}
-        if sl is not None:  # what I send left lands in the left neighbour's right box
-            ipc, doubles = every[rank - 1]["right"]
-            self.peer["left"] = Mailbox(idx, doubles, ipc=ipc)
-        if sr is not None:
-            ipc, doubles = every[rank + 1]["left"]
-            self.peer["right"] = Mailbox(idx, doubles, ipc=ipc)
+        try:
+            if sl is not None:  # what I send left lands in the left neighbour's right box
+                ipc, doubles = every[rank - 1]["right"]
+                self.peer["left"] = Mailbox(idx, doubles, ipc=ipc)
+            if sr is not None:
+                ipc, doubles = every[rank + 1]["left"]
+                self.peer["right"] = Mailbox(idx, doubles, ipc=ipc)
+        except native.NativeError:  # no IPC / peer access to that device: make_transport falls back on every rank
+            self.close(abort=True)
+            raise
         self.seq = 0
 
     @property
@@ -561,13 +580,17 @@ class PeerTransport:
         self.start()
         self.finish()
 
-    def close(self):
+    def close(self, abort: bool = False):
+        """Unmap the neighbours' boxes, then -- once every rank has -- free this
+        rank's own.  ``abort`` (an exception is propagating, or the ranks did
+        not all get their transport): no barrier, the run is over anyway."""
         if self.cuda:
             self.torch.cuda.synchronize(self.device)
         for b in self.peer.values():
             b.close()
         self.peer = {}
-        self.dist.barrier()  # nobody still maps a box when its owner frees it
+        if not abort:
+            self.dist.barrier()  # nobody still maps a box when its owner frees it
         for b in self.box.values():
             b.close()
         self.box = {}
@@ -605,7 +628,7 @@ def make_transport(state: SlabState, device, side_stream=None):
         if ok:
             return tr
         if tr is not None:
-            tr.close()
+            tr.close(abort=True)  # some rank has no transport: it would never reach a barrier
         warnings.warn(f"peer mailboxes unavailable ({err}); ghost exchange by send/recv")
     return TorchTransport(state, device, side_stream=side_stream)
 
@@ -799,7 +822,7 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
     stream = torch.cuda.Stream(device) if state_factory is None else None
     side = torch.cuda.Stream(device, priority=-1) if overlap else None
     if state_factory is None:
-        st = SlabState(solver, slabs[rank], stream=stream.cuda_stream)
+        st = SlabState(solver, slabs[rank], stream=stream.cuda_stream, stream_sources=not overlap)
     else:
         st = state_factory(solver, slabs[rank])
     strips = None
@@ -831,7 +854,7 @@ def run_slab_rank(solver, world: int, rank: int, device, state_factory=None, k=N
         if strips is not None:
             strips.close()
         if hasattr(locals().get("tr"), "close"):
-            tr.close()
+            tr.close(abort=sys.exc_info()[0] is not None)
         st.close()
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(mine, gathered, dst=0)
