@@ -532,3 +532,26 @@ def test_monitor_without_quantum_media_keeps_the_initial_report():
     s.run()
     assert s.invariant_report == ref.invariant_report == {"max_trace_dev": 0.0, "max_herm_dev": 0.0,
                                                           "min_eigenvalue": math.inf}
+
+
+@pytest.mark.gpu
+def test_fp64_operand_probes_order_as_the_register_file_model_says():
+    """bench.py's roofline denominators: DFMAs with a uniform operand reach the
+    pipe's peak, three distinct register operands cost three register-file
+    cycles per instruction (about 2/3 of it), a shared multiplier lies between."""
+    import ctypes as C
+
+    from paper_2005_05412_b200 import native
+
+    lib = native.load()
+    rate = {}
+    for mode in (1, 2, 3):
+        v = C.c_double(0)
+        assert lib.mbg_fp64_peak_operands(0, mode, C.byref(v)) == 0
+        rate[mode] = v.value
+    peak = C.c_double(0)
+    assert lib.mbg_fp64_peak(0, C.byref(peak)) == 0
+    assert 20.0 < rate[3] < rate[2] < rate[1] < 45.0
+    assert abs(peak.value - rate[1]) < 0.05 * rate[1]
+    assert 0.6 < rate[3] / rate[1] < 0.75
+    assert lib.mbg_fp64_peak_operands(0, 7, C.byref(peak)) != 0  # unknown pattern
