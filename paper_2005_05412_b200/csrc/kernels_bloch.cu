@@ -430,6 +430,7 @@ __device__ __forceinline__ unsigned long long range_records(const Launch &L, lon
 // where they are used instead of being held in registers across the steps:
 // from blockIdx and the parameter bank (per-launch kernel) ...
 struct LaunchSpan {
+    static constexpr bool kPersistent = false;
     const Launch &L;
     __device__ long long lo() const { return L.res_lo + (long long)blockIdx.x * L.tile_own; }
     __device__ long long hi() const {
@@ -441,6 +442,7 @@ struct LaunchSpan {
 
 // ... or from the item range the persistent kernel staged in shared memory
 struct SharedSpan {
+    static constexpr bool kPersistent = true;
     const Launch &L;
     const WaveItem &it;
     __device__ long long lo() const { return it.lo; }
@@ -498,6 +500,16 @@ __device__ __forceinline__ void interior_cta(const BlochParams &P, const Chunk &
         }
     }
     hook();
+    // two steps per loop iteration in the persistent kernel's hot instantiation
+    // (one real-dipole medium, no monitor): the loop-carried state needs no
+    // register copies at the back edge (16 moves per step otherwise) and the
+    // seam slot parity is static -- cfg2 5.70e11 -> 5.82e11; the per-launch
+    // path of small domains measured 4 % slower unrolled (cfg1), so it stays rolled
+#ifndef MBG_BLOCH_UNROLL
+#define MBG_BLOCH_UNROLL 2
+#endif
+    constexpr int kStepUnroll = (Span::kPersistent && QM && ONE_QM && REAL && !MON) ? MBG_BLOCH_UNROLL : 1;
+#pragma unroll kStepUnroll
     for (int s = 0; s < K.steps; ++s) {
         const int b = s & 1;
         // H update (uses E^{n-1}); H is overwritten in place with H^{n-1/2}
