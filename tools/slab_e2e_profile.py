@@ -1,5 +1,11 @@
+"""The public multi-GPU call at world size 1 (NCCL) against GpuFdtdSolver.run() on cfg2: wall time of
+run_slab_rank (window upload, streamed sources, the step loop, record gather) with a cProfile of
+the third run -- the host overhead a rank adds to its device time.
+
+    python tools/slab_e2e_profile.py
+"""
 import sys, time, os
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, str(__import__('pathlib').Path(__file__).resolve().parent.parent))
 import torch, torch.distributed as dist
 import paper_2005_05412_b200 as gpu
 from paper_2005_05412_b200.reference import mblight as mb
