@@ -45,6 +45,16 @@ def test_partition_rejects_thin_slabs():
         slabs.partition(20, 4, 8)
 
 
+def test_exchange_mode_defaults_and_switch(monkeypatch):
+    monkeypatch.delenv("MBG_SLAB_EXCHANGE", raising=False)
+    assert slabs.exchange_mode("nccl") == "p2p" and slabs.exchange_mode("gloo") == "nccl"
+    monkeypatch.setenv("MBG_SLAB_EXCHANGE", "nccl")
+    assert slabs.exchange_mode("nccl") == "nccl"
+    monkeypatch.setenv("MBG_SLAB_EXCHANGE", "shmem")
+    with pytest.raises(ValueError):
+        slabs.exchange_mode("nccl")
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
