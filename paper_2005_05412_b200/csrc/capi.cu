@@ -940,6 +940,12 @@ bool wave_worthwhile(const mbg_solver *s, int tw) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->g.device) != cudaSuccess || sms <= 0)
         sms = 148;
     const long long tiles = s->win_n / std::max(1, tw - 2 * s->k);
+    // edge ranges are one-cell-per-thread CTA items of kBlochTile - 2k cells and
+    // every item must span >= k cells (dependencies j-1 .. j+1): beyond
+    // k = kBlochTile / 3 they would be merged into ranges stepped by single
+    // warps, a serial chain through the wavefront (k = 96: 951 ms against
+    // 157 ms for one launch per chunk on cfg2) -- such depths go per launch
+    if (kBlochTile - 2 * s->k < s->k) return false;
     return tiles >= sms;
 }
 
