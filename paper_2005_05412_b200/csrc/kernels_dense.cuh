@@ -842,8 +842,8 @@ __device__ __forceinline__ void dense_dispatch(const DenseParams<N, Q> &P, doubl
     }
 }
 
-template <int N, bool RK4, class Q>
-__global__ void __launch_bounds__(Layout<N, RK4>::TW, dense_min_blocks(N, RK4)) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
+template <int N, bool RK4, class Q, int MINB>
+__global__ void __launch_bounds__(Layout<N, RK4>::TW, MINB) dense_step_kernel(const __grid_constant__ DenseParams<N, Q> P) {
     using Lay = Layout<N, RK4>;
     extern __shared__ double sm[];
     const Launch &L = P.L;

@@ -10,23 +10,36 @@ namespace mbg {
 namespace MBG_VARIANT {
 namespace dense {
 
-template <int N, bool RK4, class Q>
-static cudaError_t launch_n(const void *params, long long tiles, cudaStream_t st) {
-    static_assert(sizeof(DenseParams<N, Q>) <= 32764, "kernel parameter block over the 32 KB launch limit");
-    const auto &P = *static_cast<const DenseParams<N, Q> *>(params);
+template <int N, bool RK4, class Q, int MINB>
+static cudaError_t launch_variant(const DenseParams<N, Q> &P, long long tiles, int dev, cudaStream_t st) {
     constexpr size_t smem = Layout<N, RK4>::smem_bytes();
     static bool configured[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     if (!configured[dev]) {
-        cudaError_t err = cudaFuncSetAttribute(dense_step_kernel<N, RK4, Q>,
+        cudaError_t err = cudaFuncSetAttribute(dense_step_kernel<N, RK4, Q, MINB>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
         configured[dev] = true;
     }
-    dense_step_kernel<N, RK4, Q><<<(unsigned)tiles, Layout<N, RK4>::TW, smem, st>>>(P);
+    dense_step_kernel<N, RK4, Q, MINB><<<(unsigned)tiles, Layout<N, RK4>::TW, smem, st>>>(P);
     return cudaGetLastError();
+}
+
+template <int N, bool RK4, class Q>
+static cudaError_t launch_n(const void *params, long long tiles, cudaStream_t st) {
+    static_assert(sizeof(DenseParams<N, Q>) <= 32764, "kernel parameter block over the 32 KB launch limit");
+    const auto &P = *static_cast<const DenseParams<N, Q> *>(params);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    constexpr int kSmall = dense_min_blocks(N, RK4), kLarge = dense_min_blocks_large(N, RK4);
+    if constexpr (kSmall != kLarge) {
+        // the occupancy variant once the grid gives every CTA slot two tiles
+        static int sms[64] = {};
+        if (!sms[dev] && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms[dev] = 148;
+        if (tiles >= 2LL * kLarge * sms[dev]) return launch_variant<N, RK4, Q, kLarge>(P, tiles, dev, st);
+    }
+    return launch_variant<N, RK4, Q, kSmall>(P, tiles, dev, st);
 }
 
 template <int N, bool RK4, class Q>

@@ -58,6 +58,17 @@ __host__ __device__ constexpr int dense_min_blocks(int n, bool rk4) {
 #endif
     return n <= 3 ? 2 : 1;
 }
+// Four- and five-level splitting on large grids (at least two tiles per SM
+// slot): a second instantiation with three CTAs per SM (168 registers, 12
+// warps) beats two CTAs at 234 / 255 registers -- N = 4 1.58e10 -> 1.69e10
+// (real media 1.89e10 -> 2.11e10), N = 5 8.05e9 -> 8.54e9 (1.009e10 ->
+// 1.053e10); four CTAs at 128 registers spill and lose (N = 4: 1.55e10).
+// Small domains (every tile on its own SM, e.g. the paper's QCL setups) are
+// bound by one tile's latency and keep the spill-free variant (the
+// three-CTA one: tzenov2016 0.76 -> 0.88 s).
+__host__ __device__ constexpr int dense_min_blocks_large(int n, bool rk4) {
+    return ((n == 4 || n == 5) && !rk4) ? 3 : dense_min_blocks(n, rk4);
+}
 
 // One persistent launch of the two-level kernel over many fused chunks
 // (non-windowed solvers): work items (chunk c, tile t) are claimed in
