@@ -332,6 +332,30 @@ def test_pull_without_a_push_times_out_and_is_reported():
         box.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim", [4, 5])
+def test_occupancy_and_latency_instantiations_agree_bitwise(dim):
+    """Four- and five-level splitting has two instantiations (three CTAs per SM
+    from 888 tiles per launch on, the spill-free build below): a 2^17-cell
+    single domain (1093 tiles) against the same run as two slabs (547 tiles
+    each) and their edge strips (one tile): identical bits."""
+    from cases import random_case
+
+    nx = 1 << 17
+    dt = 0.5 * (20e-6 / nx) / 299792458.0
+    build, stepper = random_case(dim, 30 + dim, nx=nx, end=40.5 * dt, whole=True)  # every step, whole domain
+    mb.clear_material_library()
+    dev, sce = build(mb)
+    ref = gpu.GpuFdtdSolver(dev, sce, stepper=stepper).run()
+    for overlap in (False, True):
+        mb.clear_material_library()
+        dev, sce = build(mb)
+        got = slabs.run_slabs_local(gpu.GpuFdtdSolver(dev, sce, stepper=stepper), 2, overlap=overlap)
+        for a, b in zip(ref, got):
+            assert a.data.shape == b.data.shape
+            assert np.array_equal(a.data.view(np.float64), b.data.view(np.float64)), (a.name, overlap)
+
+
 def _nccl_single(fn):
     """Run fn() inside a one-rank NCCL process group (the only NCCL shape one GPU allows)."""
     import torch
